@@ -1,0 +1,131 @@
+/*
+ * gfrlnc.h -- C ABI of the B200-native (sm_100a) GF(2^w) region multiply-add
+ * and RLNC encoder: the hot path of arXiv 1909.02871 (Guenther, Appel, Carle,
+ * "Galois Field Arithmetics for Linear Network Coding using AVX 512
+ * Instruction Set Extensions").  Citations "PAPER.md:L" are lines of the
+ * paper's LaTeX source; readings "Xn" are listed in DESIGN.md.
+ *
+ * Conventions shared by every entry point
+ *   field   one of 2, 4, 16, 256: F_q with q = 2^w, w in {1,2,4,8}
+ *           (Sec. II).  Reduction polynomials x^2+x+1,
+ *           x^4+x+1, x^8+x^4+x^3+x+1 (0x11B) (reading X1).
+ *   bytes   regions are byte arrays; a byte packs 8/w words, word j at bits
+ *           [j*w, (j+1)*w) (reading X4).  Sizes (`bytes`, `M`)
+ *           count BYTES, not words: paper M = bytes * 8 / w (reading X10).
+ *   memory  every buffer pointer is a CUDA device pointer valid on the current
+ *           device, unless the name ends in _host.  The caller owns all
+ *           buffers; the library keeps no pointer after a call returns.  Any
+ *           alignment and any length are accepted (reading X6).
+ *   streams work is enqueued asynchronously on the calling thread's stream
+ *           (gf_set_stream; default: the legacy default stream).  Calls that
+ *           write disjoint destinations may run concurrently.
+ *   errors  every entry point returns a status code (GF_OK == 0); nothing
+ *           throws across the ABI.  A size of zero returns GF_OK and launches
+ *           nothing.  GF_ECUDA reports a launch / runtime failure
+ *           (cudaGetLastError after the launch).
+ *   hot path  no allocation, no host synchronisation, no host<->device copy
+ *           inside gf_maddrc / gf_mulrc / gf_encode_batch.
+ */
+#ifndef GFRLNC_H
+#define GFRLNC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    GF_OK = 0,
+    GF_EFIELD = -1,    /* field not in {2, 4, 16, 256}                          */
+    GF_ECOEFF = -2,    /* coeff >= q in gf_maddrc / gf_mulrc                    */
+    GF_EARG = -3,      /* NULL pointer with nonzero size, N < 1, K < 1, overflow */
+    GF_EOVERLAP = -4,  /* partial overlap of dst/src, or B overlapping A or C   */
+    GF_ENOINIT = -5,   /* gf_init(field) not called on the current device       */
+    GF_ECUDA = -6      /* CUDA launch / runtime failure                          */
+};
+
+/* Build the per-coefficient split multiplication tables of F_q on the host
+ * and upload them to the CURRENT device (Alg. 1 tables tl/th,
+ * re-cut for the GPU into three byte-permute tables).
+ * Idempotent and thread-safe; call once per (device, field) before any other
+ * call for that field.  Returns GF_OK, GF_EFIELD or GF_ECUDA. */
+int gf_init(int field);
+
+/* Region multiply-add  dst[j] := dst[j] + coeff * src[j]  for j < bytes:
+ * the paper's "multiply and add (madd)" b := b + c_i a_i (PAPER.md:91-92,
+ * Sec. II; Alg. 1, Alg. 2).
+ *   coeff == 0 launches nothing, coeff == 1 runs the XOR kernel
+ *   (PAPER.md:205-211 trivial cases).  dst == src (exact aliasing) is allowed
+ *   and gives (1 + coeff) * src; any partial overlap returns GF_EOVERLAP.
+ * Returns GF_OK, GF_EFIELD, GF_ECOEFF, GF_EARG, GF_EOVERLAP, GF_ENOINIT,
+ * GF_ECUDA. */
+int gf_maddrc(int field, uint8_t *dst, const uint8_t *src, uint8_t coeff, size_t bytes);
+
+/* Region scaling  dst[j] := coeff * dst[j]  (SPEC mul_region; reading X19).
+ * coeff == 1 launches nothing; coeff == 0 zeroes the region. */
+int gf_mulrc(int field, uint8_t *dst, uint8_t coeff, size_t bytes);
+
+/* Batched RLNC encode, Eq. 2 over `batch` generations:
+ *     B[g][k][m] = sum_{i<N} C[g][i][k] * A[g][i][m]
+ * for g < batch, k < K, m < M (byte columns).  Layouts (row-major, packed):
+ *     A[batch][N][M]  source packets a_i of generation g (Eq. 1)
+ *     C[batch][N][K]  one coding vector c per coded packet, one byte per
+ *                     coefficient (readings X9, X11)
+ *     B[batch][K][M]  coded packets b, OVERWRITTEN (zero accumulator, X8).
+ * Entries of C are not validated on the hot path: a byte >= q is taken
+ * modulo q by masking with q-1 (the Python layer offers a checked mode).
+ * B must not overlap A or C (GF_EOVERLAP).  Returns GF_OK, GF_EFIELD,
+ * GF_EARG, GF_EOVERLAP, GF_ENOINIT, GF_ECUDA. */
+int gf_encode_batch(int field, const uint8_t *A, const uint8_t *C, uint8_t *B,
+                    int N, int K, size_t M, size_t batch);
+
+/* Same computation with HOST buffers (A_host, C_host read, B_host written):
+ * copies in, encodes and copies out in chunks of generations, overlapping
+ * host->device copies, kernels and device->host copies on three internal
+ * streams.  dev_ws / ws_bytes is a caller-owned device workspace; it must
+ * hold at least two chunks of one generation (2 * (N*M + N*K + K*M) bytes).
+ * Pinned host memory is strongly recommended.  BLOCKING: returns after B_host
+ * is complete (the caller's stream is not used).  Returns the codes of
+ * gf_encode_batch, or GF_EARG when the workspace is too small. */
+int gf_encode_batch_host(int field, const uint8_t *A_host, const uint8_t *C_host,
+                         uint8_t *B_host, int N, int K, size_t M, size_t batch,
+                         void *dev_ws, size_t ws_bytes);
+
+/* Set the calling thread's stream (a cudaStream_t; NULL = legacy default). */
+int gf_set_stream(void *cuda_stream);
+
+/* Static description of a status code; never NULL. */
+const char *gf_strerror(int status);
+
+/* ---- harness-only exports (not part of the paper's method) -------------- */
+
+/* Counter-based generator shared with seeded_inputs:
+ *   byte(seed, stream, j) = byte (j & 7) of
+ *       mix64((seed ^ stream * 0xD1B54A32D192ED03) + ((j >> 3) + 1) * 0x9E3779B97F4A7C15)
+ * gf_fill_random:   dst[j] = byte(seed, stream, offset + j) & mask, j < bytes
+ * gf_fill_random2d: dst[r*cols + c] = byte(seed, stream, base + r*row_stride + c) & mask
+ * mask = 0xFF for payload bytes, q-1 for coefficients uniform over F_q. */
+int gf_fill_random(uint8_t *dst, size_t bytes, uint64_t seed, uint64_t stream,
+                   uint64_t offset, uint8_t mask);
+int gf_fill_random2d(uint8_t *dst, size_t rows, size_t cols, uint64_t seed, uint64_t stream,
+                     uint64_t base, uint64_t row_stride, uint8_t mask);
+
+/* Host-only (no GPU needed): copy out the per-coefficient byte-permute tables
+ * gf_init uploads, so CPU tests can emulate the kernels' lookups.  Writes
+ * q * 8 uint32 words: for coefficient c, words [8c .. 8c+7] =
+ *   { T0[0..3], T0[4..7], T1[0..3], T1[4..7], T2[0..3], M0, M1, 0 }
+ * with Tg[v] = c * (v << 3g) (packed product, one byte per entry, little
+ * endian), and M0/M1 the all-ones masks of coefficient bits 0/1 (GF(2)/GF(4)
+ * bit-plane kernels).  Returns GF_OK, GF_EFIELD or GF_EARG (cap too small). */
+int gf_host_tables(int field, uint32_t *out, size_t cap_words);
+
+/* Library version (major * 10000 + minor * 100 + patch). */
+int gf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GFRLNC_H */

@@ -1,0 +1,428 @@
+// gfrlnc.cu -- the C ABI declared in include/gfrlnc.h: argument validation,
+// per-field kernel dispatch and launches on the calling thread's stream.
+// See the header for the contract of every entry point and DESIGN.md for the
+// kernels.  Compiled for sm_100a only.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/gfrlnc.h"
+#include "encode_kernels.cuh"
+#include "region_kernels.cuh"
+#include "rng_kernels.cuh"
+#include "tables.h"
+
+namespace gfr {
+
+constexpr int kMaxDevices = 64;
+constexpr int kVersion = 100;   // 0.1.0
+
+__device__ uint32_t g_dev_tabs[4][256 * kTableWords];
+
+static uint32_t g_host_tabs[4][256 * kTableWords];
+static bool g_host_ready[4];
+static uint32_t g_dev_ready[kMaxDevices];     // bit f: field index f uploaded
+static int g_sm_count[kMaxDevices];
+static std::mutex g_lock;
+static thread_local cudaStream_t tls_stream = nullptr;
+
+static int field_index(int field)
+{
+    switch (field) {
+    case 2: return 0;
+    case 4: return 1;
+    case 16: return 2;
+    case 256: return 3;
+    default: return -1;
+    }
+}
+
+static int current_device(int *dev)
+{
+    if (cudaGetDevice(dev) != cudaSuccess || *dev < 0 || *dev >= kMaxDevices) return GF_ECUDA;
+    return GF_OK;
+}
+
+static int check_ready(int field, int *fi, int *dev)
+{
+    *fi = field_index(field);
+    if (*fi < 0) return GF_EFIELD;
+    if (current_device(dev) != GF_OK) return GF_ECUDA;
+    if (!(__atomic_load_n(&g_dev_ready[*dev], __ATOMIC_ACQUIRE) >> *fi & 1u)) return GF_ENOINIT;
+    return GF_OK;
+}
+
+static bool overlaps(const void *a, size_t na, const void *b, size_t nb)
+{
+    const uintptr_t x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+    return na && nb && x < y + nb && y < x + na;
+}
+
+static int launch_status()
+{
+    return cudaGetLastError() == cudaSuccess ? GF_OK : GF_ECUDA;
+}
+
+// ---------------------------------------------------------------- regions
+
+template <int OP>
+static int launch_region(int dev, uint8_t *dst, const uint8_t *src, size_t bytes,
+                         const RegionParams &p, cudaStream_t st)
+{
+    const size_t nvec = bytes / 16 + 1;
+    constexpr int kThreads = 256, kUnroll = 4;
+    size_t blocks = (nvec + (size_t)kThreads * kUnroll - 1) / ((size_t)kThreads * kUnroll);
+    const size_t cap = (size_t)(g_sm_count[dev] > 0 ? g_sm_count[dev] : 148) * 16;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    int mode = 0;
+    if (op_reads_src(OP)) {
+        if (src == dst) mode = 2;
+        else if (((reinterpret_cast<uintptr_t>(src) - reinterpret_cast<uintptr_t>(dst)) & 15u) != 0)
+            mode = 1;
+    }
+    if (mode == 0)
+        region_kernel<OP, 0, kUnroll><<<(unsigned)blocks, kThreads, 0, st>>>(dst, src, bytes, p);
+    else if (mode == 1)
+        region_kernel<OP, 1, kUnroll><<<(unsigned)blocks, kThreads, 0, st>>>(dst, src, bytes, p);
+    else
+        region_kernel<OP, 2, kUnroll><<<(unsigned)blocks, kThreads, 0, st>>>(dst, src, bytes, p);
+    return launch_status();
+}
+
+static RegionParams region_params(int fi, unsigned c)
+{
+    RegionParams p;
+    const uint32_t *t = g_host_tabs[fi] + (size_t)c * kTableWords;
+    p.tab.t0lo = t[0]; p.tab.t0hi = t[1]; p.tab.t1lo = t[2]; p.tab.t1hi = t[3]; p.tab.t2 = t[4];
+    p.m0 = t[5]; p.m1 = t[6];
+    return p;
+}
+
+// ---------------------------------------------------------------- encode
+
+static int pow2_at_least(int k)
+{
+    int t = 1;
+    while (t < k) t <<= 1;
+    return t;
+}
+
+template <int F, int W, int KT, bool BW>
+static int launch_encode_t(EncodeParams p, cudaStream_t st)
+{
+    const size_t spans = (p.Mw + 32u * W - 1) / (32u * W);
+    p.spans_per_gen = (int)spans;
+    int wpb;
+    if (spans <= 8) {
+        size_t gpc = 8 / spans;
+        if (gpc > p.batch) gpc = p.batch;
+        if (gpc < 1) gpc = 1;
+        p.gens_per_cta = (int)gpc;
+        p.ctas_per_gen = 1;
+        wpb = (int)(gpc * spans);
+    } else {
+        p.gens_per_cta = 1;
+        wpb = 8;
+        p.ctas_per_gen = (int)((spans + 7) / 8);
+    }
+    p.k_tiles = (p.K + KT - 1) / KT;
+    const size_t gen_groups = (p.batch + p.gens_per_cta - 1) / p.gens_per_cta;
+    const size_t grid = (size_t)p.k_tiles * gen_groups * (size_t)p.ctas_per_gen;
+    if (grid > 0x7FFFFFFFu) return GF_EARG;
+    const size_t smem = (size_t)p.gens_per_cta * enc_smem_bytes_per_gen<F, KT>();
+    if (smem > 48 * 1024) {
+        if (cudaFuncSetAttribute(encode_kernel<F, W, KT, BW>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return GF_ECUDA;
+    }
+    encode_kernel<F, W, KT, BW><<<(unsigned)grid, wpb * 32, smem, st>>>(p);
+    return launch_status();
+}
+
+template <int F, int W, int KTMAX, bool BW>
+static int launch_encode_kt(EncodeParams p, cudaStream_t st)
+{
+    int kt = pow2_at_least(p.K);
+    if (kt > KTMAX) kt = KTMAX;
+    switch (kt) {
+    case 1: return launch_encode_t<F, W, 1, BW>(p, st);
+    case 2: return launch_encode_t<F, W, 2, BW>(p, st);
+    case 4: return launch_encode_t<F, W, 4, BW>(p, st);
+    case 8: return launch_encode_t<F, W, 8, BW>(p, st);
+    case 16: return launch_encode_t<F, W, 16, BW>(p, st);
+    default:
+        if constexpr (KTMAX >= 32) return launch_encode_t<F, W, 32, BW>(p, st);
+        return GF_EARG;
+    }
+}
+
+template <bool BW>
+static int launch_encode_field(int field, EncodeParams p, cudaStream_t st)
+{
+    switch (field) {
+    case 256: return launch_encode_kt<256, 4, 16, BW>(p, st);
+    case 16: return launch_encode_kt<16, 4, 16, BW>(p, st);
+    case 4: return launch_encode_kt<4, 2, 32, BW>(p, st);
+    case 2: return launch_encode_kt<2, 2, 32, BW>(p, st);
+    default: return GF_EFIELD;
+    }
+}
+
+static int encode_on_stream(int field, int fi, const uint8_t *A, const uint8_t *C, uint8_t *B,
+                            int N, int K, size_t M, size_t batch, cudaStream_t st)
+{
+    EncodeParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.A = A; p.C = C; p.B = B;
+    void *tabs = nullptr;
+    if (cudaGetSymbolAddress(&tabs, g_dev_tabs) != cudaSuccess) return GF_ECUDA;
+    p.tabs = reinterpret_cast<const uint32_t *>(tabs) + (size_t)fi * 256 * kTableWords;
+    p.M = M; p.batch = batch; p.N = N; p.K = K; p.qmask = field - 1;
+    const bool bytewise = (M % 4) != 0 || (reinterpret_cast<uintptr_t>(A) & 3u) ||
+                          (reinterpret_cast<uintptr_t>(B) & 3u);
+    p.Mw = bytewise ? M : M / 4;
+    return bytewise ? launch_encode_field<true>(field, p, st) : launch_encode_field<false>(field, p, st);
+}
+
+static int validate_encode(int field, const uint8_t *A, const uint8_t *C, const uint8_t *B,
+                           int N, int K, size_t M, size_t batch, size_t *a_bytes, size_t *b_bytes,
+                           size_t *c_bytes)
+{
+    if (field_index(field) < 0) return GF_EFIELD;
+    if (N < 1 || K < 1) return GF_EARG;
+    size_t nm, km;
+    if (__builtin_mul_overflow((size_t)N, M, &nm) || __builtin_mul_overflow(nm, batch, a_bytes) ||
+        __builtin_mul_overflow((size_t)K, M, &km) || __builtin_mul_overflow(km, batch, b_bytes) ||
+        __builtin_mul_overflow((size_t)N * (size_t)K, batch, c_bytes) || *a_bytes > (SIZE_MAX >> 1) ||
+        *b_bytes > (SIZE_MAX >> 1))
+        return GF_EARG;
+    if (M == 0 || batch == 0) return GF_OK;
+    if (!A || !C || !B) return GF_EARG;
+    if (overlaps(B, *b_bytes, A, *a_bytes) || overlaps(B, *b_bytes, C, *c_bytes)) return GF_EOVERLAP;
+    return GF_OK;
+}
+
+// ------------------------------------------------------------ host pipeline
+
+struct HostPipe {
+    bool ready = false;
+    cudaStream_t s_h2d = nullptr, s_cmp = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_in[2], ev_cmp[2], ev_free[2];
+};
+static HostPipe g_pipes[kMaxDevices];
+
+static int pipe_for(int dev, HostPipe **out)
+{
+    std::lock_guard<std::mutex> g(g_lock);
+    HostPipe &P = g_pipes[dev];
+    if (!P.ready) {
+        if (cudaStreamCreateWithFlags(&P.s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&P.s_cmp, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&P.s_d2h, cudaStreamNonBlocking) != cudaSuccess)
+            return GF_ECUDA;
+        for (int b = 0; b < 2; b++)
+            if (cudaEventCreateWithFlags(&P.ev_in[b], cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&P.ev_cmp[b], cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&P.ev_free[b], cudaEventDisableTiming) != cudaSuccess)
+                return GF_ECUDA;
+        P.ready = true;
+    }
+    *out = &P;
+    return GF_OK;
+}
+
+}  // namespace gfr
+
+using namespace gfr;
+
+extern "C" {
+
+int gf_version(void) { return kVersion; }
+
+const char *gf_strerror(int status)
+{
+    switch (status) {
+    case GF_OK: return "ok";
+    case GF_EFIELD: return "unsupported field (expected 2, 4, 16 or 256)";
+    case GF_ECOEFF: return "coefficient >= field size";
+    case GF_EARG: return "invalid argument (NULL pointer, N/K < 1, size overflow or workspace too small)";
+    case GF_EOVERLAP: return "overlapping buffers";
+    case GF_ENOINIT: return "gf_init(field) not called on the current device";
+    case GF_ECUDA: return "CUDA launch or runtime failure";
+    default: return "unknown status";
+    }
+}
+
+int gf_set_stream(void *cuda_stream)
+{
+    tls_stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+    return GF_OK;
+}
+
+int gf_host_tables(int field, uint32_t *out, size_t cap_words)
+{
+    if (field_index(field) < 0) return GF_EFIELD;
+    if (!out) return GF_EARG;
+    const int rc = build_tables(field, out, cap_words);
+    return rc == 0 ? GF_OK : (rc == -1 ? GF_EFIELD : GF_EARG);
+}
+
+int gf_init(int field)
+{
+    const int fi = field_index(field);
+    if (fi < 0) return GF_EFIELD;
+    int dev;
+    if (current_device(&dev) != GF_OK) return GF_ECUDA;
+    std::lock_guard<std::mutex> g(g_lock);
+    if (!g_host_ready[fi]) {
+        std::memset(g_host_tabs[fi], 0, sizeof(g_host_tabs[fi]));
+        if (build_tables(field, g_host_tabs[fi], 256 * kTableWords) != 0) return GF_EFIELD;
+        g_host_ready[fi] = true;
+    }
+    if (!(g_dev_ready[dev] >> fi & 1u)) {
+        if (cudaMemcpyToSymbol(g_dev_tabs, g_host_tabs[fi], sizeof(g_host_tabs[fi]),
+                               (size_t)fi * sizeof(g_host_tabs[fi]), cudaMemcpyHostToDevice) != cudaSuccess)
+            return GF_ECUDA;
+        if (g_sm_count[dev] == 0) {
+            int sms = 0;
+            if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+                return GF_ECUDA;
+            g_sm_count[dev] = sms;
+        }
+        __atomic_or_fetch(&g_dev_ready[dev], 1u << fi, __ATOMIC_RELEASE);
+    }
+    return GF_OK;
+}
+
+int gf_maddrc(int field, uint8_t *dst, const uint8_t *src, uint8_t coeff, size_t bytes)
+{
+    int fi, dev;
+    const int rc = check_ready(field, &fi, &dev);
+    if (rc != GF_OK) return rc;
+    if (coeff >= (unsigned)field) return GF_ECOEFF;
+    if (bytes == 0) return GF_OK;
+    if (!dst || !src || bytes > (SIZE_MAX >> 1)) return GF_EARG;
+    if (dst != src && overlaps(dst, bytes, src, bytes)) return GF_EOVERLAP;
+    if (coeff == 0) return GF_OK;                            // Alg. 1: c == 0 returns
+    const cudaStream_t st = tls_stream;
+    const RegionParams p = region_params(fi, coeff);
+    if (coeff == 1) return launch_region<OP_XOR>(dev, dst, src, bytes, p, st);   // xorr
+    if (field == 4) return launch_region<OP_MADD_GF4>(dev, dst, src, bytes, p, st);
+    return launch_region<OP_MADD_PRMT>(dev, dst, src, bytes, p, st);
+}
+
+int gf_mulrc(int field, uint8_t *dst, uint8_t coeff, size_t bytes)
+{
+    int fi, dev;
+    const int rc = check_ready(field, &fi, &dev);
+    if (rc != GF_OK) return rc;
+    if (coeff >= (unsigned)field) return GF_ECOEFF;
+    if (bytes == 0) return GF_OK;
+    if (!dst || bytes > (SIZE_MAX >> 1)) return GF_EARG;
+    if (coeff == 1) return GF_OK;
+    const cudaStream_t st = tls_stream;
+    const RegionParams p = region_params(fi, coeff);
+    if (coeff == 0) return launch_region<OP_ZERO>(dev, dst, nullptr, bytes, p, st);
+    if (field == 4) return launch_region<OP_MUL_GF4>(dev, dst, nullptr, bytes, p, st);
+    return launch_region<OP_MUL_PRMT>(dev, dst, nullptr, bytes, p, st);
+}
+
+int gf_encode_batch(int field, const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K,
+                    size_t M, size_t batch)
+{
+    int fi, dev;
+    int rc = check_ready(field, &fi, &dev);
+    if (rc != GF_OK) return rc;
+    size_t ab, bb, cb;
+    rc = validate_encode(field, A, C, B, N, K, M, batch, &ab, &bb, &cb);
+    if (rc != GF_OK || M == 0 || batch == 0) return rc;
+    return encode_on_stream(field, fi, A, C, B, N, K, M, batch, tls_stream);
+}
+
+int gf_encode_batch_host(int field, const uint8_t *A_host, const uint8_t *C_host, uint8_t *B_host,
+                         int N, int K, size_t M, size_t batch, void *dev_ws, size_t ws_bytes)
+{
+    int fi, dev;
+    int rc = check_ready(field, &fi, &dev);
+    if (rc != GF_OK) return rc;
+    size_t ab, bb, cb;
+    rc = validate_encode(field, A_host, C_host, B_host, N, K, M, batch, &ab, &bb, &cb);
+    if (rc != GF_OK || M == 0 || batch == 0) return rc;
+    if (!dev_ws) return GF_EARG;
+    const size_t per_gen_a = (size_t)N * M, per_gen_c = (size_t)N * K, per_gen_b = (size_t)K * M;
+    // keep every chunk 16-B aligned inside the workspace
+    auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+    size_t chunk = ws_bytes / (2 * (per_gen_a + per_gen_c + per_gen_b) + 96);
+    if (chunk < 1) return GF_EARG;
+    if (chunk > batch) chunk = batch;
+    HostPipe *P;
+    if ((rc = pipe_for(dev, &P)) != GF_OK) return rc;
+    uint8_t *ws = static_cast<uint8_t *>(dev_ws);
+    uint8_t *bufA[2], *bufC[2], *bufB[2];
+    size_t off = 0;
+    for (int b = 0; b < 2; b++) {
+        bufA[b] = ws + off; off = al(off + chunk * per_gen_a);
+        bufC[b] = ws + off; off = al(off + chunk * per_gen_c);
+        bufB[b] = ws + off; off = al(off + chunk * per_gen_b);
+    }
+    if (off > ws_bytes) return GF_EARG;
+    const size_t nchunks = (batch + chunk - 1) / chunk;
+    for (size_t j = 0; j < nchunks; j++) {
+        const int b = (int)(j & 1);
+        const size_t g0 = j * chunk, gn = (g0 + chunk <= batch) ? chunk : batch - g0;
+        if (j >= 2 && cudaStreamWaitEvent(P->s_h2d, P->ev_free[b], 0) != cudaSuccess) return GF_ECUDA;
+        if (cudaMemcpyAsync(bufA[b], A_host + g0 * per_gen_a, gn * per_gen_a, cudaMemcpyHostToDevice,
+                            P->s_h2d) != cudaSuccess ||
+            cudaMemcpyAsync(bufC[b], C_host + g0 * per_gen_c, gn * per_gen_c, cudaMemcpyHostToDevice,
+                            P->s_h2d) != cudaSuccess ||
+            cudaEventRecord(P->ev_in[b], P->s_h2d) != cudaSuccess)
+            return GF_ECUDA;
+        if (cudaStreamWaitEvent(P->s_cmp, P->ev_in[b], 0) != cudaSuccess) return GF_ECUDA;
+        if (j >= 2 && cudaStreamWaitEvent(P->s_cmp, P->ev_free[b], 0) != cudaSuccess) return GF_ECUDA;
+        if ((rc = encode_on_stream(field, fi, bufA[b], bufC[b], bufB[b], N, K, M, gn, P->s_cmp)) != GF_OK)
+            return rc;
+        if (cudaEventRecord(P->ev_cmp[b], P->s_cmp) != cudaSuccess ||
+            cudaStreamWaitEvent(P->s_d2h, P->ev_cmp[b], 0) != cudaSuccess ||
+            cudaMemcpyAsync(B_host + g0 * per_gen_b, bufB[b], gn * per_gen_b, cudaMemcpyDeviceToHost,
+                            P->s_d2h) != cudaSuccess ||
+            cudaEventRecord(P->ev_free[b], P->s_d2h) != cudaSuccess)
+            return GF_ECUDA;
+    }
+    if (cudaStreamSynchronize(P->s_d2h) != cudaSuccess) return GF_ECUDA;
+    return GF_OK;
+}
+
+int gf_fill_random2d(uint8_t *dst, size_t rows, size_t cols, uint64_t seed, uint64_t stream,
+                     uint64_t base, uint64_t row_stride, uint8_t mask)
+{
+    if (rows == 0 || cols == 0) return GF_OK;
+    if (!dst) return GF_EARG;
+    int dev;
+    if (current_device(&dev) != GF_OK) return GF_ECUDA;
+    const uint64_t key = seed ^ (stream * kStreamMul);
+    const bool words = cols % 8 == 0 && base % 8 == 0 && row_stride % 8 == 0 &&
+                       (reinterpret_cast<uintptr_t>(dst) & 7u) == 0;
+    const size_t total = words ? rows * (cols / 8) : rows * cols;
+    size_t blocks = (total + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    if (words)
+        fill_random_kernel<true><<<(unsigned)blocks, 256, 0, tls_stream>>>(dst, rows, cols, key, base,
+                                                                            row_stride, mask);
+    else
+        fill_random_kernel<false><<<(unsigned)blocks, 256, 0, tls_stream>>>(dst, rows, cols, key, base,
+                                                                             row_stride, mask);
+    return launch_status();
+}
+
+int gf_fill_random(uint8_t *dst, size_t bytes, uint64_t seed, uint64_t stream, uint64_t offset,
+                   uint8_t mask)
+{
+    if (bytes == 0) return GF_OK;
+    // a 1-D range is a single row (64-bit stores when offset, dst, bytes allow)
+    return gf_fill_random2d(dst, 1, bytes, seed, stream, offset, bytes, mask);
+}
+
+}  // extern "C"

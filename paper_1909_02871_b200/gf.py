@@ -1,0 +1,211 @@
+"""Thin Python binding of the C ABI in include/gfrlnc.h (ctypes).
+
+Argument marshalling only: dtype / device / contiguity checks, the current
+torch stream handed to gf_set_stream, and raw pointers.  Every step of the
+computation runs in the sm_100a kernels of libgfrlnc.so; there is no CPU
+fallback -- if the library is missing, importing this module raises.
+
+Names follow the C ABI: init, maddrc, mulrc, encode_batch (Eq. 2,
+PAPER.md:84-88), encode_batch_host, plus the harness-only fill_random /
+fill_random2d / host_tables.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgfrlnc.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} not built: run `python -m paper_1909_02871_b200.build` "
+        "(or __graft_entry__.build()); there is no fallback path")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+_u8p = ctypes.c_void_p
+_sz = ctypes.c_size_t
+_u64 = ctypes.c_uint64
+
+_lib.gf_init.argtypes = [ctypes.c_int]
+_lib.gf_maddrc.argtypes = [ctypes.c_int, _u8p, _u8p, ctypes.c_uint8, _sz]
+_lib.gf_mulrc.argtypes = [ctypes.c_int, _u8p, ctypes.c_uint8, _sz]
+_lib.gf_encode_batch.argtypes = [ctypes.c_int, _u8p, _u8p, _u8p, ctypes.c_int, ctypes.c_int, _sz, _sz]
+_lib.gf_encode_batch_host.argtypes = [ctypes.c_int, _u8p, _u8p, _u8p, ctypes.c_int, ctypes.c_int,
+                                      _sz, _sz, _u8p, _sz]
+_lib.gf_set_stream.argtypes = [ctypes.c_void_p]
+_lib.gf_strerror.argtypes = [ctypes.c_int]
+_lib.gf_strerror.restype = ctypes.c_char_p
+_lib.gf_fill_random.argtypes = [_u8p, _sz, _u64, _u64, _u64, ctypes.c_uint8]
+_lib.gf_fill_random2d.argtypes = [_u8p, _sz, _sz, _u64, _u64, _u64, _u64, ctypes.c_uint8]
+_lib.gf_host_tables.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_uint32), _sz]
+_lib.gf_version.argtypes = []
+
+GF_OK, GF_EFIELD, GF_ECOEFF, GF_EARG, GF_EOVERLAP, GF_ENOINIT, GF_ECUDA = 0, -1, -2, -3, -4, -5, -6
+FIELDS = (2, 4, 16, 256)
+
+# every symbol include/gfrlnc.h declares (tests check the library exports them)
+ABI_SYMBOLS = ("gf_init", "gf_maddrc", "gf_mulrc", "gf_encode_batch", "gf_encode_batch_host",
+               "gf_set_stream", "gf_strerror", "gf_fill_random", "gf_fill_random2d",
+               "gf_host_tables", "gf_version")
+
+
+class GFError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"{what}: {strerror(status)} ({status})")
+
+
+def lib() -> ctypes.CDLL:
+    return _lib
+
+
+def strerror(status: int) -> str:
+    return _lib.gf_strerror(status).decode()
+
+
+def version() -> int:
+    return _lib.gf_version()
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != GF_OK:
+        raise GFError(rc, what)
+
+
+def _dev_u8(t: torch.Tensor, name: str) -> int:
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.uint8:
+        raise TypeError(f"{name} must be a torch.uint8 tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t.data_ptr()
+
+
+def _host_u8(t: torch.Tensor, name: str) -> int:
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.uint8:
+        raise TypeError(f"{name} must be a torch.uint8 tensor")
+    if t.is_cuda:
+        raise ValueError(f"{name} must be a host tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t.data_ptr()
+
+
+def _coeff(c: int) -> int:
+    c = int(c)
+    if not 0 <= c < 256:
+        raise GFError(GF_ECOEFF, f"coefficient {c} does not fit a byte")
+    return c
+
+
+def _use_stream(device: torch.device) -> None:
+    _lib.gf_set_stream(ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream))
+
+
+def init(field: int, device=None) -> None:
+    """gf_init(field) on `device` (default: current device)."""
+    with torch.cuda.device(device if device is not None else torch.cuda.current_device()):
+        _check(_lib.gf_init(field), f"gf_init({field})")
+
+
+def maddrc(field: int, dst: torch.Tensor, src: torch.Tensor, coeff: int) -> torch.Tensor:
+    """dst += coeff * src in place over F_field. Returns dst."""
+    pd, ps = _dev_u8(dst, "dst"), _dev_u8(src, "src")
+    if dst.numel() != src.numel():
+        raise ValueError("dst and src must have the same number of bytes")
+    with torch.cuda.device(dst.device):
+        _use_stream(dst.device)
+        _check(_lib.gf_maddrc(field, pd, ps, _coeff(coeff), dst.numel()), "gf_maddrc")
+    return dst
+
+
+def mulrc(field: int, dst: torch.Tensor, coeff: int) -> torch.Tensor:
+    """dst = coeff * dst in place. Returns dst."""
+    pd = _dev_u8(dst, "dst")
+    with torch.cuda.device(dst.device):
+        _use_stream(dst.device)
+        _check(_lib.gf_mulrc(field, pd, _coeff(coeff), dst.numel()), "gf_mulrc")
+    return dst
+
+
+def encode_batch(field: int, A: torch.Tensor, C: torch.Tensor, B: torch.Tensor | None = None,
+                 checked: bool = False) -> torch.Tensor:
+    """B[g,k,m] = sum_i C[g,i,k] * A[g,i,m] over F_field (Eq. 2).
+
+    A: uint8 [batch, N, M], C: uint8 [batch, N, K] on one CUDA device.
+    B (optional, [batch, K, M]) is overwritten and returned.  checked=True
+    verifies C < field first (one device reduction); otherwise entries of C
+    are taken modulo the field size by masking, as the ABI documents."""
+    if A.dim() != 3 or C.dim() != 3 or A.shape[:2] != C.shape[:2]:
+        raise ValueError("expected A [batch, N, M] and C [batch, N, K]")
+    batch, N, M = A.shape
+    K = C.shape[2]
+    if B is None:
+        B = torch.empty((batch, K, M), dtype=torch.uint8, device=A.device)
+    elif tuple(B.shape) != (batch, K, M):
+        raise ValueError(f"B must have shape {(batch, K, M)}")
+    pa, pc, pb = _dev_u8(A, "A"), _dev_u8(C, "C"), _dev_u8(B, "B")
+    if checked and C.numel() and int(C.max()) >= field:
+        raise GFError(GF_ECOEFF, "encode_batch(checked)")
+    with torch.cuda.device(A.device):
+        _use_stream(A.device)
+        _check(_lib.gf_encode_batch(field, pa, pc, pb, N, K, M, batch), "gf_encode_batch")
+    return B
+
+
+def encode_batch_host(field: int, A: torch.Tensor, C: torch.Tensor, B: torch.Tensor,
+                      workspace: torch.Tensor) -> torch.Tensor:
+    """Encode from / to HOST tensors (pinned recommended) through a device
+    workspace, overlapping copies and kernels; blocking."""
+    batch, N, M = A.shape
+    K = C.shape[2]
+    pa, pc, pb = _host_u8(A, "A"), _host_u8(C, "C"), _host_u8(B, "B")
+    pw = _dev_u8(workspace, "workspace")
+    with torch.cuda.device(workspace.device):
+        _check(_lib.gf_encode_batch_host(field, pa, pc, pb, N, K, M, batch, pw, workspace.numel()),
+               "gf_encode_batch_host")
+    return B
+
+
+def host_workspace_bytes(N: int, K: int, M: int, gens_per_chunk: int) -> int:
+    """Device workspace for encode_batch_host with the given chunk size."""
+    return 2 * gens_per_chunk * (N * M + N * K + K * M) + 96
+
+
+# ---- harness-only --------------------------------------------------------------
+
+def fill_random(dst: torch.Tensor, seed: int, stream: int, offset: int = 0, mask: int = 0xFF) -> torch.Tensor:
+    """dst[j] = byte(seed, stream, offset + j) & mask (seeded_inputs definition)."""
+    p = _dev_u8(dst, "dst")
+    with torch.cuda.device(dst.device):
+        _use_stream(dst.device)
+        _check(_lib.gf_fill_random(p, dst.numel(), seed, stream, offset, mask), "gf_fill_random")
+    return dst
+
+
+def fill_random2d(dst: torch.Tensor, seed: int, stream: int, base: int, row_stride: int,
+                  mask: int = 0xFF) -> torch.Tensor:
+    """dst viewed as [rows, cols] (last dim = cols):
+    dst[r, c] = byte(seed, stream, base + r * row_stride + c) & mask."""
+    p = _dev_u8(dst, "dst")
+    cols = dst.shape[-1] if dst.dim() else 1
+    rows = dst.numel() // cols if cols else 0
+    with torch.cuda.device(dst.device):
+        _use_stream(dst.device)
+        _check(_lib.gf_fill_random2d(p, rows, cols, seed, stream, base, row_stride, mask),
+               "gf_fill_random2d")
+    return dst
+
+
+def host_tables(field: int):
+    """The byte-permute tables gf_init uploads (host-only; no GPU needed):
+    list of q entries, each 8 uint32 words (see include/gfrlnc.h)."""
+    q = field
+    buf = (ctypes.c_uint32 * (max(q, 1) * 8))()
+    _check(_lib.gf_host_tables(field, buf, len(buf)), "gf_host_tables")
+    return [list(buf[8 * c: 8 * c + 8]) for c in range(q)]

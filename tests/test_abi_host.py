@@ -1,0 +1,133 @@
+"""CPU-side checks of the product library (no GPU compute calls):
+the C ABI loads and exports every symbol include/gfrlnc.h declares, status
+strings, and the host-built byte-permute tables -- emulating the kernels'
+PRMT / bit-plane arithmetic in Python against the oracle's byte products
+(the SURVEY.md 4 "fake backend")."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1909_02871_b200 import gf
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "gfrlnc.h")
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(gf_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_symbols_exported():
+    syms = declared_symbols()
+    assert len(syms) >= 10
+    assert set(syms) == set(gf.ABI_SYMBOLS)
+    L = gf.lib()
+    for s in syms:
+        assert hasattr(L, s), f"{s} not exported"
+
+
+def test_status_strings_and_version():
+    for code in range(-6, 1):
+        assert gf.strerror(code) and gf.strerror(code) != "unknown status"
+    assert gf.strerror(-99) == "unknown status"
+    assert gf.version() >= 100
+
+
+def test_host_tables_errors():
+    L = gf.lib()
+    buf = (ctypes.c_uint32 * 16)()
+    assert L.gf_host_tables(3, buf, 8) == gf.GF_EFIELD
+    assert L.gf_host_tables(256, buf, 8) == gf.GF_EARG        # capacity too small
+    assert L.gf_host_tables(2, buf, 16) == gf.GF_OK
+
+
+def test_abi_validation_without_gpu():
+    """Argument errors are reported before any device work."""
+    L = gf.lib()
+    assert L.gf_init(3) == gf.GF_EFIELD
+    assert L.gf_maddrc(5, None, None, 1, 16) == gf.GF_EFIELD
+    assert L.gf_encode_batch(7, None, None, None, 1, 1, 1, 1) == gf.GF_EFIELD
+
+
+# ---- PRMT emulation ------------------------------------------------------------
+
+def prmt(a, b, s):
+    src = [(a >> (8 * i)) & 0xFF for i in range(4)] + [(b >> (8 * i)) & 0xFF for i in range(4)]
+    out = 0
+    for i in range(4):
+        nib = (s >> (4 * i)) & 0xF
+        v = src[nib & 7]
+        if nib & 8:
+            v = 0xFF if v & 0x80 else 0
+        out |= v << (8 * i)
+    return out
+
+
+def make_sel(x):
+    t0 = x & 0x07070707
+    t1 = (x >> 3) & 0x07070707
+    t2 = (x >> 6) & 0x03030303
+    return [(t | (t >> 12)) & 0xFFFFFFFF for t in (t0, t1, t2)]
+
+
+def lookup_word(T, x):
+    s0, s1, s2 = make_sel(x)
+    y = prmt(T[0], T[1], s0) ^ prmt(T[2], T[3], s1) ^ prmt(T[4], T[4], s2)
+    return prmt(y, y, 0x3120)
+
+
+@pytest.mark.parametrize("q", (2, 4, 16, 256))
+def test_prmt_split_tables_match_oracle(q):
+    """For every coefficient and every byte value in every byte position of a
+    word, the emulated 3-PRMT lookup + un-permute equals the oracle product."""
+    tabs = gf.host_tables(q)
+    MB = oracle.mulbyte_table(q)
+    rng = np.random.default_rng(q)
+    vals = list(range(256))
+    for c in range(q):
+        T = tabs[c]
+        for pos in range(4):
+            for v in vals:
+                x = (v << (8 * pos)) | (int(rng.integers(0, 2 ** 32)) & ~(0xFF << (8 * pos)) & 0xFFFFFFFF)
+                y = lookup_word(T, x)
+                assert (y >> (8 * pos)) & 0xFF == MB[c, v]
+        # whole random words
+        for _ in range(64):
+            x = int(rng.integers(0, 2 ** 32))
+            y = lookup_word(T, x)
+            exp = sum(int(MB[c, (x >> (8 * i)) & 0xFF]) << (8 * i) for i in range(4))
+            assert y == exp
+
+
+def test_selectors_never_set_sign_mode():
+    for x in (0, 0xFFFFFFFF, 0x80808080, 0x7F7F7F7F, 0x12345678):
+        for s in make_sel(x):
+            for i in range(4):
+                assert not (s >> (4 * i)) & 0x8
+
+
+def gf4_xtime(a):
+    hi = (a >> 1) & 0x55555555
+    return hi | (((a & 0x55555555) ^ hi) << 1)
+
+
+def test_gf4_bitplane_masks_match_oracle():
+    tabs = gf.host_tables(4)
+    MB = oracle.mulbyte_table(4)
+    for c in range(4):
+        m0, m1 = tabs[c][5], tabs[c][6]
+        for v in range(256):
+            x = v * 0x01010101
+            y = (x & m0) ^ (gf4_xtime(x) & m1)
+            assert y == int(MB[c, v]) * 0x01010101
+
+
+def test_gf2_mask():
+    tabs = gf.host_tables(2)
+    assert tabs[0][5] == 0 and tabs[1][5] == 0xFFFFFFFF

@@ -1,0 +1,310 @@
+"""GPU parity: the sm_100a kernels, called through the C ABI (ctypes binding),
+against the CPU oracle on the same seeded inputs.  Bit-exact (integer work).
+
+Inputs for the oracle always come from seeded_inputs on the host; the device
+generator is only used where it was first shown equal to seeded_inputs
+(test_device_rng_matches_host) and is then regenerated on the host for the
+sampled outputs the oracle computes.
+"""
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import seeded_inputs as si
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = (2, 4, 16, 256)
+
+
+@pytest.fixture(scope="module")
+def gfm():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1909_02871_b200 import gf
+    torch.cuda.set_device(0)
+    for q in FIELDS:
+        gf.init(q)
+    return gf
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+# ---- generator ------------------------------------------------------------------
+
+@pytest.mark.parametrize("offset,n", [(0, 1), (0, 4096), (3, 1000), (8, 64), (13, 12345), (1 << 33, 777)])
+def test_device_rng_matches_host(gfm, offset, n):
+    t = torch.empty(n, dtype=torch.uint8, device="cuda")
+    gfm.fill_random(t, 190902871, 1, offset)
+    assert np.array_equal(t.cpu().numpy(), si.random_bytes(190902871, 1, offset, n))
+    gfm.fill_random(t, 77, 2, offset, mask=15)
+    assert np.array_equal(t.cpu().numpy(), si.random_bytes(77, 2, offset, n) & 15)
+
+
+@pytest.mark.parametrize("rows,cols,base,stride", [(5, 64, 0, 64), (7, 24, 8, 4096), (3, 17, 5, 100),
+                                                   (4, 8192, 16384, 65536)])
+def test_device_rng_2d_matches_host(gfm, rows, cols, base, stride):
+    t = torch.empty((rows, cols), dtype=torch.uint8, device="cuda")
+    gfm.fill_random2d(t, 9, 1, base, stride)
+    assert np.array_equal(t.cpu().numpy(), si.random_bytes_2d(9, 1, base, stride, rows, cols))
+
+
+# ---- region ops -------------------------------------------------------------------
+
+SIZES = (0, 1, 3, 15, 16, 17, 63, 64, 100, 1500, 4096 + 5, (1 << 20) + 7)
+
+
+def coeffs_for(q):
+    cs = {0, 1, q - 1, (q // 2) | 1}
+    cs |= {int(c) for c in si.rejection_coeffs(q, 0, 5, 2, 3)}
+    return sorted(c for c in cs if c < q)
+
+
+@pytest.mark.parametrize("q", FIELDS)
+def test_maddrc_parity_sizes_offsets_canaries(gfm, q):
+    pad = 64
+    for n in SIZES:
+        for doff, soff in ((0, 0), (1, 0), (0, 3), (5, 9), (16, 4), (7, 7)):
+            src_all = si.random_bytes(31, si.STREAM_SRC, 0, n + 2 * pad)
+            dst_all = si.random_bytes(31, si.STREAM_DST, 0, n + 2 * pad)
+            for c in coeffs_for(q):
+                d = dev(dst_all)
+                s = dev(src_all)
+                gfm.maddrc(q, d[pad + doff: pad + doff + n], s[pad + soff: pad + soff + n], c)
+                exp = dst_all.copy()
+                seg = exp[pad + doff: pad + doff + n].copy()
+                oracle.maddrc(q, seg, src_all[pad + soff: pad + soff + n].copy(), c)
+                exp[pad + doff: pad + doff + n] = seg
+                got = d.cpu().numpy()
+                assert np.array_equal(got, exp), (n, doff, soff, c)   # includes canaries
+                assert np.array_equal(s.cpu().numpy(), src_all)       # src untouched
+
+
+@pytest.mark.parametrize("q", FIELDS)
+def test_mulrc_parity(gfm, q):
+    pad = 32
+    for n in SIZES:
+        for off in (0, 1, 6):
+            base = si.random_bytes(41, si.STREAM_DST, 0, n + 2 * pad)
+            for c in coeffs_for(q):
+                d = dev(base)
+                gfm.mulrc(q, d[pad + off: pad + off + n], c)
+                exp = base.copy()
+                seg = exp[pad + off: pad + off + n].copy()
+                oracle.mulrc(q, seg, c)
+                exp[pad + off: pad + off + n] = seg
+                assert np.array_equal(d.cpu().numpy(), exp), (n, off, c)
+
+
+@pytest.mark.parametrize("q", FIELDS)
+def test_maddrc_exact_aliasing(gfm, q):
+    a = si.random_bytes(43, 3, 0, 10007)
+    for c in coeffs_for(q):
+        t = dev(a)
+        gfm.maddrc(q, t, t, c)                      # (1 + c) * a
+        exp = a.copy()
+        oracle.maddrc(q, exp, a.copy(), c)
+        assert np.array_equal(t.cpu().numpy(), exp)
+
+
+@pytest.mark.parametrize("q", FIELDS)
+def test_c2_sweep_full_parity(gfm, q):
+    """BASELINE.json configs[1]: every size 64 B .. 256 MiB, seeded c (X12)."""
+    c = si.c2_coeff(q)
+    for n in si.C2_SIZES:
+        src = si.random_bytes(si.C2_SEED, si.STREAM_SRC, 0, n)
+        dst = si.random_bytes(si.C2_SEED, si.STREAM_DST, 0, n)
+        d = dev(dst)
+        gfm.maddrc(q, d, dev(src), c)
+        oracle.maddrc(q, dst, src, c)
+        assert np.array_equal(d.cpu().numpy(), dst), n
+
+
+def test_region_errors(gfm):
+    L = gfm.lib()
+    t = torch.zeros(256, dtype=torch.uint8, device="cuda")
+    p = t.data_ptr()
+    assert L.gf_maddrc(16, p, p + 128, 16, 64) == gfm.GF_ECOEFF
+    assert L.gf_maddrc(4, p, p + 128, 4, 64) == gfm.GF_ECOEFF
+    assert L.gf_mulrc(2, p, 2, 64) == gfm.GF_ECOEFF
+    assert L.gf_maddrc(256, p, p + 8, 3, 64) == gfm.GF_EOVERLAP
+    assert L.gf_maddrc(256, None, p, 3, 64) == gfm.GF_EARG
+    assert L.gf_maddrc(256, None, None, 3, 0) == gfm.GF_OK
+    assert L.gf_encode_batch(256, p, p, p + 64, 0, 1, 4, 1) == gfm.GF_EARG
+    assert L.gf_encode_batch(256, p, p + 200, p + 8, 2, 2, 16, 1) == gfm.GF_EOVERLAP
+    assert L.gf_encode_batch(256, p, p, p, 1, 1, 0, 5) == gfm.GF_OK
+
+
+def test_not_initialised_in_fresh_process():
+    import subprocess
+    import sys
+    code = ("import torch; from paper_1909_02871_b200 import gf; torch.cuda.init();"
+            "t=torch.zeros(64,dtype=torch.uint8,device='cuda');"
+            "L=gf.lib(); r=L.gf_maddrc(256,t.data_ptr(),t.data_ptr()+32,3,32);"
+            "print(r); assert r == gf.GF_ENOINIT")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    subprocess.check_call([sys.executable, "-c", code])
+
+
+# ---- encode -----------------------------------------------------------------------
+
+def run_encode(gfm, q, A, C, **kw):
+    return gfm.encode_batch(q, dev(A), dev(C), **kw).cpu().numpy()
+
+
+def test_c1_full(gfm):
+    """BASELINE.json configs[0]: GF(256), N=16 x 1500 B, K=1, non-zero c."""
+    A, C = si.encode_inputs(si.C1, 256)
+    assert np.array_equal(run_encode(gfm, 256, A, C), oracle.encode_batch(256, A, C))
+
+
+@pytest.mark.parametrize("q", FIELDS)
+@pytest.mark.parametrize("N,K,M,batch", [
+    (1, 1, 1, 1), (1, 1, 4, 1), (3, 2, 5, 2), (16, 1, 1500, 3), (17, 33, 1500, 3),
+    (64, 64, 1500, 4), (5, 7, 4096, 2), (2, 3, 130, 9), (32, 32, 4100, 2), (40, 17, 999, 2),
+    (8, 5, 12, 17)])
+def test_encode_parity_shapes(gfm, q, N, K, M, batch):
+    A = si.random_bytes(51 + N, si.STREAM_A, 0, batch * N * M).reshape(batch, N, M)
+    C = si.uniform_coeffs(q, 52 + K, si.STREAM_C, 0, batch * N * K).reshape(batch, N, K)
+    assert np.array_equal(run_encode(gfm, q, A, C), oracle.encode_batch(q, A, C))
+
+
+@pytest.mark.parametrize("q", FIELDS)
+def test_encode_unaligned_views(gfm, q):
+    """Rows not 4-B aligned (byte path) and B at an odd address."""
+    batch, N, K, M = 3, 6, 5, 64
+    A = si.random_bytes(61, 1, 0, batch * N * M).reshape(batch, N, M)
+    C = si.uniform_coeffs(q, 62, 2, 0, batch * N * K).reshape(batch, N, K)
+    bufA = torch.zeros(A.size + 1, dtype=torch.uint8, device="cuda")
+    bufA[1:] = dev(A.reshape(-1))
+    bufB = torch.full((batch * K * M + 3,), 0xEE, dtype=torch.uint8, device="cuda")
+    Av = bufA[1:].view(batch, N, M)
+    Bv = bufB[1:-2].view(batch, K, M)
+    gfm.encode_batch(q, Av, dev(C), Bv)
+    got = bufB.cpu().numpy()
+    assert np.array_equal(got[1:-2].reshape(batch, K, M), oracle.encode_batch(q, A, C))
+    assert got[0] == 0xEE and (got[-2:] == 0xEE).all()
+
+
+@pytest.mark.parametrize("q", FIELDS)
+def test_encode_coefficient_edge_cases(gfm, q):
+    batch, N, M = 2, 6, 1500
+    A = si.random_bytes(71, 1, 0, batch * N * M).reshape(batch, N, M)
+    I = np.broadcast_to(np.eye(N, dtype=np.uint8), (batch, N, N)).copy()
+    assert np.array_equal(run_encode(gfm, q, A, I), A)
+    Z = np.zeros((batch, N, 3), dtype=np.uint8)
+    assert (run_encode(gfm, q, A, Z) == 0).all()
+    F = np.full((batch, N, 4), q - 1, dtype=np.uint8)
+    assert np.array_equal(run_encode(gfm, q, A, F), oracle.encode_batch(q, A, F))
+
+
+def test_encode_sharding_invariance(gfm):
+    """Generation shards and byte-range shards, launched separately, equal the
+    unsharded launch (the multi-GPU partitioning of DESIGN.md)."""
+    q, batch, N, K, M = 256, 6, 20, 9, 4096
+    A = si.random_bytes(81, 1, 0, batch * N * M).reshape(batch, N, M)
+    C = si.uniform_coeffs(q, 82, 2, 0, batch * N * K).reshape(batch, N, K)
+    full = run_encode(gfm, q, A, C)
+    parts = [run_encode(gfm, q, A[g0:g1], C[g0:g1]) for g0, g1 in ((0, 1), (1, 4), (4, 6))]
+    assert np.array_equal(np.concatenate(parts), full)
+    for m0, m1 in ((0, 1024), (1024, 3072), (3072, 4096)):
+        assert np.array_equal(run_encode(gfm, q, A[:, :, m0:m1], C), full[:, :, m0:m1])
+
+
+def test_encode_checked_mode(gfm):
+    A = np.zeros((1, 2, 8), dtype=np.uint8)
+    C = np.array([[[1], [16]]], dtype=np.uint8)
+    with pytest.raises(gfm.GFError):
+        gfm.encode_batch(16, dev(A), dev(C), checked=True)
+
+
+@pytest.mark.parametrize("q", (16, 256))
+def test_c3_full_size_sampled(gfm, q):
+    """BASELINE.json configs[2] at full size (65536 generations, the launch
+    bench.py times): device-generated inputs, sampled generations recomputed by
+    the oracle from host-regenerated inputs, plus Freivalds on more."""
+    cfg = si.C3
+    seed = si.field_seed(cfg, q)
+    A = torch.empty((cfg.batch, cfg.N, cfg.M), dtype=torch.uint8, device="cuda")
+    C = torch.empty((cfg.batch, cfg.N, cfg.K), dtype=torch.uint8, device="cuda")
+    gfm.fill_random(A, seed, si.STREAM_A, 0)
+    gfm.fill_random(C, seed, si.STREAM_C, 0, mask=q - 1)
+    B = gfm.encode_batch(q, A, C)
+    rng = np.random.default_rng(q)
+    gens = sorted({0, 1, cfg.batch - 1, *rng.integers(0, cfg.batch, 13).tolist()})
+    for g in gens:
+        Ah, Ch = si.encode_inputs(cfg, q, g, g + 1)
+        assert np.array_equal(B[g].cpu().numpy(), oracle.encode_batch(q, Ah, Ch)[0]), g
+    t = oracle.freivalds_trials(q)
+    for g in rng.integers(0, cfg.batch, 48).tolist():
+        Ah, Ch = si.encode_inputs(cfg, q, g, g + 1)
+        r = si.uniform_coeffs(q, seed, si.STREAM_FREIVALDS, g * 64 * t, t * cfg.K).reshape(t, cfg.K)
+        Bg = B[g].cpu().numpy()
+        assert all(oracle.freivalds_gen(q, Ah[0], Ch[0], Bg, rr) == 0 for rr in r), g
+    del A, B, C
+    torch.cuda.empty_cache()
+
+
+def test_c4_full_size_sampled(gfm):
+    """BASELINE.json configs[3]: GF(256), N=K=256, 64 KiB packets, 2048
+    generations (32 GiB of A) in one launch; sampled generations x byte ranges."""
+    cfg = si.C4
+    q = 256
+    seed = si.field_seed(cfg, q)
+    free, _ = torch.cuda.mem_get_info()
+    need = cfg.batch * (cfg.N + cfg.K) * cfg.M + cfg.batch * cfg.N * cfg.K
+    if free < need * 1.05:
+        pytest.skip(f"needs {need / 2**30:.1f} GiB")
+    A = torch.empty((cfg.batch, cfg.N, cfg.M), dtype=torch.uint8, device="cuda")
+    C = torch.empty((cfg.batch, cfg.N, cfg.K), dtype=torch.uint8, device="cuda")
+    gfm.fill_random(A, seed, si.STREAM_A, 0)
+    gfm.fill_random(C, seed, si.STREAM_C, 0, mask=q - 1)
+    B = gfm.encode_batch(q, A, C)
+    for g, m0, m1 in ((0, 0, 2048), (cfg.batch - 1, cfg.M - 2048, cfg.M), (777, 30000, 31000)):
+        Ah, Ch = si.encode_inputs(cfg, q, g, g + 1)
+        exp = oracle.encode_gen_cols(q, Ah[0], Ch[0], m0, m1)
+        assert np.array_equal(B[g, :, m0:m1].cpu().numpy(), exp), (g, m0)
+    del A, B, C
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("q", (2, 4))
+def test_c5_chunk_sampled(gfm, q):
+    """BASELINE.json configs[4] (N=K=32, 1 MiB packets) in the chunk size the
+    bench launches: one chunk of generations from the middle of the job."""
+    cfg = si.C5
+    seed = si.field_seed(cfg, q)
+    g0, G = 1000, 64
+    A = torch.empty((G, cfg.N, cfg.M), dtype=torch.uint8, device="cuda")
+    C = torch.empty((G, cfg.N, cfg.K), dtype=torch.uint8, device="cuda")
+    gfm.fill_random(A, seed, si.STREAM_A, g0 * cfg.N * cfg.M)
+    gfm.fill_random(C, seed, si.STREAM_C, g0 * cfg.N * cfg.K, mask=q - 1)
+    B = gfm.encode_batch(q, A, C)
+    for gl, m0, m1 in ((0, 0, 8192), (G - 1, cfg.M - 8192, cfg.M), (17, 500000, 510000)):
+        Ah, Ch = si.encode_inputs(cfg, q, g0 + gl, g0 + gl + 1)
+        exp = oracle.encode_gen_cols(q, Ah[0], Ch[0], m0, m1)
+        assert np.array_equal(B[gl, :, m0:m1].cpu().numpy(), exp), (gl, m0)
+    del A, B, C
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("q", (4, 256))
+def test_encode_host_path(gfm, q):
+    batch, N, K, M = 37, 16, 8, 1500
+    A = si.random_bytes(91, 1, 0, batch * N * M).reshape(batch, N, M)
+    C = si.uniform_coeffs(q, 92, 2, 0, batch * N * K).reshape(batch, N, K)
+    Ah = torch.from_numpy(A).pin_memory()
+    Ch = torch.from_numpy(C).pin_memory()
+    Bh = torch.empty((batch, K, M), dtype=torch.uint8).pin_memory()
+    ws = torch.empty(gfm.host_workspace_bytes(N, K, M, 5), dtype=torch.uint8, device="cuda")
+    gfm.encode_batch_host(q, Ah, Ch, Bh, ws)
+    assert np.array_equal(Bh.numpy(), oracle.encode_batch(q, A, C))
+    L = gfm.lib()
+    assert L.gf_encode_batch_host(q, Ah.data_ptr(), Ch.data_ptr(), Bh.data_ptr(), N, K, M, batch,
+                                  ws.data_ptr(), 100) == gfm.GF_EARG
