@@ -221,7 +221,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_1909_02871_b200 import gf
+    from paper_1909_02871_b200 import gf, shard
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -236,38 +236,42 @@ def main():
         gf.init(f)
     peaks = load_peaks()
 
-    # ---- per-rank workload (weak scaling by generation; C4 by byte range)
-    batch = cfg.batch
-    g_base = rank * batch                    # absolute generation index of this rank
-    M = cfg.M
+    # ---- this rank's shard: weak scaling by generation (C1, C3, C5) or
+    # strong scaling by packet byte range (C4), SURVEY.md 8(e)
+    by_bytes = cfg.shard == "bytes"
+    sh = shard.plan(cfg.batch, cfg.M, ws, rank, by="bytes" if by_bytes else "generation",
+                    weak=not by_bytes)
+    G, Ms, N, K, M = sh.generations, sh.columns, cfg.N, cfg.K, cfg.M
     free, _ = torch.cuda.mem_get_info(device)
-    per_gen = (cfg.N + cfg.K) * M + cfg.N * cfg.K
-    chunk = args.chunk_gens or batch
-    if per_gen * chunk > 0.85 * free:
-        chunk = max(1, int(0.85 * free // per_gen))
+    per_gen = (N + K) * Ms + N * K
+    chunk = min(G, args.chunk_gens or G)
+    if per_gen * chunk > 0.8 * free:
+        chunk = max(1, int(0.8 * free // per_gen))
+    nchunks = -(-G // chunk)
     stream = torch.cuda.current_stream(device)
 
-    def alloc(G):
-        A = torch.empty((G, cfg.N, M), dtype=torch.uint8, device=device)
-        C = torch.empty((G, cfg.N, cfg.K), dtype=torch.uint8, device=device)
-        B = torch.empty((G, cfg.K, M), dtype=torch.uint8, device=device)
-        return A, C, B
+    A = torch.empty((chunk, N, Ms), dtype=torch.uint8, device=device)
+    Cm = torch.empty((chunk, N, K), dtype=torch.uint8, device=device)
+    B = torch.empty((chunk, K, Ms), dtype=torch.uint8, device=device)
 
-    def fill(A, C, f, g0):
+    def fill(f, j):
+        """Inputs of chunk j, generated on device by absolute index."""
         seed = si.field_seed(cfg, f)
-        gf.fill_random(A, seed, si.STREAM_A, (g_base + g0) * cfg.N * M)
-        gf.fill_random(C, seed, si.STREAM_C, (g_base + g0) * cfg.N * cfg.K, mask=f - 1)
+        g = sh.g0 + j * chunk
+        n = min(chunk, G - j * chunk)
+        gf.fill_random2d(A[:n].view(n * N, Ms), seed, si.STREAM_A, g * N * M + sh.m0, M)
+        gf.fill_random(Cm[:n], seed, si.STREAM_C, g * N * K, mask=f - 1)
+        return n
 
     def time_field(f, steps, warmup, sampler=None):
-        """Device-resident throughput: inputs in HBM before the timed region."""
-        A, C, B = alloc(chunk)
-        nchunks = (batch + chunk - 1) // chunk
-        fill(A, C, f, 0)
+        """Device-resident throughput: inputs in HBM before the timed region.
+        One chunk: CUDA-event span over all steps.  Several chunks (C5 does not
+        fit): inputs of each chunk are regenerated between launches and only
+        the encode launches are timed (sum of their event durations)."""
+        n0 = fill(f, 0)
         torch.cuda.synchronize()
         for _ in range(warmup):
-            for j in range(nchunks):
-                G = min(chunk, batch - j * chunk)
-                gf.encode_batch(f, A[:G], C[:G], B[:G])
+            gf.encode_batch(f, A[:n0], Cm[:n0], B[:n0])
         torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
@@ -275,79 +279,79 @@ def main():
         if sampler:
             sampler.start()
             time.sleep(0.3)
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * steps * nchunks)]
-        launches = 0
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(steps * nchunks)]
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
+        launches = 0
         t_start.record(stream)
         for s in range(steps):
             for j in range(nchunks):
-                G = min(chunk, batch - j * chunk)
-                if nchunks > 1:
-                    # chunked configs: regenerate C per chunk outside the kernel timing
-                    pass
-                ev[2 * (s * nchunks + j)].record(stream)
-                gf.encode_batch(f, A[:G], C[:G], B[:G])
-                ev[2 * (s * nchunks + j) + 1].record(stream)
+                n = fill(f, j) if nchunks > 1 else n0
+                e0, e1 = ev[s * nchunks + j]
+                e0.record(stream)
+                gf.encode_batch(f, A[:n], Cm[:n], B[:n])
+                e1.record(stream)
                 launches += 1
         t_end.record(stream)
         torch.cuda.synchronize()
         clocks = sampler.stop() if sampler else None
-        total_ms = t_start.elapsed_time(t_end)
-        kern_ms = [ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(steps * nchunks)]
+        kern_ms = [a.elapsed_time(b) for a, b in ev]
+        total_ms = t_start.elapsed_time(t_end) if nchunks == 1 else sum(kern_ms)
         if ws > 1:
             t = torch.tensor([total_ms], device=device)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             total_ms = float(t.item())
             dist.barrier()
-        del A, C, B
-        torch.cuda.empty_cache()
         return total_ms, kern_ms, launches, clocks
 
+    job_src_per_step = (cfg.batch * N * M) if by_bytes else ws * G * N * M
     sampler = ClockSampler(local)
     total_ms, kern_ms, launches, clocks = time_field(q, args.steps, args.warmup, sampler)
-    src_bytes_rank = batch * cfg.N * M
-    value = ws * src_bytes_rank * args.steps / (total_ms / 1e3) / 1e9
+    value = job_src_per_step * args.steps / (total_ms / 1e3) / 1e9
     ms_per_step = total_ms / args.steps
 
     per_field = {str(q): round(value, 3)}
     for f in fields[1:]:
-        tms, _, _, _ = time_field(f, max(3, args.steps // 2), args.warmup)
-        per_field[str(f)] = round(ws * src_bytes_rank * max(3, args.steps // 2) / (tms / 1e3) / 1e9, 3)
+        st = max(3, args.steps // 2)
+        tms, _, _, _ = time_field(f, st, args.warmup)
+        per_field[str(f)] = round(job_src_per_step * st / (tms / 1e3) / 1e9, 3)
 
-    # ---- roofline of the dominant kernel (the encode launch; one per step)
-    avg_kernel_s = statistics.mean(kern_ms) / 1e3 * (1 if chunk >= batch else 1)
-    gens_per_launch = min(chunk, batch)
-    bm_per_launch = cfg.N * cfg.K * M * gens_per_launch
+    # ---- roofline of the dominant kernel: the encode launch (every launch of
+    # the timed region is one); algorithmic work per launch / mean duration
+    avg_kernel_s = statistics.mean(kern_ms) / 1e3
+    gens_per_launch = chunk
+    bm_per_launch = N * K * Ms * gens_per_launch
     ops = bm_per_launch * OPS_PER_BYTE_MADD[q]
     alu_peak_tops = N_SM * ALU_LANES_PER_SM_CLK * peaks["sm_max_mhz"] * 1e6 / 1e12
     alu_achieved = ops / avg_kernel_s / 1e12
-    hbm_bytes = ((cfg.N + cfg.K) * M + cfg.N * cfg.K) * gens_per_launch
+    hbm_bytes = per_gen * gens_per_launch
     hbm_achieved = hbm_bytes / avg_kernel_s / 1e9
     alu_frac = alu_achieved / alu_peak_tops
     hbm_frac = hbm_achieved / peaks["hbm_gbs"]
+    traffic = lookup_traffic(q, cfg, gens_per_launch, Ms, gf.version())
     if alu_frac >= hbm_frac:
         roof = {"bound": "alu", "achieved": round(alu_achieved, 3), "peak": round(alu_peak_tops, 3),
-                "unit": "Tops/s", "frac": round(alu_frac, 4), "traffic": None,
-                "peak_source": f"{N_SM} SMs x {ALU_LANES_PER_SM_CLK} ALU lanes/clk x "
-                               f"{peaks['sm_max_mhz']:.0f} MHz (B300_MICROARCH.md pipe rates, "
-                               "B200 SM count/clock)",
+                "unit": "Tops/s", "frac": round(alu_frac, 4),
+                "peak_source": f"{N_SM} SMs x {ALU_LANES_PER_SM_CLK} ALU-pipe lanes/clk x "
+                               f"{peaks['sm_max_mhz']:.0f} MHz (DESIGN.md 'roofline')",
                 "ops_per_byte_madd": OPS_PER_BYTE_MADD[q]}
     else:
         roof = {"bound": "hbm", "achieved": round(hbm_achieved, 1), "peak": peaks["hbm_gbs"],
-                "unit": "GB/s", "frac": round(hbm_frac, 4), "traffic": None,
-                "peak_source": peaks["source"]}
+                "unit": "GB/s", "frac": round(hbm_frac, 4), "peak_source": peaks["source"]}
+    roof["traffic"] = traffic
     roof["kernel"] = f"encode_kernel<F={q}>"
     roof["kernel_ms"] = round(statistics.mean(kern_ms), 4)
     roof["byte_madds_per_launch"] = bm_per_launch
     roof["hbm_bytes_per_launch"] = hbm_bytes
     hbm = {"achieved": round(hbm_achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
            "frac": round(hbm_frac, 4), "peak_source": peaks["source"]}
+    del A, Cm, B
+    torch.cuda.empty_cache()
 
-    # ---- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(gf, torch, dist, cfg, q, batch, g_base, device, ws, args)
+        e2e = run_e2e(gf, torch, dist, cfg, q, sh, device, ws, args)
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -358,14 +362,18 @@ def main():
         out = {
             "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "higher_is_better": True, "scaling": "strong" if by_bytes else "weak",
+            "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (seeded splitmix64 byte stream: uniform payload bytes, "
                     "i.i.d. uniform coefficients over F_q; generated on device)",
-            "config": {"workload": workload_name(cfg, q, batch), "field": q, "N": cfg.N, "K": cfg.K,
-                       "M": M, "batch_per_gpu": batch, "global_batch": ws * batch,
-                       "gens_per_launch": gens_per_launch,
-                       "parallelism": f"generation-sharded x{ws}, no collective",
-                       "l2": f"inputs {src_bytes_rank / 1e9:.2f} GB per GPU >> 126 MB L2 (no flush)"},
+            "config": {"workload": workload_name(cfg, q, G), "field": q, "N": N, "K": K, "M": M,
+                       "gens_per_gpu": G, "bytes_per_packet_per_gpu": Ms,
+                       "global_batch": cfg.batch if by_bytes else ws * G,
+                       "gens_per_launch": gens_per_launch, "launches_per_step": nchunks,
+                       "parallelism": (f"byte-range sharded x{ws}" if by_bytes else
+                                       f"generation-sharded x{ws}") + ", no collective",
+                       "l2": (f"inputs {G * N * Ms / 1e9:.2f} GB per GPU >> 126 MB L2 (no flush)"
+                              if G * N * Ms > 2 * 126e6 else "L2-resident working set")},
             "per_field": per_field,
             "roofline": roof,
             "hbm": hbm,
@@ -373,7 +381,7 @@ def main():
             "e2e": e2e,
             "clocks": clocks,
             "gpu_launches": launches,
-            "kernel_ms_per_step": round(statistics.mean(kern_ms), 4),
+            "kernel_ms_per_launch": round(statistics.mean(kern_ms), 4),
         }
         print(json.dumps(out), flush=True)
     if ws > 1:
@@ -381,34 +389,48 @@ def main():
         dist.destroy_process_group()
 
 
-def run_e2e(gf, torch, dist, cfg, q, batch, g_base, device, ws, args):
+def lookup_traffic(q, cfg, gens, Ms, lib_version):
+    """dram__bytes_read + dram__bytes_write per launch of the encode kernel from
+    the committed ncu --set full capture of the same launch (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(p))
+        e = d.get(f"{cfg.name}/GF{q}/{gens}/{Ms}")
+        if e and e.get("lib_version") == lib_version:
+            return e["bytes"]
+    except Exception:
+        pass
+    return None
+
+
+def run_e2e(gf, torch, dist, cfg, q, sh, device, ws, args):
     """Same metric through gf_encode_batch_host: pinned host A/C in, host B
     out, host<->device copies inside the timed region every step."""
-    M = cfg.M
-    N, K = cfg.N, cfg.K
+    N, K, M, Ms = cfg.N, cfg.K, cfg.M, sh.columns
+    per_gen_host = N * Ms + N * K + K * Ms
+    G = min(sh.generations, max(1, int(14e9 // per_gen_host)))
     try:
-        Ah = torch.empty((batch, N, M), dtype=torch.uint8).pin_memory()
-        Ch = torch.empty((batch, N, K), dtype=torch.uint8).pin_memory()
-        Bh = torch.empty((batch, K, M), dtype=torch.uint8).pin_memory()
+        Ah = torch.empty((G, N, Ms), dtype=torch.uint8).pin_memory()
+        Ch = torch.empty((G, N, K), dtype=torch.uint8).pin_memory()
+        Bh = torch.empty((G, K, Ms), dtype=torch.uint8).pin_memory()
     except Exception as e:  # pinned host memory exhausted
         return {"value": None, "unit": "GB/s", "error": f"pinned alloc failed: {e}"}
     seed = si.field_seed(cfg, q)
-    # host inputs: generated on device in slices, copied down before timing
-    step = 4096
-    tmpA = torch.empty((step, N, M), dtype=torch.uint8, device=device)
+    step = max(1, min(G, int(2e9 // (N * Ms + N * K))))
+    tmpA = torch.empty((step, N, Ms), dtype=torch.uint8, device=device)
     tmpC = torch.empty((step, N, K), dtype=torch.uint8, device=device)
-    for g0 in range(0, batch, step):
-        G = min(step, batch - g0)
-        gf.fill_random(tmpA[:G], seed, si.STREAM_A, (g_base + g0) * N * M)
-        gf.fill_random(tmpC[:G], seed, si.STREAM_C, (g_base + g0) * N * K, mask=q - 1)
-        Ah[g0:g0 + G].copy_(tmpA[:G])
-        Ch[g0:g0 + G].copy_(tmpC[:G])
+    for j in range(0, G, step):
+        n = min(step, G - j)
+        g = sh.g0 + j
+        gf.fill_random2d(tmpA[:n].view(n * N, Ms), seed, si.STREAM_A, g * N * M + sh.m0, M)
+        gf.fill_random(tmpC[:n], seed, si.STREAM_C, g * N * K, mask=q - 1)
+        Ah[j:j + n].copy_(tmpA[:n])
+        Ch[j:j + n].copy_(tmpC[:n])
     del tmpA, tmpC
-    chunk = 2048
-    ws_t = torch.empty(gf.host_workspace_bytes(N, K, M, chunk), dtype=torch.uint8, device=device)
+    chunk = max(1, min(G, int(0.5e9 // per_gen_host)))
+    ws_t = torch.empty(gf.host_workspace_bytes(N, K, Ms, chunk), dtype=torch.uint8, device=device)
     torch.cuda.synchronize()
-    for _ in range(max(1, min(2, args.warmup))):
-        gf.encode_batch_host(q, Ah, Ch, Bh, ws_t)
+    gf.encode_batch_host(q, Ah, Ch, Bh, ws_t)
     steps = max(1, min(args.steps, 5))
     if ws > 1:
         dist.barrier()
@@ -421,12 +443,14 @@ def run_e2e(gf, torch, dist, cfg, q, batch, g_base, device, ws, args):
         t = torch.tensor([dt], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt = float(t.item())
-    value = ws * steps * batch * N * M / dt / 1e9
+    src = (G * N * Ms) * ws
+    value = steps * src / dt / 1e9
     del ws_t
     torch.cuda.empty_cache()
-    return {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": batch * (N * M + N * K),
-            "d2h_bytes_per_step": batch * K * M, "steps": steps,
-            "path": "gf_encode_batch_host (pinned host buffers, 3-stream copy/compute overlap)",
+    return {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": G * (N * Ms + N * K),
+            "d2h_bytes_per_step": G * K * Ms, "steps": steps, "gens_per_step": G,
+            "path": f"gf_encode_batch_host: pinned host buffers, {chunk}-generation chunks, "
+                    "3-stream copy/compute overlap",
             "timing": "host wall clock around blocking calls, max over ranks"}
 
 

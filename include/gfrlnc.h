@@ -112,13 +112,16 @@ int gf_fill_random(uint8_t *dst, size_t bytes, uint64_t seed, uint64_t stream,
 int gf_fill_random2d(uint8_t *dst, size_t rows, size_t cols, uint64_t seed, uint64_t stream,
                      uint64_t base, uint64_t row_stride, uint8_t mask);
 
-/* Host-only (no GPU needed): copy out the per-coefficient byte-permute tables
- * gf_init uploads, so CPU tests can emulate the kernels' lookups.  Writes
- * q * 8 uint32 words: for coefficient c, words [8c .. 8c+7] =
- *   { T0[0..3], T0[4..7], T1[0..3], T1[4..7], T2[0..3], M0, M1, 0 }
+/* Host-only (no GPU needed): copy out the per-coefficient tables gf_init
+ * uploads, so CPU tests can emulate the kernels' arithmetic.  Writes
+ * q * 16 uint32 words: for coefficient c, words [16c .. 16c+15] =
+ *   { T0[0..3], T0[4..7], T1[0..3], T1[4..7], T2[0..3], M0, M1, 0,
+ *     pow[c][0], ..., pow[c][7] }
  * with Tg[v] = c * (v << 3g) (packed product, one byte per entry, little
- * endian), and M0/M1 the all-ones masks of coefficient bits 0/1 (GF(2)/GF(4)
- * bit-plane kernels).  Returns GF_OK, GF_EFIELD or GF_EARG (cap too small). */
+ * endian; byte-permute split tables, GPU form of Alg. 1's tl/th), M0/M1 the
+ * all-ones masks of coefficient bits 0/1 (GF(2)/GF(4) bit planes), and
+ * pow[c][j] = c * x^j for j < w, else 0 (Alg. 2's imul constants,
+ * PAPER.md:245,266).  Returns GF_OK, GF_EFIELD or GF_EARG (cap too small). */
 int gf_host_tables(int field, uint32_t *out, size_t cap_words);
 
 /* Library version (major * 10000 + minor * 100 + patch). */

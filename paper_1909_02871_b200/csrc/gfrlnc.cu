@@ -17,7 +17,7 @@
 namespace gfr {
 
 constexpr int kMaxDevices = 64;
-constexpr int kVersion = 100;   // 0.1.0
+constexpr int kVersion = 102;   // 0.1.2
 
 __device__ uint32_t g_dev_tabs[4][256 * kTableWords];
 
@@ -132,13 +132,15 @@ static int launch_encode_t(EncodeParams p, cudaStream_t st)
     const size_t gen_groups = (p.batch + p.gens_per_cta - 1) / p.gens_per_cta;
     const size_t grid = (size_t)p.k_tiles * gen_groups * (size_t)p.ctas_per_gen;
     if (grid > 0x7FFFFFFFu) return GF_EARG;
-    const size_t smem = (size_t)p.gens_per_cta * enc_smem_bytes_per_gen<F, KT>();
+    constexpr int S = enc_stages<F>();
+    const size_t smem = (size_t)p.gens_per_cta * enc_table_bytes_per_gen<F, KT>() +
+                        (BW ? 0 : (size_t)S * W * wpb * 32 * 4);
     if (smem > 48 * 1024) {
-        if (cudaFuncSetAttribute(encode_kernel<F, W, KT, BW>,
+        if (cudaFuncSetAttribute(encode_kernel<F, W, KT, S, BW>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
             return GF_ECUDA;
     }
-    encode_kernel<F, W, KT, BW><<<(unsigned)grid, wpb * 32, smem, st>>>(p);
+    encode_kernel<F, W, KT, S, BW><<<(unsigned)grid, wpb * 32, smem, st>>>(p);
     return launch_status();
 }
 

@@ -18,6 +18,8 @@
 // sm_100a byte permute (PRMT) selects among 8 bytes with a 3-bit index:
 //     T0[v] = c * v,  T1[v] = c * (v << 3),  T2[v] = c * (v << 6)
 // and c * byte = T0[b & 7] ^ T1[(b >> 3) & 7] ^ T2[b >> 6] by linearity.
+// Each entry also carries the bit-plane masks of c (GF(2)/GF(4)) and the imul
+// constants pow[c][j] = c * x^j of Alg. 2.
 #include <cstdint>
 #include <cstring>
 
@@ -103,6 +105,8 @@ int build_tables(int field, uint32_t *out, size_t cap_words)
         t[5] = (c & 1) ? 0xFFFFFFFFu : 0u;  // bit-plane mask of coefficient bit 0
         t[6] = (c & 2) ? 0xFFFFFFFFu : 0u;  // bit-plane mask of coefficient bit 1
         t[7] = 0u;
+        // imul constants (Alg. 2): pow[c][j] = c * x^j
+        for (int j = 0; j < 8; j++) t[8 + j] = j < w ? elem_mul(field, c, 1u << j) : 0u;
     }
     return 0;
 }

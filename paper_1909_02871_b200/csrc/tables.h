@@ -5,7 +5,7 @@
 
 namespace gfr {
 
-constexpr int kTableWords = 8;   // uint32 words per coefficient entry
+constexpr int kTableWords = 16;  // uint32 words per coefficient entry
 
 int field_width(int field);                                  // -1 if unsupported
 uint32_t elem_mul(int field, uint32_t a, uint32_t b);        // a * b in F_q

@@ -46,6 +46,7 @@ _lib.gf_version.argtypes = []
 
 GF_OK, GF_EFIELD, GF_ECOEFF, GF_EARG, GF_EOVERLAP, GF_ENOINIT, GF_ECUDA = 0, -1, -2, -3, -4, -5, -6
 FIELDS = (2, 4, 16, 256)
+TABLE_WORDS = 16          # uint32 words per coefficient in gf_host_tables
 
 # every symbol include/gfrlnc.h declares (tests check the library exports them)
 ABI_SYMBOLS = ("gf_init", "gf_maddrc", "gf_mulrc", "gf_encode_batch", "gf_encode_batch_host",
@@ -204,8 +205,8 @@ def fill_random2d(dst: torch.Tensor, seed: int, stream: int, base: int, row_stri
 
 def host_tables(field: int):
     """The byte-permute tables gf_init uploads (host-only; no GPU needed):
-    list of q entries, each 8 uint32 words (see include/gfrlnc.h)."""
+    list of q entries, each TABLE_WORDS uint32 words (see include/gfrlnc.h)."""
     q = field
-    buf = (ctypes.c_uint32 * (max(q, 1) * 8))()
+    buf = (ctypes.c_uint32 * (max(q, 1) * TABLE_WORDS))()
     _check(_lib.gf_host_tables(field, buf, len(buf)), "gf_host_tables")
-    return [list(buf[8 * c: 8 * c + 8]) for c in range(q)]
+    return [list(buf[TABLE_WORDS * c: TABLE_WORDS * (c + 1)]) for c in range(q)]

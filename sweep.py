@@ -1,0 +1,156 @@
+#!/usr/bin/env python
+"""sweep.py -- every BASELINE.json workload on one GPU, one JSON line each.
+
+    python sweep.py [--configs C1,C2,C3,C4,C5] [--out gpurun_out/sweep.jsonl]
+
+C1: single-generation latency (us per gf_encode_batch call).
+C2: gf_maddrc / gf_mulrc region sweep, 64 B .. 256 MiB per field; points whose
+    3 x size working set fits twice in L2 are timed both with an L2 flush
+    between reps (HBM numbers) and L2-resident (labelled).
+C3, C4, C5: batched encode, source GB/s, % of HBM and of the ALU-pipe peak.
+Timing: CUDA events on the launching stream, >= 3 warm-ups, >= 10 reps and
+>= 0.5 s per point; median reported.  Inputs come from the device generator.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import seeded_inputs as si  # noqa: E402
+from bench import ALU_LANES_PER_SM_CLK, N_SM, OPS_PER_BYTE_MADD, ClockSampler, load_peaks  # noqa: E402
+
+
+def timed(torch, fn, stream, min_reps=10, min_s=0.5, warmup=3, flush=None):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    times = []
+    total = 0.0
+    while len(times) < min_reps or total < min_s * 1e3:
+        if flush is not None:
+            flush()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        e1.synchronize()
+        t = e0.elapsed_time(e1)
+        times.append(t)
+        total += t
+        if len(times) > 20000:
+            break
+    return statistics.median(times), min(times), len(times)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="C1,C2,C3,C4,C5")
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep.jsonl"))
+    args = ap.parse_args()
+    import torch
+
+    from paper_1909_02871_b200 import gf
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    for q in (2, 4, 16, 256):
+        gf.init(q)
+    st = torch.cuda.current_stream(dev)
+    peaks = load_peaks()
+    alu_peak = N_SM * ALU_LANES_PER_SM_CLK * peaks["sm_max_mhz"] * 1e6
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush_buf = torch.empty(2 * l2 + (64 << 20), dtype=torch.uint8, device=dev)
+
+    def flush():
+        flush_buf.fill_(1)
+
+    out = open(args.out, "a")
+    sampler = ClockSampler(0)
+    sampler.start()
+
+    def emit(rec):
+        rec["gpu"] = torch.cuda.get_device_name(dev)
+        print(json.dumps(rec), flush=True)
+        out.write(json.dumps(rec) + "\n")
+        out.flush()
+
+    todo = args.configs.split(",")
+    if "C1" in todo:
+        cfg = si.C1
+        A = torch.empty((1, cfg.N, cfg.M), dtype=torch.uint8, device=dev)
+        Ah, Chh = si.encode_inputs(cfg, 256)
+        A.copy_(torch.from_numpy(Ah))
+        C = torch.from_numpy(Chh).to(dev)
+        B = torch.empty((1, cfg.K, cfg.M), dtype=torch.uint8, device=dev)
+        med, best, n = timed(torch, lambda: gf.encode_batch(256, A, C, B), st, min_reps=1000)
+        emit({"config": "C1", "field": 256, "us_per_call_median": round(med * 1e3, 3),
+              "us_per_call_best": round(best * 1e3, 3), "reps": n,
+              "source_GBps": round(cfg.source_bytes() / (med / 1e3) / 1e9, 3),
+              "note": "launch-latency bound (25.5 KB per call), L2-resident"})
+
+    if "C2" in todo:
+        nmax = si.C2_SIZES[-1]
+        src = torch.empty(nmax, dtype=torch.uint8, device=dev)
+        dst = torch.empty(nmax, dtype=torch.uint8, device=dev)
+        gf.fill_random(src, si.C2_SEED, si.STREAM_SRC, 0)
+        gf.fill_random(dst, si.C2_SEED, si.STREAM_DST, 0)
+        for q in (2, 4, 16, 256):
+            c = si.c2_coeff(q)
+            for n in si.C2_SIZES:
+                s, d = src[:n], dst[:n]
+                for op in ("maddrc", "mulrc"):
+                    fn = (lambda: gf.maddrc(q, d, s, c)) if op == "maddrc" else (lambda: gf.mulrc(q, d, c))
+                    traffic = 3 * n if op == "maddrc" else 2 * n
+                    resident = traffic < 2 * l2
+                    modes = [("hbm", flush)] + ([("l2", None)] if resident else [])
+                    for mode, fl in modes:
+                        med, best, reps = timed(torch, fn, st, flush=fl,
+                                                min_s=0.2 if n < (1 << 20) else 0.5)
+                        rec = {"config": "C2", "op": op, "field": q, "coeff": c, "bytes": n,
+                               "mode": mode, "us_median": round(med * 1e3, 3), "reps": reps,
+                               "source_GBps": round(n / (med / 1e3) / 1e9, 3),
+                               "hbm_GBps": round(traffic / (med / 1e3) / 1e9, 2)}
+                        if mode == "hbm":
+                            rec["hbm_frac"] = round(traffic / (med / 1e3) / 1e9 / peaks["hbm_gbs"], 4)
+                        emit(rec)
+        del src, dst
+
+    for name in ("C3", "C4", "C5"):
+        if name not in todo:
+            continue
+        cfg = si.ENCODE_CONFIGS[name]
+        free, _ = torch.cuda.mem_get_info(dev)
+        per_gen = (cfg.N + cfg.K) * cfg.M + cfg.N * cfg.K
+        chunk = min(cfg.batch, int(0.7 * (free - flush_buf.numel()) // per_gen))
+        A = torch.empty((chunk, cfg.N, cfg.M), dtype=torch.uint8, device=dev)
+        C = torch.empty((chunk, cfg.N, cfg.K), dtype=torch.uint8, device=dev)
+        B = torch.empty((chunk, cfg.K, cfg.M), dtype=torch.uint8, device=dev)
+        for q in cfg.fields:
+            seed = si.field_seed(cfg, q)
+            gf.fill_random(A, seed, si.STREAM_A, 0)
+            gf.fill_random(C, seed, si.STREAM_C, 0, mask=q - 1)
+            med, best, reps = timed(torch, lambda: gf.encode_batch(q, A, C, B), st, min_reps=5,
+                                    min_s=1.0)
+            src_b = chunk * cfg.N * cfg.M
+            bm = chunk * cfg.N * cfg.K * cfg.M
+            emit({"config": name, "field": q, "gens_per_launch": chunk, "of_batch": cfg.batch,
+                  "ms_median": round(med, 3), "ms_best": round(best, 3), "reps": reps,
+                  "source_GBps": round(src_b / (med / 1e3) / 1e9, 2),
+                  "byte_madds_per_s_T": round(bm / (med / 1e3) / 1e12, 3),
+                  "hbm_frac": round(per_gen * chunk / (med / 1e3) / 1e9 / peaks["hbm_gbs"], 4),
+                  "alu_frac": round(bm * OPS_PER_BYTE_MADD[q] / (med / 1e3) / alu_peak, 4)})
+        del A, B, C
+        torch.cuda.empty_cache()
+
+    emit({"clocks": sampler.stop()})
+
+
+if __name__ == "__main__":
+    main()

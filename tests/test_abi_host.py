@@ -41,10 +41,10 @@ def test_status_strings_and_version():
 
 def test_host_tables_errors():
     L = gf.lib()
-    buf = (ctypes.c_uint32 * 16)()
+    buf = (ctypes.c_uint32 * (2 * gf.TABLE_WORDS))()
     assert L.gf_host_tables(3, buf, 8) == gf.GF_EFIELD
     assert L.gf_host_tables(256, buf, 8) == gf.GF_EARG        # capacity too small
-    assert L.gf_host_tables(2, buf, 16) == gf.GF_OK
+    assert L.gf_host_tables(2, buf, 2 * gf.TABLE_WORDS) == gf.GF_OK
 
 
 def test_abi_validation_without_gpu():
@@ -131,3 +131,63 @@ def test_gf4_bitplane_masks_match_oracle():
 def test_gf2_mask():
     tabs = gf.host_tables(2)
     assert tabs[0][5] == 0 and tabs[1][5] == 0xFFFFFFFF
+
+
+# ---- imul (Alg. 2) emulation: the FMA-pipe half of the encode kernels --------
+
+M32 = 0xFFFFFFFF
+SLOT = {2: 0xFFFFFFFF, 4: 0x55555555, 16: 0x11111111, 256: 0x01010101}
+
+
+def imul_word(q, tab, x):
+    """XOR_j ((x >> j) & slot_mask) * pow[c][j], as IMAD + LOP3 do it."""
+    w = oracle.width(q)
+    r = 0
+    for j in range(w):
+        r ^= (((x >> j) & SLOT[q]) * tab[8 + j]) & M32
+    return r
+
+
+@pytest.mark.parametrize("q", (2, 4, 16, 256))
+def test_imul_planes_match_oracle(q):
+    """Carry-free plane products (reading X7: scalar constant per 32-bit lane)."""
+    tabs = gf.host_tables(q)
+    MB = oracle.mulbyte_table(q)
+    rng = np.random.default_rng(7 + q)
+    for c in range(q):
+        assert tabs[c][8:8 + oracle.width(q)] == [oracle.mul(q, c, 1 << j) for j in range(oracle.width(q))]
+        for _ in range(256):
+            x = int(rng.integers(0, 2 ** 32))
+            exp = sum(int(MB[c, (x >> (8 * i)) & 0xFF]) << (8 * i) for i in range(4))
+            assert imul_word(q, tabs[c], x) == exp
+
+
+def test_gf256_hybrid_prmt_imul_matches_oracle():
+    """Encode engine for GF(256): bits 0-5 by PRMT (permuted byte order),
+    bits 6-7 by IMAD on the byte-permuted word, one final un-permute."""
+    tabs = gf.host_tables(256)
+    MB = oracle.mulbyte_table(256)
+    rng = np.random.default_rng(11)
+    for c in range(256):
+        T = tabs[c]
+        for _ in range(32):
+            x = int(rng.integers(0, 2 ** 32))
+            s0, s1, _ = make_sel(x)
+            xp = prmt(x, x, 0x3120)
+            b6 = (xp >> 6) & 0x01010101
+            b7 = (xp >> 7) & 0x01010101
+            acc = prmt(T[0], T[1], s0) ^ prmt(T[2], T[3], s1) ^ ((b6 * T[14]) & M32) ^ ((b7 * T[15]) & M32)
+            y = prmt(acc, acc, 0x3120)
+            assert y == sum(int(MB[c, (x >> (8 * i)) & 0xFF]) << (8 * i) for i in range(4))
+
+
+def test_gf16_permuted_imul_matches_prmt_order():
+    tabs = gf.host_tables(16)
+    rng = np.random.default_rng(12)
+    for c in range(16):
+        for _ in range(32):
+            x = int(rng.integers(0, 2 ** 32))
+            xp = prmt(x, x, 0x3120)
+            s0, s1, s2 = make_sel(x)
+            T = tabs[c]
+            assert imul_word(16, T, xp) == prmt(T[0], T[1], s0) ^ prmt(T[2], T[3], s1) ^ prmt(T[4], T[4], s2)
