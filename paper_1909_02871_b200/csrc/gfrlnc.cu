@@ -5,11 +5,13 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
 #include "../../include/gfrlnc.h"
 #include "encode_kernels.cuh"
+#include "encode_lanek.cuh"
 #include "region_kernels.cuh"
 #include "rng_kernels.cuh"
 #include "tables.h"
@@ -17,7 +19,7 @@
 namespace gfr {
 
 constexpr int kMaxDevices = 64;
-constexpr int kVersion = 102;   // 0.1.2
+constexpr int kVersion = 110;   // 0.1.10: lane-k encode
 
 __device__ uint32_t g_dev_tabs[4][256 * kTableWords];
 
@@ -173,9 +175,56 @@ static int launch_encode_field(int field, EncodeParams p, cudaStream_t st)
     }
 }
 
+template <int F>
+static int launch_lanek(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M,
+                        size_t batch, cudaStream_t st)
+{
+    LanekParams p;
+    p.A = A; p.C = C; p.B = B; p.M = M; p.Mw = (uint32_t)(M / 4); p.batch = batch;
+    p.N = N; p.K = K; p.qmask = F - 1;
+    p.tiles = (int)((p.Mw + kLkTW - 1) / kLkTW);
+    p.k_tiles = (K + kLkKT - 1) / kLkKT;
+    p.ncpad = (N + 3) & ~3;
+    const size_t grid = batch * (size_t)p.tiles * (size_t)p.k_tiles;
+    if (grid > 0x7FFFFFFFu) return GF_EARG;
+    const size_t smem = (size_t)2 * LkField<F>::kRows * kLkQS * 4 + (size_t)kLkStages * kLkTW * 4 +
+                        (size_t)kLkKT * p.N;
+    if (smem > 227 * 1024) return GF_EARG;
+    if (cudaFuncSetAttribute(encode_lanek_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return GF_ECUDA;
+    encode_lanek_kernel<F><<<(unsigned)grid, kLkThreads, smem, st>>>(p);
+    return launch_status();
+}
+
+// encode path: "lanek" (shared-memory product tables, k on lanes) for GF(16) /
+// GF(256) with K >= 32 on word-aligned packets; the column kernel otherwise.
+// GFRLNC_ENCODE_PATH=column|lanek overrides (experiments).
+static int encode_path_override()
+{
+    static const int v = [] {
+        const char *e = getenv("GFRLNC_ENCODE_PATH");
+        if (!e) return 0;
+        if (!strcmp(e, "column")) return 1;
+        if (!strcmp(e, "lanek")) return 2;
+        return 0;
+    }();
+    return v;
+}
+
 static int encode_on_stream(int field, int fi, const uint8_t *A, const uint8_t *C, uint8_t *B,
                             int N, int K, size_t M, size_t batch, cudaStream_t st)
 {
+    {
+        const bool aligned = M % 4 == 0 && (reinterpret_cast<uintptr_t>(A) & 3u) == 0 &&
+                             (reinterpret_cast<uintptr_t>(B) & 3u) == 0 && M / 4 < 0xFFFFFFFFull;
+        const int ov = encode_path_override();
+        const bool lanek = (field == 16 || field == 256) && aligned &&
+                           (ov == 2 || (ov == 0 && K >= 32));
+        if (lanek)
+            return field == 256 ? launch_lanek<256>(A, C, B, N, K, M, batch, st)
+                                : launch_lanek<16>(A, C, B, N, K, M, batch, st);
+    }
     EncodeParams p;
     std::memset(&p, 0, sizeof(p));
     p.A = A; p.C = C; p.B = B;
