@@ -1,31 +1,39 @@
-// encode_lanek.cuh -- batched RLNC encode over GF(16) / GF(256) with the
-// coded packet index k on the lanes ("lane = k" layout), shared-memory
-// product tables, and warp specialisation.
+// encode_lanek.cuh -- batched RLNC encode with the coded-packet index k on the
+// lanes ("lane = k" layout), shared-memory product tables and warp
+// specialisation.  All four fields.
 //
 //   B[g][k][m] = sum_i C[g][i][k] * A[g][i][m]          (Eq. 2)
 //
-// Why: in the column layout (encode_kernels.cuh) every (i, k, word) costs >= 4
-// ALU-pipe instructions for GF(256) and the kernel is ALU-bound.  Here the
-// multiply becomes a shared-memory lookup that the LSU pipe serves:
-//   * for every source packet i and every word w of the CTA's tile, builder
-//     warps write the products of a_i[w] with ALL coefficients of a nibble:
-//       GF(16):  Q[c][w]     = c * a_i[w],                 c < 16
-//       GF(256): Q[c][w]     = c * a_i[w],                 c < 16   (low nibble)
-//                Q[16+c][w]  = (c * x^4) * a_i[w],         c < 16   (high nibble)
-//     (GF(2)-linearity in c: c*a = c_lo*a + c_hi*(x^4 a)); this is the paper's
-//     split-table idea (Alg. 1) with the roles of data and
-//     coefficient exchanged, built from the xtime chain a, xa, x^2 a, ...;
-//   * gatherer warps: lane = coded packet k (32 per warp), each lane reads
-//     the row of ITS coefficient c_ik, so one warp-wide LDS gathers 32
-//     different products of the same source word (<= 16 distinct rows; the
-//     row stride is odd so the rows sit in distinct banks: one wavefront);
-//     acc[w] ^= Q[c_lo][w] ^ Q[16 + c_hi][w], 48 words per lane in registers;
-//   * the Q tables are double-buffered: builders fill buffer i&1 while the
-//     gatherers read buffer (i-1)&1; named barriers FULL/EMPTY hand them over;
-//   * builders also stream the source tile HBM -> smem with a cp.async ring.
-// Per (i, k, word): GF(256) 2 LDS + 1 LOP3; GF(16) 1 LDS + 1 LOP3.  The table
-// build (15 or 30 products per source word) is amortised over the CTA's 64
-// coded packets.
+// Why: in the column layout (encode_kernels.cuh) every (i, k, word) costs ALU
+// instructions (>= 4 for GF(256)) and the kernel is ALU-bound.  Here the
+// multiply becomes a shared-memory gather that the LSU pipe serves:
+//   * a "step" consumes SG source packets (SG = 4 for GF(2), 2 for GF(4), 1
+//     otherwise).  For every word w of the CTA's tile, builder warps write the
+//     16 XOR-combinations of four generator values P0..P3 of the step:
+//        Q[r][w] = XOR_{j : bit j of r} P_j[w]            r < 16
+//       GF(2):   P_j = a_{4s+j}                  (r = the 4 coefficient bits)
+//       GF(4):   P = a_{2s}, x a_{2s}, a_{2s+1}, x a_{2s+1}   (r = c0 | c1 << 2)
+//       GF(16):  P_j = x^j a_s                   (r = c: Q[c] = c * a)
+//       GF(256): as GF(16) for the low nibble of c, plus 16 more rows built
+//                from x^4 a .. x^7 a for the high nibble
+//     i.e. the paper's split-table idea (Alg. 1) with the
+//     roles of data and coefficient exchanged (a "four Russians" table over
+//     the coefficient bits), built from the xtime chain by linearity over GF(2);
+//   * gatherer warps: lane = coded packet k (32 per warp), each lane reads the
+//     row r of ITS coefficients, so one warp-wide LDS gathers 32 products of
+//     the same source word (<= 16 distinct rows; odd row stride puts them in
+//     distinct banks: one wavefront); WT words per lane accumulate in
+//     registers;
+//   * Q is double-buffered between builders and gatherers (named barriers
+//     FULL / EMPTY); builders also stream the source tile HBM -> smem with a
+//     cp.async ring several steps deep.
+// Per (step, k, word): 1 LDS + 1 LOP3 (GF(256): 2 LDS + 1 LOP3); the table
+// build (15 or 30 words per source word) is shared by the CTA's 32*KG lanes.
+//
+// Geometry (LkGeom): KG = 2 k-groups (64 coded packets per CTA, 48 words per
+// lane, 384-word tiles, one CTA per SM) for K > 32; KG = 1 (32 coded packets,
+// 32 words per lane, 256-word tiles, three CTAs per SM so that one CTA's
+// prologue / epilogue overlaps the others' streaming) otherwise.
 #pragma once
 #include <cstdint>
 
@@ -34,16 +42,18 @@
 
 namespace gfr {
 
-constexpr int kLkWT = 48;                 // words per gatherer lane
-constexpr int kLkWG = 8;                  // word groups per CTA
-constexpr int kLkTW = kLkWT * kLkWG;      // words per CTA tile (384)
-constexpr int kLkQS = kLkTW + 1;          // Q row stride in words (odd: bank-conflict-free gathers)
-constexpr int kLkKT = 64;                 // coded packets per CTA (2 gatherer k-groups)
-constexpr int kLkGatherWarps = 16;
+constexpr int kLkWG = 8;                  // word groups (gatherer warps per k-group)
 constexpr int kLkBuildWarps = 4;
-constexpr int kLkThreads = 32 * (kLkGatherWarps + kLkBuildWarps);
-constexpr int kLkStages = 4;              // cp.async ring depth (source rows)
-constexpr int kLkBuildWords = kLkTW / (32 * kLkBuildWarps);   // words per builder thread (3)
+constexpr int kLkSteps = 4;               // cp.async ring depth in steps
+
+template <int KG> struct LkGeom {
+    static constexpr int WT = KG == 1 ? 32 : 48;          // words per gatherer lane
+    static constexpr int TW = WT * kLkWG;                 // words per tile
+    static constexpr int QS = TW + 1;                     // Q row stride (odd)
+    static constexpr int BWORDS = TW / (32 * kLkBuildWarps);
+    static constexpr int THREADS = 32 * (KG * kLkWG + kLkBuildWarps);
+    static constexpr int MINB = KG == 1 ? 3 : 1;          // CTAs per SM targeted
+};
 
 struct LanekParams {
     const uint8_t *A;
@@ -55,24 +65,35 @@ struct LanekParams {
     int N, K;
     int qmask;
     int tiles;         // word tiles per packet
-    int k_tiles;       // ceil(K / 64)
-    int ncpad;         // coefficient cache row length (N rounded up to 4)
+    int k_tiles;       // ceil(K / (32 KG))
 };
 
 template <int F> struct LkField;
+template <> struct LkField<2> {
+    static constexpr int kRows = 16, kSG = 4;
+    __device__ __forceinline__ static uint32_t index(const uint8_t *c) {
+        return (c[0] & 1u) | (c[1] & 1u) << 1 | (c[2] & 1u) << 2 | (c[3] & 1u) << 3;
+    }
+};
+template <> struct LkField<4> {
+    static constexpr int kRows = 16, kSG = 2;
+    __device__ __forceinline__ static uint32_t index(const uint8_t *c) { return (c[0] & 3u) | (c[1] & 3u) << 2; }
+};
 template <> struct LkField<16> {
-    static constexpr int kRows = 16;
+    static constexpr int kRows = 16, kSG = 1;
     __device__ __forceinline__ static uint32_t xtime(uint32_t a)
     {
         return ((a << 1) & 0xEEEEEEEEu) ^ (((a >> 3) & 0x11111111u) * 3u);
     }
+    __device__ __forceinline__ static uint32_t index(const uint8_t *c) { return c[0] & 15u; }
 };
 template <> struct LkField<256> {
-    static constexpr int kRows = 32;
+    static constexpr int kRows = 32, kSG = 1;
     __device__ __forceinline__ static uint32_t xtime(uint32_t a)
     {
         return ((a << 1) & 0xFEFEFEFEu) ^ (((a >> 7) & 0x01010101u) * 0x1Bu);
     }
+    __device__ __forceinline__ static uint32_t index(const uint8_t *c) { return c[0]; }
 };
 
 __device__ __forceinline__ void nbar_sync(int id, int n)
@@ -84,27 +105,54 @@ __device__ __forceinline__ void nbar_arrive(int id, int n)
     asm volatile("bar.arrive %0, %1;" :: "r"(id), "r"(n) : "memory");
 }
 
-// Q rows 1..15 (and 17..31) of one word from its xtime chain
+// rows 1..15 of Q for one word: XOR combinations of p0..p3 (11 XORs)
+template <int QS>
 __device__ __forceinline__ void store_nibble_products(uint32_t *q, uint32_t p0, uint32_t p1, uint32_t p2,
                                                       uint32_t p3)
 {
     const uint32_t q3 = p0 ^ p1, q5 = p2 ^ p0, q6 = p2 ^ p1, q7 = q6 ^ p0;
-    q[1 * kLkQS] = p0;  q[2 * kLkQS] = p1;  q[3 * kLkQS] = q3;  q[4 * kLkQS] = p2;
-    q[5 * kLkQS] = q5;  q[6 * kLkQS] = q6;  q[7 * kLkQS] = q7;  q[8 * kLkQS] = p3;
-    q[9 * kLkQS] = p3 ^ p0;  q[10 * kLkQS] = p3 ^ p1;  q[11 * kLkQS] = p3 ^ q3;
-    q[12 * kLkQS] = p3 ^ p2; q[13 * kLkQS] = p3 ^ q5;  q[14 * kLkQS] = p3 ^ q6;
-    q[15 * kLkQS] = p3 ^ q7;
+    q[1 * QS] = p0;  q[2 * QS] = p1;  q[3 * QS] = q3;  q[4 * QS] = p2;
+    q[5 * QS] = q5;  q[6 * QS] = q6;  q[7 * QS] = q7;  q[8 * QS] = p3;
+    q[9 * QS] = p3 ^ p0;  q[10 * QS] = p3 ^ p1;  q[11 * QS] = p3 ^ q3;
+    q[12 * QS] = p3 ^ p2; q[13 * QS] = p3 ^ q5;  q[14 * QS] = p3 ^ q6;
+    q[15 * QS] = p3 ^ q7;
 }
 
-template <int F>
-__global__ void __launch_bounds__(kLkThreads, 1) encode_lanek_kernel(LanekParams p)
+// generator values of one word for step s (a[j] = word of source packet SG*s+j)
+template <int F, int QS>
+__device__ __forceinline__ void build_word(uint32_t *q, const uint32_t (&a)[LkField<F>::kSG])
+{
+    if constexpr (F == 2) {
+        store_nibble_products<QS>(q, a[0], a[1], a[2], a[3]);
+    } else if constexpr (F == 4) {
+        store_nibble_products<QS>(q, a[0], gf4_xtime(a[0]), a[1], gf4_xtime(a[1]));
+    } else {
+        using L = LkField<F>;
+        const uint32_t p1 = L::xtime(a[0]), p2 = L::xtime(p1), p3 = L::xtime(p2);
+        store_nibble_products<QS>(q, a[0], p1, p2, p3);
+        if constexpr (F == 256) {
+            const uint32_t p4 = L::xtime(p3), p5 = L::xtime(p4), p6 = L::xtime(p5), p7 = L::xtime(p6);
+            store_nibble_products<QS>(q + 16 * QS, p4, p5, p6, p7);
+        }
+    }
+}
+
+template <int F, int KG>
+__global__ void __launch_bounds__(LkGeom<KG>::THREADS, LkGeom<KG>::MINB) encode_lanek_kernel(LanekParams p)
 {
     using L = LkField<F>;
+    using G = LkGeom<KG>;
+    constexpr int SG = L::kSG;
+    constexpr int WT = G::WT, TW = G::TW, QS = G::QS;
+    constexpr int KTL = 32 * KG;                               // coded packets per CTA
+    constexpr int GW = KG * kLkWG;                             // gatherer warps
+    constexpr int NT = G::THREADS;
+    constexpr int kQWords = L::kRows * QS;
+    constexpr int kRingRows = SG * kLkSteps;
     extern __shared__ __align__(16) uint32_t smem[];
-    constexpr int kQWords = L::kRows * kLkQS;
     uint32_t *Q = smem;                                        // [2][rows][QS]
-    uint32_t *ring = Q + 2 * kQWords;                          // [S][TW]
-    uint8_t *ccache = reinterpret_cast<uint8_t *>(ring + kLkStages * kLkTW);   // [N][64]
+    uint32_t *ring = Q + 2 * kQWords;                          // [ring rows][TW]
+    uint8_t *ccache = reinterpret_cast<uint8_t *>(ring + kRingRows * TW);   // [steps][KTL]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t bid = blockIdx.x;
@@ -112,125 +160,142 @@ __global__ void __launch_bounds__(kLkThreads, 1) encode_lanek_kernel(LanekParams
     const size_t rest = bid / (size_t)p.k_tiles;
     const int tile = (int)(rest % (size_t)p.tiles);
     const size_t g = rest / (size_t)p.tiles;
-    const int k0 = kt * kLkKT;
-    const uint32_t w0 = (uint32_t)tile * kLkTW;                // first word of the tile
+    const int k0 = kt * KTL;
+    const uint32_t w0 = (uint32_t)tile * TW;                   // first word of the tile
     const uint8_t *Ag = p.A + g * (size_t)p.N * p.M;
+    const int NS = (p.N + SG - 1) / SG;                        // steps
 
-    // zero rows (c_lo = 0, c_hi = 0) of both buffers; coefficient cache
-    for (int t = threadIdx.x; t < kLkQS; t += blockDim.x) {
+    // zero rows (index 0, and 16 for GF(256)) of both buffers; row indices of
+    // every (step, k) from the coefficients (rows past N count as c = 0)
+    for (int t = threadIdx.x; t < QS; t += blockDim.x) {
 #pragma unroll
         for (int b = 0; b < 2; b++) {
             Q[b * kQWords + t] = 0u;
-            if (F == 256) Q[b * kQWords + 16 * kLkQS + t] = 0u;
+            if (F == 256) Q[b * kQWords + 16 * QS + t] = 0u;
         }
     }
-    for (int e = threadIdx.x; e < kLkKT * p.N; e += blockDim.x) {
-        const int i = e / kLkKT, kl = e - i * kLkKT;      // consecutive threads: consecutive k
-        uint8_t c = 0;
-        if (k0 + kl < p.K)
-            c = p.C[(g * (size_t)p.N + (size_t)i) * p.K + (size_t)(k0 + kl)] & (uint8_t)p.qmask;
-        ccache[e] = c;
+    for (int e = threadIdx.x; e < KTL * NS; e += blockDim.x) {
+        const int s = e / KTL, kl = e - s * KTL;               // consecutive threads: consecutive k
+        uint8_t c[SG];
+#pragma unroll
+        for (int j = 0; j < SG; j++) {
+            const int i = s * SG + j;
+            c[j] = (i < p.N && k0 + kl < p.K)
+                       ? (uint8_t)(p.C[(g * (size_t)p.N + (size_t)i) * p.K + (size_t)(k0 + kl)] & p.qmask)
+                       : (uint8_t)0;
+        }
+        ccache[e] = (uint8_t)L::index(c);
     }
     __syncthreads();
 
-    constexpr int NT = kLkThreads;
     constexpr int BAR_FULL = 1, BAR_EMPTY = 3;   // ids 1,2 and 3,4
 
-    if (warp >= kLkGatherWarps) {
-        // ---------------- builders: stream a_i into the ring, write Q[i & 1]
-        const int bt = threadIdx.x - 32 * kLkGatherWarps;      // 0 .. 127
+    if (warp >= GW) {
+        // ---------------- builders: stream the step's sources into the ring, write Q[s & 1]
+        const int bt = threadIdx.x - 32 * GW;                  // 0 .. 127
         const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
-        auto issue = [&](int i) {
-            if (i < p.N) {
-                const uint32_t *row = reinterpret_cast<const uint32_t *>(Ag + (size_t)i * p.M);
-                const uint32_t slot = (uint32_t)(i % kLkStages) * kLkTW;
+        auto issue = [&](int s) {
+            if (s < NS) {
 #pragma unroll
-                for (int j = 0; j < kLkBuildWords; j++) {
-                    const uint32_t tw = (uint32_t)bt + 128u * j;
-                    const uint32_t wd = w0 + tw;
-                    const bool v = wd < p.Mw;
-                    cp_async4(ring_s + (slot + tw) * 4u, v ? row + wd : row, v);
+                for (int j = 0; j < SG; j++) {
+                    const int i = s * SG + j;
+                    const uint32_t *row = reinterpret_cast<const uint32_t *>(Ag + (size_t)min(i, p.N - 1) * p.M);
+                    const uint32_t slot = (uint32_t)((s % kLkSteps) * SG + j) * TW;
+#pragma unroll
+                    for (int u = 0; u < G::BWORDS; u++) {
+                        const uint32_t tw = (uint32_t)bt + 128u * u;
+                        const uint32_t wd = w0 + tw;
+                        const bool v = i < p.N && wd < p.Mw;
+                        cp_async4(ring_s + (slot + tw) * 4u, v ? row + wd : row, v);
+                    }
                 }
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
         };
 #pragma unroll 1
-        for (int s = 0; s < kLkStages - 1; s++) issue(s);
+        for (int s = 0; s < kLkSteps - 1; s++) issue(s);
 #pragma unroll 1
-        for (int i = 0; i < p.N; i++) {
-            issue(i + kLkStages - 1);
-            asm volatile("cp.async.wait_group %0;" :: "n"(kLkStages - 1) : "memory");
-            if (i >= 2) nbar_sync(BAR_EMPTY + (i & 1), NT);     // gatherers done with row i-2
-            uint32_t *q = Q + (i & 1) * kQWords;
-            const uint32_t *slot = ring + (i % kLkStages) * kLkTW;
+        for (int s = 0; s < NS; s++) {
+            issue(s + kLkSteps - 1);
+            asm volatile("cp.async.wait_group %0;" :: "n"(kLkSteps - 1) : "memory");
+            if (s >= 2) nbar_sync(BAR_EMPTY + (s & 1), NT);     // gatherers done with step s-2
+            uint32_t *q = Q + (s & 1) * kQWords;
+            const uint32_t *slot = ring + (s % kLkSteps) * SG * TW;
 #pragma unroll
-            for (int j = 0; j < kLkBuildWords; j++) {
-                const int tw = bt + 128 * j;
-                const uint32_t a = slot[tw];
-                const uint32_t p1 = L::xtime(a), p2 = L::xtime(p1), p3 = L::xtime(p2);
-                store_nibble_products(q + tw, a, p1, p2, p3);
-                if (F == 256) {
-                    const uint32_t p4 = L::xtime(p3), p5 = L::xtime(p4), p6 = L::xtime(p5), p7 = L::xtime(p6);
-                    store_nibble_products(q + 16 * kLkQS + tw, p4, p5, p6, p7);
-                }
+            for (int u = 0; u < G::BWORDS; u++) {
+                const int tw = bt + 128 * u;
+                uint32_t a[SG];
+#pragma unroll
+                for (int j = 0; j < SG; j++) a[j] = slot[j * TW + tw];
+                build_word<F, QS>(q + tw, a);
             }
-            nbar_arrive(BAR_FULL + (i & 1), NT);
+            nbar_arrive(BAR_FULL + (s & 1), NT);
         }
         // consume the gatherers' last two EMPTY signals
-        for (int i = max(p.N, 2); i < p.N + 2; i++) nbar_sync(BAR_EMPTY + (i & 1), NT);
+        for (int s = max(NS, 2); s < NS + 2; s++) nbar_sync(BAR_EMPTY + (s & 1), NT);
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         return;
     }
 
-    // ---------------- gatherers: lane = coded packet k, 48 words per lane
-    const int kl = (warp & 1) * 32 + lane;                     // local k (0..63)
-    const int wg = warp >> 1;                                  // word group (0..7)
-    const uint8_t *ccol = ccache + kl;                        // c of row i at ccol[64 i]
-    uint32_t acc[kLkWT];
+    // ---------------- gatherers: lane = coded packet k, WT words per lane
+    const int kl = (warp % KG) * 32 + lane;                    // local k
+    const int wg = warp / KG;                                  // word group (0..7)
+    const uint8_t *ccol = ccache + kl;                         // row index of step s at ccol[KTL s]
+    uint32_t acc[WT];
 #pragma unroll
-    for (int w = 0; w < kLkWT; w++) acc[w] = 0u;
+    for (int w = 0; w < WT; w++) acc[w] = 0u;
 
 #pragma unroll 1
-    for (int i = 0; i < p.N; i++) {
-        const uint32_t c = ccol[i * kLkKT];
-        nbar_sync(BAR_FULL + (i & 1), NT);
-        const uint32_t *q = Q + (i & 1) * kQWords + wg * kLkWT;
+    for (int s = 0; s < NS; s++) {
+        const uint32_t r = ccol[s * KTL];
+        nbar_sync(BAR_FULL + (s & 1), NT);
+        const uint32_t *q = Q + (s & 1) * kQWords + wg * WT;
         if (F == 256) {
-            const uint32_t *lo = q + (c & 15u) * kLkQS;
-            const uint32_t *hi = q + (16u + (c >> 4)) * kLkQS;
+            const uint32_t *lo = q + (r & 15u) * QS;
+            const uint32_t *hi = q + (16u + (r >> 4)) * QS;
 #pragma unroll
-            for (int w = 0; w < kLkWT; w++) acc[w] ^= lo[w] ^ hi[w];
+            for (int w = 0; w < WT; w++) acc[w] ^= lo[w] ^ hi[w];
         } else {
-            const uint32_t *lo = q + c * kLkQS;
+            const uint32_t *lo = q + r * QS;
 #pragma unroll
-            for (int w = 0; w < kLkWT; w++) acc[w] ^= lo[w];
+            for (int w = 0; w < WT; w++) acc[w] ^= lo[w];
         }
-        nbar_arrive(BAR_EMPTY + (i & 1), NT);
+        nbar_arrive(BAR_EMPTY + (s & 1), NT);
     }
 
     // ---- epilogue: transpose through shared memory so that each warp writes
     // contiguous runs of one coded packet (the Q buffers are free once every
-    // gatherer passed its last row: named barrier over the gatherers only)
-    constexpr int kLkOS = kLkTW + 1;
-    constexpr int kHalves = (2 * L::kRows * kLkQS >= kLkKT * kLkOS) ? 1 : 2;   // GF(16): 2 passes
-    uint32_t *ot = Q;                                           // [64 / kHalves][kLkOS]
-    const uint32_t nw = min((uint32_t)kLkTW, p.Mw - w0);
+    // gatherer passed its last step: named barrier over the gatherers only)
+    constexpr int OS = TW + 1;
+    constexpr int kPasses = (KTL * OS + 2 * kQWords - 1) / (2 * kQWords);
+    constexpr int kRowsPerPass = KTL / kPasses;
+    static_assert(kRowsPerPass * kPasses == KTL && kRowsPerPass % 32 == 0, "epilogue passes");
+    uint32_t *ot = Q;                                           // [rows per pass][OS]
+    const uint32_t nw = min((uint32_t)TW, p.Mw - w0);
 #pragma unroll 1
-    for (int h = 0; h < kHalves; h++) {
-        nbar_sync(5, 32 * kLkGatherWarps);
-        if (kHalves == 1 || (warp & 1) == h) {
-            const int r = kHalves == 1 ? kl : lane;
+    for (int h = 0; h < kPasses; h++) {
+        nbar_sync(5, 32 * GW);
+        if (kl / kRowsPerPass == h) {
+            const int r = kl - h * kRowsPerPass;
 #pragma unroll
-            for (int w = 0; w < kLkWT; w++) ot[r * kLkOS + wg * kLkWT + w] = acc[w];
+            for (int w = 0; w < WT; w++) ot[r * OS + wg * WT + w] = acc[w];
         }
-        nbar_sync(5, 32 * kLkGatherWarps);
-        const int rows = kLkKT / kHalves, kbase = k0 + h * rows;
-        for (int r = warp; r < rows; r += kLkGatherWarps) {
+        nbar_sync(5, 32 * GW);
+        const int kbase = k0 + h * kRowsPerPass;
+        for (int r = warp; r < kRowsPerPass; r += GW) {
             if (kbase + r >= p.K) break;
             uint32_t *row = reinterpret_cast<uint32_t *>(p.B + (g * (size_t)p.K + (size_t)(kbase + r)) * p.M) + w0;
-            for (uint32_t w = lane; w < nw; w += 32) row[w] = ot[r * kLkOS + w];
+            for (uint32_t w = lane; w < nw; w += 32) row[w] = ot[r * OS + w];
         }
     }
+}
+
+template <int F, int KG>
+__host__ __device__ constexpr size_t lk_smem_bytes(int N)
+{
+    using G = LkGeom<KG>;
+    return (size_t)2 * LkField<F>::kRows * G::QS * 4 + (size_t)LkField<F>::kSG * kLkSteps * G::TW * 4 +
+           (size_t)32 * KG * ((N + LkField<F>::kSG - 1) / LkField<F>::kSG);
 }
 
 }  // namespace gfr

@@ -19,7 +19,7 @@
 namespace gfr {
 
 constexpr int kMaxDevices = 64;
-constexpr int kVersion = 110;   // 0.1.10: lane-k encode
+constexpr int kVersion = 113;   // 0.1.13: lane-k encode, all fields
 
 __device__ uint32_t g_dev_tabs[4][256 * kTableWords];
 
@@ -175,30 +175,38 @@ static int launch_encode_field(int field, EncodeParams p, cudaStream_t st)
     }
 }
 
-template <int F>
+template <int F, int KG>
 static int launch_lanek(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M,
                         size_t batch, cudaStream_t st)
 {
+    using G = LkGeom<KG>;
     LanekParams p;
     p.A = A; p.C = C; p.B = B; p.M = M; p.Mw = (uint32_t)(M / 4); p.batch = batch;
     p.N = N; p.K = K; p.qmask = F - 1;
-    p.tiles = (int)((p.Mw + kLkTW - 1) / kLkTW);
-    p.k_tiles = (K + kLkKT - 1) / kLkKT;
-    p.ncpad = (N + 3) & ~3;
+    p.tiles = (int)((p.Mw + G::TW - 1) / G::TW);
+    p.k_tiles = (K + 32 * KG - 1) / (32 * KG);
     const size_t grid = batch * (size_t)p.tiles * (size_t)p.k_tiles;
     if (grid > 0x7FFFFFFFu) return GF_EARG;
-    const size_t smem = (size_t)2 * LkField<F>::kRows * kLkQS * 4 + (size_t)kLkStages * kLkTW * 4 +
-                        (size_t)kLkKT * p.N;
+    const size_t smem = lk_smem_bytes<F, KG>(N);
     if (smem > 227 * 1024) return GF_EARG;
-    if (cudaFuncSetAttribute(encode_lanek_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(encode_lanek_kernel<F, KG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
         return GF_ECUDA;
-    encode_lanek_kernel<F><<<(unsigned)grid, kLkThreads, smem, st>>>(p);
+    encode_lanek_kernel<F, KG><<<(unsigned)grid, G::THREADS, smem, st>>>(p);
     return launch_status();
 }
 
-// encode path: "lanek" (shared-memory product tables, k on lanes) for GF(16) /
-// GF(256) with K >= 32 on word-aligned packets; the column kernel otherwise.
+template <int F>
+static int launch_lanek_kg(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M,
+                           size_t batch, cudaStream_t st)
+{
+    return K > 32 ? launch_lanek<F, 2>(A, C, B, N, K, M, batch, st)
+                  : launch_lanek<F, 1>(A, C, B, N, K, M, batch, st);
+}
+
+// encode path: "lanek" (shared-memory product tables, k on lanes) when K >= 24
+// on word-aligned packets (enough coded packets to fill the lanes); the column
+// kernel otherwise.
 // GFRLNC_ENCODE_PATH=column|lanek overrides (experiments).
 static int encode_path_override()
 {
@@ -219,11 +227,16 @@ static int encode_on_stream(int field, int fi, const uint8_t *A, const uint8_t *
         const bool aligned = M % 4 == 0 && (reinterpret_cast<uintptr_t>(A) & 3u) == 0 &&
                              (reinterpret_cast<uintptr_t>(B) & 3u) == 0 && M / 4 < 0xFFFFFFFFull;
         const int ov = encode_path_override();
-        const bool lanek = (field == 16 || field == 256) && aligned &&
-                           (ov == 2 || (ov == 0 && K >= 32));
-        if (lanek)
-            return field == 256 ? launch_lanek<256>(A, C, B, N, K, M, batch, st)
-                                : launch_lanek<16>(A, C, B, N, K, M, batch, st);
+        const bool lanek = aligned && (ov == 2 || (ov == 0 && K >= 24));
+        if (lanek) {
+            switch (field) {
+            case 256: return launch_lanek_kg<256>(A, C, B, N, K, M, batch, st);
+            case 16: return launch_lanek_kg<16>(A, C, B, N, K, M, batch, st);
+            case 4: return launch_lanek_kg<4>(A, C, B, N, K, M, batch, st);
+            case 2: return launch_lanek_kg<2>(A, C, B, N, K, M, batch, st);
+            default: return GF_EFIELD;
+            }
+        }
     }
     EncodeParams p;
     std::memset(&p, 0, sizeof(p));
