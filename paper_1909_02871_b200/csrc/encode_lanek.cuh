@@ -24,7 +24,7 @@
 //     the same source word (<= 16 distinct rows; odd row stride puts them in
 //     distinct banks: one wavefront); WT words per lane accumulate in
 //     registers;
-//   * Q is double-buffered between builders and gatherers (named barriers
+//   * Q is triple-buffered between builders and gatherers (named barriers
 //     FULL / EMPTY); builders also stream the source tile HBM -> smem with a
 //     cp.async ring several steps deep.
 // Per (step, k, word): 1 LDS + 1 LOP3 (GF(256): 2 LDS + 1 LOP3); the table
@@ -45,6 +45,7 @@ namespace gfr {
 constexpr int kLkWG = 8;                  // word groups (gatherer warps per k-group)
 constexpr int kLkBuildWarps = 4;
 constexpr int kLkSteps = 4;               // cp.async ring depth in steps
+constexpr int kLkNQ = 3;                  // Q buffers between builders and gatherers
 
 template <int KG> struct LkGeom {
     static constexpr int WT = KG == 1 ? 32 : 48;          // words per gatherer lane
@@ -150,8 +151,8 @@ __global__ void __launch_bounds__(LkGeom<KG>::THREADS, LkGeom<KG>::MINB) encode_
     constexpr int kQWords = L::kRows * QS;
     constexpr int kRingRows = SG * kLkSteps;
     extern __shared__ __align__(16) uint32_t smem[];
-    uint32_t *Q = smem;                                        // [2][rows][QS]
-    uint32_t *ring = Q + 2 * kQWords;                          // [ring rows][TW]
+    uint32_t *Q = smem;                                        // [NQ][rows][QS]
+    uint32_t *ring = Q + kLkNQ * kQWords;                      // [ring rows][TW]
     uint8_t *ccache = reinterpret_cast<uint8_t *>(ring + kRingRows * TW);   // [steps][KTL]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -165,11 +166,11 @@ __global__ void __launch_bounds__(LkGeom<KG>::THREADS, LkGeom<KG>::MINB) encode_
     const uint8_t *Ag = p.A + g * (size_t)p.N * p.M;
     const int NS = (p.N + SG - 1) / SG;                        // steps
 
-    // zero rows (index 0, and 16 for GF(256)) of both buffers; row indices of
+    // zero rows (index 0, and 16 for GF(256)) of every buffer; row indices of
     // every (step, k) from the coefficients (rows past N count as c = 0)
     for (int t = threadIdx.x; t < QS; t += blockDim.x) {
 #pragma unroll
-        for (int b = 0; b < 2; b++) {
+        for (int b = 0; b < kLkNQ; b++) {
             Q[b * kQWords + t] = 0u;
             if (F == 256) Q[b * kQWords + 16 * QS + t] = 0u;
         }
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(LkGeom<KG>::THREADS, LkGeom<KG>::MINB) encode_
     }
     __syncthreads();
 
-    constexpr int BAR_FULL = 1, BAR_EMPTY = 3;   // ids 1,2 and 3,4
+    constexpr int BAR_FULL = 1, BAR_EMPTY = 1 + kLkNQ, BAR_EPI = 1 + 2 * kLkNQ;   // named barrier ids
 
     if (warp >= GW) {
         // ---------------- builders: stream the step's sources into the ring, write Q[s & 1]
@@ -218,8 +219,9 @@ __global__ void __launch_bounds__(LkGeom<KG>::THREADS, LkGeom<KG>::MINB) encode_
         for (int s = 0; s < NS; s++) {
             issue(s + kLkSteps - 1);
             asm volatile("cp.async.wait_group %0;" :: "n"(kLkSteps - 1) : "memory");
-            if (s >= 2) nbar_sync(BAR_EMPTY + (s & 1), NT);     // gatherers done with step s-2
-            uint32_t *q = Q + (s & 1) * kQWords;
+            const int b = s % kLkNQ;
+            if (s >= kLkNQ) nbar_sync(BAR_EMPTY + b, NT);       // gatherers done with step s-NQ
+            uint32_t *q = Q + b * kQWords;
             const uint32_t *slot = ring + (s % kLkSteps) * SG * TW;
 #pragma unroll
             for (int u = 0; u < G::BWORDS; u++) {
@@ -229,10 +231,10 @@ __global__ void __launch_bounds__(LkGeom<KG>::THREADS, LkGeom<KG>::MINB) encode_
                 for (int j = 0; j < SG; j++) a[j] = slot[j * TW + tw];
                 build_word<F, QS>(q + tw, a);
             }
-            nbar_arrive(BAR_FULL + (s & 1), NT);
+            nbar_arrive(BAR_FULL + b, NT);
         }
-        // consume the gatherers' last two EMPTY signals
-        for (int s = max(NS, 2); s < NS + 2; s++) nbar_sync(BAR_EMPTY + (s & 1), NT);
+        // consume the gatherers' last NQ EMPTY signals
+        for (int s = max(NS, kLkNQ); s < NS + kLkNQ; s++) nbar_sync(BAR_EMPTY + s % kLkNQ, NT);
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         return;
     }
@@ -248,8 +250,9 @@ __global__ void __launch_bounds__(LkGeom<KG>::THREADS, LkGeom<KG>::MINB) encode_
 #pragma unroll 1
     for (int s = 0; s < NS; s++) {
         const uint32_t r = ccol[s * KTL];
-        nbar_sync(BAR_FULL + (s & 1), NT);
-        const uint32_t *q = Q + (s & 1) * kQWords + wg * WT;
+        const int b = s % kLkNQ;
+        nbar_sync(BAR_FULL + b, NT);
+        const uint32_t *q = Q + b * kQWords + wg * WT;
         if (F == 256) {
             const uint32_t *lo = q + (r & 15u) * QS;
             const uint32_t *hi = q + (16u + (r >> 4)) * QS;
@@ -260,27 +263,27 @@ __global__ void __launch_bounds__(LkGeom<KG>::THREADS, LkGeom<KG>::MINB) encode_
 #pragma unroll
             for (int w = 0; w < WT; w++) acc[w] ^= lo[w];
         }
-        nbar_arrive(BAR_EMPTY + (s & 1), NT);
+        nbar_arrive(BAR_EMPTY + b, NT);
     }
 
     // ---- epilogue: transpose through shared memory so that each warp writes
     // contiguous runs of one coded packet (the Q buffers are free once every
     // gatherer passed its last step: named barrier over the gatherers only)
     constexpr int OS = TW + 1;
-    constexpr int kPasses = (KTL * OS + 2 * kQWords - 1) / (2 * kQWords);
+    constexpr int kPasses = (KTL * OS + kLkNQ * kQWords - 1) / (kLkNQ * kQWords);
     constexpr int kRowsPerPass = KTL / kPasses;
     static_assert(kRowsPerPass * kPasses == KTL && kRowsPerPass % 32 == 0, "epilogue passes");
     uint32_t *ot = Q;                                           // [rows per pass][OS]
     const uint32_t nw = min((uint32_t)TW, p.Mw - w0);
 #pragma unroll 1
     for (int h = 0; h < kPasses; h++) {
-        nbar_sync(5, 32 * GW);
+        nbar_sync(BAR_EPI, 32 * GW);
         if (kl / kRowsPerPass == h) {
             const int r = kl - h * kRowsPerPass;
 #pragma unroll
             for (int w = 0; w < WT; w++) ot[r * OS + wg * WT + w] = acc[w];
         }
-        nbar_sync(5, 32 * GW);
+        nbar_sync(BAR_EPI, 32 * GW);
         const int kbase = k0 + h * kRowsPerPass;
         for (int r = warp; r < kRowsPerPass; r += GW) {
             if (kbase + r >= p.K) break;
@@ -294,7 +297,7 @@ template <int F, int KG>
 __host__ __device__ constexpr size_t lk_smem_bytes(int N)
 {
     using G = LkGeom<KG>;
-    return (size_t)2 * LkField<F>::kRows * G::QS * 4 + (size_t)LkField<F>::kSG * kLkSteps * G::TW * 4 +
+    return (size_t)kLkNQ * LkField<F>::kRows * G::QS * 4 + (size_t)LkField<F>::kSG * kLkSteps * G::TW * 4 +
            (size_t)32 * KG * ((N + LkField<F>::kSG - 1) / LkField<F>::kSG);
 }
 
