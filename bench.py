@@ -321,31 +321,10 @@ def main():
     # the timed region is one); algorithmic work per launch / mean duration
     avg_kernel_s = statistics.mean(kern_ms) / 1e3
     gens_per_launch = chunk
-    bm_per_launch = N * K * Ms * gens_per_launch
-    ops = bm_per_launch * OPS_PER_BYTE_MADD[q]
-    alu_peak_tops = N_SM * ALU_LANES_PER_SM_CLK * peaks["sm_max_mhz"] * 1e6 / 1e12
-    alu_achieved = ops / avg_kernel_s / 1e12
-    hbm_bytes = per_gen * gens_per_launch
-    hbm_achieved = hbm_bytes / avg_kernel_s / 1e9
-    alu_frac = alu_achieved / alu_peak_tops
-    hbm_frac = hbm_achieved / peaks["hbm_gbs"]
-    traffic = lookup_traffic(q, cfg, gens_per_launch, Ms, gf.version())
-    if alu_frac >= hbm_frac:
-        roof = {"bound": "alu", "achieved": round(alu_achieved, 3), "peak": round(alu_peak_tops, 3),
-                "unit": "Tops/s", "frac": round(alu_frac, 4),
-                "peak_source": f"{N_SM} SMs x {ALU_LANES_PER_SM_CLK} ALU-pipe lanes/clk x "
-                               f"{peaks['sm_max_mhz']:.0f} MHz (DESIGN.md 'roofline')",
-                "ops_per_byte_madd": OPS_PER_BYTE_MADD[q]}
-    else:
-        roof = {"bound": "hbm", "achieved": round(hbm_achieved, 1), "peak": peaks["hbm_gbs"],
-                "unit": "GB/s", "frac": round(hbm_frac, 4), "peak_source": peaks["source"]}
-    roof["traffic"] = traffic
-    roof["kernel"] = f"encode_kernel<F={q}>"
+    path = gf.encode_path(q, N, K, Ms)
+    roof, hbm = dominant_roofline(q, N, K, Ms, gens_per_launch, path, avg_kernel_s, peaks)
+    roof["traffic"] = lookup_traffic(q, cfg, gens_per_launch, Ms, gf.version())
     roof["kernel_ms"] = round(statistics.mean(kern_ms), 4)
-    roof["byte_madds_per_launch"] = bm_per_launch
-    roof["hbm_bytes_per_launch"] = hbm_bytes
-    hbm = {"achieved": round(hbm_achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-           "frac": round(hbm_frac, 4), "peak_source": peaks["source"]}
     del A, Cm, B
     torch.cuda.empty_cache()
 
@@ -387,6 +366,55 @@ def main():
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+SMEM_BYTES_PER_SM_CLK = 128   # shared-memory crossbar (B300_MICROARCH.md; tools/ubench_smem.cu)
+LANEK = {2: (4, 1, 15), 4: (2, 1, 15), 16: (1, 1, 15), 256: (1, 2, 30)}   # SG, gathers/unit, build rows
+
+
+def dominant_roofline(q, N, K, Ms, gens, path, kernel_s, peaks):
+    """Roofline of the encode launch.
+
+    lane-k kernels are bound by the shared-memory pipe: algorithmic smem bytes
+    = gathers (4 B per gathered word, G per (step, k, word)) + table build
+    (R rows x 4 B per (step, word), once per CTA k-tile); peak = 148 SMs x
+    128 B/clk x max SM clock.  Column kernels are bound by the ALU pipe:
+    byte-madds x ops per byte-madd of the method; peak = 148 x 64 lanes/clk x
+    clock.  Both carry the HBM view (read A, write B, read C)."""
+    clk = peaks["sm_max_mhz"] * 1e6
+    bm = N * K * Ms * gens
+    hbm_bytes = ((N + K) * Ms + N * K) * gens
+    hbm_ach = hbm_bytes / kernel_s / 1e9
+    hbm = {"achieved": round(hbm_ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+           "frac": round(hbm_ach / peaks["hbm_gbs"], 4), "peak_source": peaks["source"]}
+    if path.startswith("lanek"):
+        SG, G, R = LANEK[q]
+        ktl = 64 if path == "lanek-64" else 32
+        steps = -(-N // SG)
+        k_tiles = -(-K // ktl)
+        smem_bytes = gens * steps * (Ms // 4) * 4 * (K * G + R * k_tiles)
+        peak = N_SM * SMEM_BYTES_PER_SM_CLK * clk
+        ach = smem_bytes / kernel_s
+        roof = {"bound": "smem", "achieved": round(ach / 1e12, 3), "peak": round(peak / 1e12, 3),
+                "unit": "TB/s", "frac": round(ach / peak, 4),
+                "peak_source": f"{N_SM} SMs x {SMEM_BYTES_PER_SM_CLK} B/clk shared-memory pipe x "
+                               f"{peaks['sm_max_mhz']:.0f} MHz (DESIGN.md 'roofline')",
+                "smem_bytes_per_launch": smem_bytes}
+    else:
+        ops = bm * OPS_PER_BYTE_MADD[q]
+        peak = N_SM * ALU_LANES_PER_SM_CLK * clk
+        ach = ops / kernel_s
+        roof = {"bound": "alu", "achieved": round(ach / 1e12, 3), "peak": round(peak / 1e12, 3),
+                "unit": "Tops/s", "frac": round(ach / peak, 4),
+                "peak_source": f"{N_SM} SMs x {ALU_LANES_PER_SM_CLK} ALU-pipe lanes/clk x "
+                               f"{peaks['sm_max_mhz']:.0f} MHz (DESIGN.md 'roofline')",
+                "ops_per_byte_madd": OPS_PER_BYTE_MADD[q]}
+    if hbm["frac"] > roof["frac"]:
+        roof = dict(hbm, bound="hbm")
+    roof["kernel"] = f"encode {path} GF({q})"
+    roof["byte_madds_per_launch"] = bm
+    roof["hbm_bytes_per_launch"] = hbm_bytes
+    return roof, hbm
 
 
 def lookup_traffic(q, cfg, gens, Ms, lib_version):

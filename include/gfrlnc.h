@@ -124,6 +124,14 @@ int gf_fill_random2d(uint8_t *dst, size_t rows, size_t cols, uint64_t seed, uint
  * PAPER.md:245,266).  Returns GF_OK, GF_EFIELD or GF_EARG (cap too small). */
 int gf_host_tables(int field, uint32_t *out, size_t cap_words);
 
+/* Host-only introspection (harness / roofline accounting): which encode kernel
+ * gf_encode_batch launches for these arguments, given the byte offsets of A
+ * and B modulo 16.  Returns 0 = column kernel on 32-bit words, 1 = column
+ * kernel on bytes (unaligned or M % 4 != 0), 2 = lane-k kernel with 32 coded
+ * packets per CTA, 3 = lane-k kernel with 64, or
+ * GF_EFIELD / GF_EARG. */
+int gf_encode_path(int field, int N, int K, size_t M, size_t a_align, size_t b_align);
+
 /* Library version (major * 10000 + minor * 100 + patch). */
 int gf_version(void);
 

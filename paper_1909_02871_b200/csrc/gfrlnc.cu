@@ -220,15 +220,21 @@ static int encode_path_override()
     return v;
 }
 
+// 0 column (words), 1 column (bytes), 2 lane-k KG=1, 3 lane-k KG=2
+static int encode_path(int K, size_t M, const void *A, const void *B)
+{
+    const bool aligned = M % 4 == 0 && (reinterpret_cast<uintptr_t>(A) & 3u) == 0 &&
+                         (reinterpret_cast<uintptr_t>(B) & 3u) == 0 && M / 4 < 0xFFFFFFFFull;
+    const int ov = encode_path_override();
+    if (aligned && (ov == 2 || (ov == 0 && K >= 24))) return K > 32 ? 3 : 2;
+    return aligned ? 0 : 1;
+}
+
 static int encode_on_stream(int field, int fi, const uint8_t *A, const uint8_t *C, uint8_t *B,
                             int N, int K, size_t M, size_t batch, cudaStream_t st)
 {
     {
-        const bool aligned = M % 4 == 0 && (reinterpret_cast<uintptr_t>(A) & 3u) == 0 &&
-                             (reinterpret_cast<uintptr_t>(B) & 3u) == 0 && M / 4 < 0xFFFFFFFFull;
-        const int ov = encode_path_override();
-        const bool lanek = aligned && (ov == 2 || (ov == 0 && K >= 24));
-        if (lanek) {
+        if (encode_path(K, M, A, B) >= 2) {
             switch (field) {
             case 256: return launch_lanek_kg<256>(A, C, B, N, K, M, batch, st);
             case 16: return launch_lanek_kg<16>(A, C, B, N, K, M, batch, st);
@@ -305,6 +311,14 @@ using namespace gfr;
 extern "C" {
 
 int gf_version(void) { return kVersion; }
+
+int gf_encode_path(int field, int N, int K, size_t M, size_t a_align, size_t b_align)
+{
+    if (field_index(field) < 0) return GF_EFIELD;
+    if (N < 1 || K < 1) return GF_EARG;
+    return encode_path(K, M, reinterpret_cast<const void *>(a_align & 15u),
+                       reinterpret_cast<const void *>(b_align & 15u));
+}
 
 const char *gf_strerror(int status)
 {

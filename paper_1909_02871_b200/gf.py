@@ -43,6 +43,7 @@ _lib.gf_fill_random.argtypes = [_u8p, _sz, _u64, _u64, _u64, ctypes.c_uint8]
 _lib.gf_fill_random2d.argtypes = [_u8p, _sz, _sz, _u64, _u64, _u64, _u64, ctypes.c_uint8]
 _lib.gf_host_tables.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_uint32), _sz]
 _lib.gf_version.argtypes = []
+_lib.gf_encode_path.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _sz, _sz, _sz]
 
 GF_OK, GF_EFIELD, GF_ECOEFF, GF_EARG, GF_EOVERLAP, GF_ENOINIT, GF_ECUDA = 0, -1, -2, -3, -4, -5, -6
 FIELDS = (2, 4, 16, 256)
@@ -51,7 +52,7 @@ TABLE_WORDS = 16          # uint32 words per coefficient in gf_host_tables
 # every symbol include/gfrlnc.h declares (tests check the library exports them)
 ABI_SYMBOLS = ("gf_init", "gf_maddrc", "gf_mulrc", "gf_encode_batch", "gf_encode_batch_host",
                "gf_set_stream", "gf_strerror", "gf_fill_random", "gf_fill_random2d",
-               "gf_host_tables", "gf_version")
+               "gf_host_tables", "gf_version", "gf_encode_path")
 
 
 class GFError(RuntimeError):
@@ -70,6 +71,17 @@ def strerror(status: int) -> str:
 
 def version() -> int:
     return _lib.gf_version()
+
+
+ENCODE_PATHS = {0: "column-words", 1: "column-bytes", 2: "lanek-32", 3: "lanek-64"}
+
+
+def encode_path(field: int, N: int, K: int, M: int, a_align: int = 0, b_align: int = 0) -> str:
+    """Name of the encode kernel gf_encode_batch picks (host-only query)."""
+    rc = _lib.gf_encode_path(field, N, K, M, a_align, b_align)
+    if rc < 0:
+        raise GFError(rc, "gf_encode_path")
+    return ENCODE_PATHS[rc]
 
 
 def _check(rc: int, what: str) -> None:

@@ -191,3 +191,13 @@ def test_gf16_permuted_imul_matches_prmt_order():
             s0, s1, s2 = make_sel(x)
             T = tabs[c]
             assert imul_word(16, T, xp) == prmt(T[0], T[1], s0) ^ prmt(T[2], T[3], s1) ^ prmt(T[4], T[4], s2)
+
+
+def test_encode_path_query():
+    assert gf.encode_path(256, 64, 64, 1500) == "lanek-64"
+    assert gf.encode_path(2, 32, 32, 1 << 20) == "lanek-32"
+    assert gf.encode_path(256, 16, 1, 1500) == "column-words"
+    assert gf.encode_path(4, 3, 5, 13) == "column-bytes"
+    assert gf.encode_path(256, 64, 64, 1500, a_align=1) == "column-bytes"
+    with pytest.raises(gf.GFError):
+        gf.encode_path(3, 1, 1, 4)
