@@ -117,7 +117,26 @@ def _coeff(c: int) -> int:
 
 
 def _use_stream(device: torch.device) -> None:
-    _lib.gf_set_stream(ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream))
+    _lib.gf_set_stream(torch.cuda.current_stream(device).cuda_stream)
+
+
+class _on_device:
+    """Make `device` current for the call (cheap no-op when it already is)."""
+    __slots__ = ("idx", "prev")
+
+    def __init__(self, device: torch.device):
+        self.idx = device.index if device.index is not None else torch.cuda.current_device()
+
+    def __enter__(self):
+        self.prev = torch.cuda.current_device()
+        if self.prev != self.idx:
+            torch.cuda.set_device(self.idx)
+        return self
+
+    def __exit__(self, *exc):
+        if self.prev != self.idx:
+            torch.cuda.set_device(self.prev)
+        return False
 
 
 def init(field: int, device=None) -> None:
@@ -131,7 +150,7 @@ def maddrc(field: int, dst: torch.Tensor, src: torch.Tensor, coeff: int) -> torc
     pd, ps = _dev_u8(dst, "dst"), _dev_u8(src, "src")
     if dst.numel() != src.numel():
         raise ValueError("dst and src must have the same number of bytes")
-    with torch.cuda.device(dst.device):
+    with _on_device(dst.device):
         _use_stream(dst.device)
         _check(_lib.gf_maddrc(field, pd, ps, _coeff(coeff), dst.numel()), "gf_maddrc")
     return dst
@@ -140,7 +159,7 @@ def maddrc(field: int, dst: torch.Tensor, src: torch.Tensor, coeff: int) -> torc
 def mulrc(field: int, dst: torch.Tensor, coeff: int) -> torch.Tensor:
     """dst = coeff * dst in place. Returns dst."""
     pd = _dev_u8(dst, "dst")
-    with torch.cuda.device(dst.device):
+    with _on_device(dst.device):
         _use_stream(dst.device)
         _check(_lib.gf_mulrc(field, pd, _coeff(coeff), dst.numel()), "gf_mulrc")
     return dst
@@ -165,7 +184,7 @@ def encode_batch(field: int, A: torch.Tensor, C: torch.Tensor, B: torch.Tensor |
     pa, pc, pb = _dev_u8(A, "A"), _dev_u8(C, "C"), _dev_u8(B, "B")
     if checked and C.numel() and int(C.max()) >= field:
         raise GFError(GF_ECOEFF, "encode_batch(checked)")
-    with torch.cuda.device(A.device):
+    with _on_device(A.device):
         _use_stream(A.device)
         _check(_lib.gf_encode_batch(field, pa, pc, pb, N, K, M, batch), "gf_encode_batch")
     return B
@@ -195,7 +214,7 @@ def host_workspace_bytes(N: int, K: int, M: int, gens_per_chunk: int) -> int:
 def fill_random(dst: torch.Tensor, seed: int, stream: int, offset: int = 0, mask: int = 0xFF) -> torch.Tensor:
     """dst[j] = byte(seed, stream, offset + j) & mask (seeded_inputs definition)."""
     p = _dev_u8(dst, "dst")
-    with torch.cuda.device(dst.device):
+    with _on_device(dst.device):
         _use_stream(dst.device)
         _check(_lib.gf_fill_random(p, dst.numel(), seed, stream, offset, mask), "gf_fill_random")
     return dst
@@ -208,7 +227,7 @@ def fill_random2d(dst: torch.Tensor, seed: int, stream: int, base: int, row_stri
     p = _dev_u8(dst, "dst")
     cols = dst.shape[-1] if dst.dim() else 1
     rows = dst.numel() // cols if cols else 0
-    with torch.cuda.device(dst.device):
+    with _on_device(dst.device):
         _use_stream(dst.device)
         _check(_lib.gf_fill_random2d(p, rows, cols, seed, stream, base, row_stride, mask),
                "gf_fill_random2d")

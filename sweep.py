@@ -90,10 +90,28 @@ def main():
         C = torch.from_numpy(Chh).to(dev)
         B = torch.empty((1, cfg.K, cfg.M), dtype=torch.uint8, device=dev)
         med, best, n = timed(torch, lambda: gf.encode_batch(256, A, C, B), st, min_reps=1000)
+        # device time per call without the Python/ctypes submission cost:
+        # capture 100 calls in a CUDA graph and replay it
+        reps = 100
+        g = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(st)
+        with torch.cuda.stream(cap):
+            gf.encode_batch(256, A, C, B)
+            with torch.cuda.graph(g, stream=cap):
+                for _ in range(reps):
+                    gf.encode_batch(256, A, C, B)
+        st.wait_stream(cap)
+        gmed, gbest, gn = timed(torch, g.replay, st, min_reps=50)
         emit({"config": "C1", "field": 256, "us_per_call_median": round(med * 1e3, 3),
               "us_per_call_best": round(best * 1e3, 3), "reps": n,
+              "us_per_call_graph": round(gmed * 1e3 / reps, 3),
               "source_GBps": round(cfg.source_bytes() / (med / 1e3) / 1e9, 3),
-              "note": "launch-latency bound (25.5 KB per call), L2-resident"})
+              "source_GBps_graph": round(cfg.source_bytes() / (gmed / reps / 1e3) / 1e9, 3),
+              "path": gf.encode_path(256, cfg.N, cfg.K, cfg.M),
+              "note": "launch-latency bound (25.5 KB per call), L2-resident; per-call = one "
+                      "gf_encode_batch through ctypes incl. submission; graph = 100 calls "
+                      "captured in a CUDA graph, device time per call"})
 
     if "C2" in todo:
         nmax = si.C2_SIZES[-1]
@@ -147,6 +165,33 @@ def main():
                   "hbm_frac": round(per_gen * chunk / (med / 1e3) / 1e9 / peaks["hbm_gbs"], 4),
                   "alu_frac": round(bm * OPS_PER_BYTE_MADD[q] / (med / 1e3) / alu_peak, 4)})
         del A, B, C
+        torch.cuda.empty_cache()
+
+    if "NEXT2" in todo:
+        # paper-shaped sweep (Fig. 2): random linear
+        # combinations of N=16 packets, K=1 coded packet, packet sizes 128 B ..
+        # 64 KiB, all fields; enough generations per launch for ~2 GiB of source.
+        # Coded throughput in Gbit/s is the paper's unit (X13).
+        for q in (2, 4, 16, 256):
+            for size in [128 << j for j in range(10)]:
+                N, K = 16, 1
+                gens = max(1, (2 << 30) // (N * size))
+                A = torch.empty((gens, N, size), dtype=torch.uint8, device=dev)
+                C = torch.empty((gens, N, K), dtype=torch.uint8, device=dev)
+                B = torch.empty((gens, K, size), dtype=torch.uint8, device=dev)
+                gf.fill_random(A, 77, si.STREAM_A, 0)
+                gf.fill_random(C, 77, si.STREAM_C, 0, mask=q - 1)
+                med, best, reps = timed(torch, lambda: gf.encode_batch(q, A, C, B), st, min_reps=10,
+                                        min_s=0.3)
+                src_b = gens * N * size
+                hbm = gens * ((N + K) * size + N * K)
+                emit({"config": "NEXT2", "field": q, "packet_bytes": size, "N": N, "K": K,
+                      "gens_per_launch": gens, "ms_median": round(med, 4),
+                      "source_GBps": round(src_b / (med / 1e3) / 1e9, 2),
+                      "coded_Gbitps": round(gens * K * size * 8 / (med / 1e3) / 1e9, 2),
+                      "hbm_frac": round(hbm / (med / 1e3) / 1e9 / peaks["hbm_gbs"], 4),
+                      "path": gf.encode_path(q, N, K, size)})
+                del A, B, C
         torch.cuda.empty_cache()
 
     emit({"clocks": sampler.stop()})
