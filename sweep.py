@@ -124,14 +124,18 @@ def main():
             for n in si.C2_SIZES:
                 s, d = src[:n], dst[:n]
                 for op in ("maddrc", "mulrc"):
-                    fn = (lambda: gf.maddrc(q, d, s, c)) if op == "maddrc" else (lambda: gf.mulrc(q, d, c))
-                    traffic = 3 * n if op == "maddrc" else 2 * n
+                    # GF(2) mulrc by c = 1 is a no-op (nothing launched): time c = 0
+                    # (the zeroing kernel, write-only) instead
+                    cm = 0 if (op == "mulrc" and q == 2) else c
+                    fn = (lambda: gf.maddrc(q, d, s, c)) if op == "maddrc" else (lambda: gf.mulrc(q, d, cm))
+                    traffic = 3 * n if op == "maddrc" else (n if cm == 0 else 2 * n)
                     resident = traffic < 2 * l2
                     modes = [("hbm", flush)] + ([("l2", None)] if resident else [])
                     for mode, fl in modes:
                         med, best, reps = timed(torch, fn, st, flush=fl,
                                                 min_s=0.2 if n < (1 << 20) else 0.5)
-                        rec = {"config": "C2", "op": op, "field": q, "coeff": c, "bytes": n,
+                        rec = {"config": "C2", "op": op, "field": q, "coeff": c if op == "maddrc" else cm,
+                               "bytes": n,
                                "mode": mode, "us_median": round(med * 1e3, 3), "reps": reps,
                                "source_GBps": round(n / (med / 1e3) / 1e9, 3),
                                "hbm_GBps": round(traffic / (med / 1e3) / 1e9, 2)}
