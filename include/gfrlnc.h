@@ -128,8 +128,8 @@ int gf_host_tables(int field, uint32_t *out, size_t cap_words);
  * gf_encode_batch launches for these arguments, given the byte offsets of A
  * and B modulo 16.  Returns 0 = column kernel on 32-bit words, 1 = column
  * kernel on bytes (unaligned or M % 4 != 0), 2 = lane-k kernel with 32 coded
- * packets per CTA, 3 = lane-k kernel with 64, or
- * GF_EFIELD / GF_EARG. */
+ * packets per CTA, 3 = lane-k kernel with 64, 4 / 5 = fused lane-k + column
+ * kernel with 32 / 64, or GF_EFIELD / GF_EARG. */
 int gf_encode_path(int field, int N, int K, size_t M, size_t a_align, size_t b_align);
 
 /* Library version (major * 10000 + minor * 100 + patch). */

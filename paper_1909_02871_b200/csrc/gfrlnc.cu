@@ -12,6 +12,7 @@
 #include "../../include/gfrlnc.h"
 #include "encode_kernels.cuh"
 #include "encode_lanek.cuh"
+#include "encode_fused.cuh"
 #include "region_kernels.cuh"
 #include "rng_kernels.cuh"
 #include "tables.h"
@@ -19,7 +20,7 @@
 namespace gfr {
 
 constexpr int kMaxDevices = 64;
-constexpr int kVersion = 113;   // 0.1.13: lane-k encode, all fields
+constexpr int kVersion = 121;   // 0.1.21: lane-k default, fused opt-in
 
 __device__ uint32_t g_dev_tabs[4][256 * kTableWords];
 
@@ -196,6 +197,27 @@ static int launch_lanek(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, i
     return launch_status();
 }
 
+template <int F, int KG, int WGL, int CWS>
+static int launch_fused(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M,
+                        size_t batch, cudaStream_t st, const uint32_t *tabs)
+{
+    using G = FuGeom<KG, WGL, CWS>;
+    LanekParams p;
+    p.A = A; p.C = C; p.B = B; p.M = M; p.Mw = (uint32_t)(M / 4); p.batch = batch;
+    p.N = N; p.K = K; p.qmask = F - 1;
+    p.tiles = (int)((p.Mw + G::TW - 1) / G::TW);
+    p.k_tiles = (K + G::KTL - 1) / G::KTL;
+    const size_t grid = batch * (size_t)p.tiles * (size_t)p.k_tiles;
+    if (grid > 0x7FFFFFFFu) return GF_EARG;
+    const size_t smem = fu_smem_bytes<F, KG, WGL, CWS>(N);
+    if (smem > 227 * 1024) return GF_EARG;
+    if (cudaFuncSetAttribute(encode_fused_kernel<F, KG, WGL, CWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return GF_ECUDA;
+    encode_fused_kernel<F, KG, WGL, CWS><<<(unsigned)grid, G::THREADS, smem, st>>>(p, tabs);
+    return launch_status();
+}
+
 template <int F>
 static int launch_lanek_kg(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M,
                            size_t batch, cudaStream_t st)
@@ -215,26 +237,52 @@ static int encode_path_override()
         if (!e) return 0;
         if (!strcmp(e, "column")) return 1;
         if (!strcmp(e, "lanek")) return 2;
+        if (!strcmp(e, "fused")) return 3;
         return 0;
     }();
     return v;
 }
 
-// 0 column (words), 1 column (bytes), 2 lane-k KG=1, 3 lane-k KG=2
-static int encode_path(int K, size_t M, const void *A, const void *B)
+// 0 column (words), 1 column (bytes), 2 lane-k KG=1, 3 lane-k KG=2,
+// 4 fused KG=1, 5 fused KG=2.  The fused kernel (lane-k + column warps on one
+// tile) is correct but measured slower than lane-k alone (per-step barrier
+// coupling of the two roles): opt-in via GFRLNC_ENCODE_PATH=fused.
+static int encode_path(int field, int K, size_t M, const void *A, const void *B)
 {
     const bool aligned = M % 4 == 0 && (reinterpret_cast<uintptr_t>(A) & 3u) == 0 &&
                          (reinterpret_cast<uintptr_t>(B) & 3u) == 0 && M / 4 < 0xFFFFFFFFull;
     const int ov = encode_path_override();
-    if (aligned && (ov == 2 || (ov == 0 && K >= 24))) return K > 32 ? 3 : 2;
-    return aligned ? 0 : 1;
+    if (!aligned) return 1;
+    if (ov == 1 || (ov == 0 && K < 24)) return 0;
+    const int kg2 = K > 32 ? 1 : 0;
+    (void)field;
+    if (ov == 3) return 4 + kg2;
+    return 2 + kg2;
 }
 
 static int encode_on_stream(int field, int fi, const uint8_t *A, const uint8_t *C, uint8_t *B,
                             int N, int K, size_t M, size_t batch, cudaStream_t st)
 {
     {
-        if (encode_path(K, M, A, B) >= 2) {
+        const int path = encode_path(field, K, M, A, B);
+        if (path >= 4) {
+            void *tabs = nullptr;
+            if (cudaGetSymbolAddress(&tabs, g_dev_tabs) != cudaSuccess) return GF_ECUDA;
+            const uint32_t *t = reinterpret_cast<const uint32_t *>(tabs) + (size_t)fi * 256 * kTableWords;
+            const bool kg2 = path == 5;
+            switch (field) {
+            case 256: return kg2 ? launch_fused<256, 2, 4, 4>(A, C, B, N, K, M, batch, st, t)
+                                 : launch_fused<256, 1, 4, 4>(A, C, B, N, K, M, batch, st, t);
+            case 16: return kg2 ? launch_fused<16, 2, 4, 4>(A, C, B, N, K, M, batch, st, t)
+                                : launch_fused<16, 1, 4, 4>(A, C, B, N, K, M, batch, st, t);
+            case 4: return kg2 ? launch_fused<4, 2, 4, 4>(A, C, B, N, K, M, batch, st, t)
+                               : launch_fused<4, 1, 4, 2>(A, C, B, N, K, M, batch, st, t);
+            case 2: return kg2 ? launch_fused<2, 2, 6, 4>(A, C, B, N, K, M, batch, st, t)
+                               : launch_fused<2, 1, 6, 2>(A, C, B, N, K, M, batch, st, t);
+            default: return GF_EFIELD;
+            }
+        }
+        if (path >= 2) {
             switch (field) {
             case 256: return launch_lanek_kg<256>(A, C, B, N, K, M, batch, st);
             case 16: return launch_lanek_kg<16>(A, C, B, N, K, M, batch, st);
@@ -316,7 +364,7 @@ int gf_encode_path(int field, int N, int K, size_t M, size_t a_align, size_t b_a
 {
     if (field_index(field) < 0) return GF_EFIELD;
     if (N < 1 || K < 1) return GF_EARG;
-    return encode_path(K, M, reinterpret_cast<const void *>(a_align & 15u),
+    return encode_path(field, K, M, reinterpret_cast<const void *>(a_align & 15u),
                        reinterpret_cast<const void *>(b_align & 15u));
 }
 

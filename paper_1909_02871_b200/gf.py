@@ -73,7 +73,8 @@ def version() -> int:
     return _lib.gf_version()
 
 
-ENCODE_PATHS = {0: "column-words", 1: "column-bytes", 2: "lanek-32", 3: "lanek-64"}
+ENCODE_PATHS = {0: "column-words", 1: "column-bytes", 2: "lanek-32", 3: "lanek-64", 4: "fused-32",
+                5: "fused-64"}
 
 
 def encode_path(field: int, N: int, K: int, M: int, a_align: int = 0, b_align: int = 0) -> str:

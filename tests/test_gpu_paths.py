@@ -1,0 +1,42 @@
+"""Every encode kernel, forced through GFRLNC_ENCODE_PATH in a fresh process
+(the library reads the override once), against the oracle."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import oracle, seeded_inputs as si
+from paper_1909_02871_b200 import gf
+want = sys.argv[1]
+for q in (2, 4, 16, 256):
+    gf.init(q)
+    for (N, K, M, batch) in ((17, 33, 1500, 3), (64, 64, 1500, 2), (32, 32, 4100, 2), (5, 24, 400, 3),
+                             (33, 96, 3000, 2), (7, 65, 1540, 2)):
+        A = si.random_bytes(7 + N, 1, 0, batch * N * M).reshape(batch, N, M)
+        C = si.uniform_coeffs(q, 8 + K, 2, 0, batch * N * K).reshape(batch, N, K)
+        path = gf.encode_path(q, N, K, M)
+        assert path.startswith(want), (path, want)
+        got = gf.encode_batch(q, torch.from_numpy(A).cuda(), torch.from_numpy(C).cuda()).cpu().numpy()
+        assert np.array_equal(got, oracle.encode_batch(q, A, C)), (q, N, K, M, path)
+print("ok", want)
+''' % ROOT
+
+
+@pytest.mark.parametrize("path", ["column", "lanek", "fused"])
+def test_forced_encode_path(path):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = dict(os.environ, GFRLNC_ENCODE_PATH=path)
+    out = subprocess.run([sys.executable, "-c", SCRIPT, path], env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    assert ("ok " + path) in out.stdout
