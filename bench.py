@@ -473,10 +473,39 @@ def run_e2e(gf, torch, dist, cfg, q, sh, device, ws, args):
         dt = float(t.item())
     src = (G * N * Ms) * ws
     value = steps * src / dt / 1e9
+    # the PCIe roofline of this path: plain pinned copies of the same sizes,
+    # concurrently in both directions (the e2e pipeline overlaps them)
+    h2d_b, d2h_b = G * (N * Ms + N * K), G * K * Ms
+    pcie = {}
+    try:
+        nb = min(h2d_b, 2 << 30)
+        dbuf = torch.empty(nb, dtype=torch.uint8, device=device)
+        hsrc = Ah.view(-1)[:nb]
+        hdst = Bh.view(-1)[:min(nb, Bh.numel())]
+        s1, s2 = torch.cuda.Stream(device), torch.cuda.Stream(device)
+        for _ in range(2):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            with torch.cuda.stream(s1):
+                dbuf.copy_(hsrc, non_blocking=True)
+            torch.cuda.synchronize()
+            t_h2d = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            with torch.cuda.stream(s2):
+                hdst.copy_(dbuf[:hdst.numel()], non_blocking=True)
+            torch.cuda.synchronize()
+            t_d2h = time.perf_counter() - t0
+        pcie = {"h2d_GBps": round(nb / t_h2d / 1e9, 1), "d2h_GBps": round(hdst.numel() / t_d2h / 1e9, 1)}
+        bound_s = max(h2d_b / (pcie["h2d_GBps"] * 1e9), d2h_b / (pcie["d2h_GBps"] * 1e9))
+        pcie["e2e_bound_GBps"] = round(G * N * Ms / bound_s / 1e9, 2)
+        pcie["e2e_frac_of_bound"] = round(value / ws / pcie["e2e_bound_GBps"], 3)
+        del dbuf
+    except Exception as e:  # diagnostics only
+        pcie = {"error": str(e)[:200]}
     del ws_t
     torch.cuda.empty_cache()
-    return {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": G * (N * Ms + N * K),
-            "d2h_bytes_per_step": G * K * Ms, "steps": steps, "gens_per_step": G,
+    return {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d_b,
+            "d2h_bytes_per_step": d2h_b, "steps": steps, "gens_per_step": G, "pcie": pcie,
             "path": f"gf_encode_batch_host: pinned host buffers, {chunk}-generation chunks, "
                     "3-stream copy/compute overlap",
             "timing": "host wall clock around blocking calls, max over ranks"}

@@ -49,10 +49,11 @@ constexpr int kLkNQ = 3;                  // Q buffers between builders and gath
 
 template <int KG> struct LkGeom {
     static constexpr int WT = KG == 1 ? 32 : 48;          // words per gatherer lane
-    static constexpr int TW = WT * kLkWG;                 // words per tile
+    static constexpr int WG = KG == 4 ? 4 : kLkWG;        // word groups
+    static constexpr int TW = WT * WG;                    // words per tile
     static constexpr int QS = TW + 1;                     // Q row stride (odd)
-    static constexpr int BWORDS = TW / (32 * kLkBuildWarps);
-    static constexpr int THREADS = 32 * (KG * kLkWG + kLkBuildWarps);
+    static constexpr int BWORDS = (TW + 32 * kLkBuildWarps - 1) / (32 * kLkBuildWarps);
+    static constexpr int THREADS = 32 * (KG * WG + kLkBuildWarps);
     static constexpr int MINB = KG == 1 ? 3 : 1;          // CTAs per SM targeted
 };
 
@@ -146,7 +147,7 @@ __global__ void __launch_bounds__(LkGeom<KG>::THREADS, LkGeom<KG>::MINB) encode_
     constexpr int SG = L::kSG;
     constexpr int WT = G::WT, TW = G::TW, QS = G::QS;
     constexpr int KTL = 32 * KG;                               // coded packets per CTA
-    constexpr int GW = KG * kLkWG;                             // gatherer warps
+    constexpr int GW = KG * G::WG;                             // gatherer warps
     constexpr int NT = G::THREADS;
     constexpr int kQWords = L::kRows * QS;
     constexpr int kRingRows = SG * kLkSteps;
@@ -205,9 +206,11 @@ __global__ void __launch_bounds__(LkGeom<KG>::THREADS, LkGeom<KG>::MINB) encode_
 #pragma unroll
                     for (int u = 0; u < G::BWORDS; u++) {
                         const uint32_t tw = (uint32_t)bt + 128u * u;
-                        const uint32_t wd = w0 + tw;
-                        const bool v = i < p.N && wd < p.Mw;
-                        cp_async4(ring_s + (slot + tw) * 4u, v ? row + wd : row, v);
+                        if (tw < (uint32_t)TW) {
+                            const uint32_t wd = w0 + tw;
+                            const bool v = i < p.N && wd < p.Mw;
+                            cp_async4(ring_s + (slot + tw) * 4u, v ? row + wd : row, v);
+                        }
                     }
                 }
             }
@@ -226,10 +229,12 @@ __global__ void __launch_bounds__(LkGeom<KG>::THREADS, LkGeom<KG>::MINB) encode_
 #pragma unroll
             for (int u = 0; u < G::BWORDS; u++) {
                 const int tw = bt + 128 * u;
-                uint32_t a[SG];
+                if (tw < TW) {
+                    uint32_t a[SG];
 #pragma unroll
-                for (int j = 0; j < SG; j++) a[j] = slot[j * TW + tw];
-                build_word<F, QS>(q + tw, a);
+                    for (int j = 0; j < SG; j++) a[j] = slot[j * TW + tw];
+                    build_word<F, QS>(q + tw, a);
+                }
             }
             nbar_arrive(BAR_FULL + b, NT);
         }
@@ -241,7 +246,7 @@ __global__ void __launch_bounds__(LkGeom<KG>::THREADS, LkGeom<KG>::MINB) encode_
 
     // ---------------- gatherers: lane = coded packet k, WT words per lane
     const int kl = (warp % KG) * 32 + lane;                    // local k
-    const int wg = warp / KG;                                  // word group (0..7)
+    const int wg = warp / KG;                                  // word group
     const uint8_t *ccol = ccache + kl;                         // row index of step s at ccol[KTL s]
     uint32_t acc[WT];
 #pragma unroll
@@ -270,8 +275,11 @@ __global__ void __launch_bounds__(LkGeom<KG>::THREADS, LkGeom<KG>::MINB) encode_
     // contiguous runs of one coded packet (the Q buffers are free once every
     // gatherer passed its last step: named barrier over the gatherers only)
     constexpr int OS = TW + 1;
-    constexpr int kPasses = (KTL * OS + kLkNQ * kQWords - 1) / (kLkNQ * kQWords);
-    constexpr int kRowsPerPass = KTL / kPasses;
+    // rows of coded packets staged per pass: the largest of KTL, KTL/2, ... (>= 32)
+    // that fits in the Q buffers
+    constexpr int kFit = (kLkNQ * kQWords) / OS;
+    constexpr int kRowsPerPass = KTL <= kFit ? KTL : (KTL / 2 <= kFit ? KTL / 2 : (KTL / 4 <= kFit ? KTL / 4 : 32));
+    constexpr int kPasses = KTL / kRowsPerPass;
     static_assert(kRowsPerPass * kPasses == KTL && kRowsPerPass % 32 == 0, "epilogue passes");
     uint32_t *ot = Q;                                           // [rows per pass][OS]
     const uint32_t nw = min((uint32_t)TW, p.Mw - w0);

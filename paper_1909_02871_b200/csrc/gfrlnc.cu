@@ -20,7 +20,7 @@
 namespace gfr {
 
 constexpr int kMaxDevices = 64;
-constexpr int kVersion = 121;   // 0.1.21: lane-k default, fused opt-in
+constexpr int kVersion = 122;   // 0.1.22: lane-k 128-packet CTAs for K > 64
 
 __device__ uint32_t g_dev_tabs[4][256 * kTableWords];
 
@@ -30,6 +30,13 @@ static uint32_t g_dev_ready[kMaxDevices];     // bit f: field index f uploaded
 static int g_sm_count[kMaxDevices];
 static std::mutex g_lock;
 static thread_local cudaStream_t tls_stream = nullptr;
+
+// experiment knobs (never needed in production): integer environment variable
+static int env_int(const char *name, int dflt)
+{
+    const char *v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
 
 static int field_index(int field)
 {
@@ -222,8 +229,13 @@ template <int F>
 static int launch_lanek_kg(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M,
                            size_t batch, cudaStream_t st)
 {
-    return K > 32 ? launch_lanek<F, 2>(A, C, B, N, K, M, batch, st)
-                  : launch_lanek<F, 1>(A, C, B, N, K, M, batch, st);
+    // coded packets per CTA: 32 (3 CTAs/SM), 64 or 128 (one CTA/SM); larger
+    // groups share each table build among more lanes
+    static const int kg_override = env_int("GFRLNC_LANEK_KG", 0);   // experiments only
+    const int kg = kg_override ? kg_override : (K > 64 ? 4 : K > 32 ? 2 : 1);
+    if (kg == 4) return launch_lanek<F, 4>(A, C, B, N, K, M, batch, st);
+    if (kg == 2) return launch_lanek<F, 2>(A, C, B, N, K, M, batch, st);
+    return launch_lanek<F, 1>(A, C, B, N, K, M, batch, st);
 }
 
 // encode path: "lanek" (shared-memory product tables, k on lanes) when K >= 24
@@ -254,7 +266,7 @@ static int encode_path(int field, int K, size_t M, const void *A, const void *B)
     const int ov = encode_path_override();
     if (!aligned) return 1;
     if (ov == 1 || (ov == 0 && K < 24)) return 0;
-    const int kg2 = K > 32 ? 1 : 0;
+    const int kg2 = K > 32 ? 1 : 0;      // (K > 64 uses 128 coded packets per CTA)
     (void)field;
     if (ov == 3) return 4 + kg2;
     return 2 + kg2;
