@@ -455,7 +455,7 @@ def run_e2e(gf, torch, dist, cfg, q, sh, device, ws, args):
         Ah[j:j + n].copy_(tmpA[:n])
         Ch[j:j + n].copy_(tmpC[:n])
     del tmpA, tmpC
-    chunk = max(1, min(G, int(0.5e9 // per_gen_host)))
+    chunk = max(1, min(G, int(0.2e9 // per_gen_host)))
     ws_t = torch.empty(gf.host_workspace_bytes(N, K, Ms, chunk), dtype=torch.uint8, device=device)
     torch.cuda.synchronize()
     gf.encode_batch_host(q, Ah, Ch, Bh, ws_t)

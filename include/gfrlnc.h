@@ -85,7 +85,8 @@ int gf_encode_batch(int field, const uint8_t *A, const uint8_t *C, uint8_t *B,
  * copies in, encodes and copies out in chunks of generations, overlapping
  * host->device copies, kernels and device->host copies on three internal
  * streams.  dev_ws / ws_bytes is a caller-owned device workspace; it must
- * hold at least two chunks of one generation (2 * (N*M + N*K + K*M) bytes).
+ * hold at least three chunks of one generation (3 * (N*M + N*K + K*M) + 144
+ * bytes); larger workspaces give larger chunks.
  * Pinned host memory is strongly recommended.  BLOCKING: returns after B_host
  * is complete (the caller's stream is not used).  Returns the codes of
  * gf_encode_batch, or GF_EARG when the workspace is too small. */

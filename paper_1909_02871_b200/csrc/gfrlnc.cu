@@ -337,10 +337,12 @@ static int validate_encode(int field, const uint8_t *A, const uint8_t *C, const 
 
 // ------------------------------------------------------------ host pipeline
 
+constexpr int kPipeBufs = 3;     // chunks in flight: H2D(j+2) | kernel(j+1) | D2H(j)
+
 struct HostPipe {
     bool ready = false;
     cudaStream_t s_h2d = nullptr, s_cmp = nullptr, s_d2h = nullptr;
-    cudaEvent_t ev_in[2], ev_cmp[2], ev_free[2];
+    cudaEvent_t ev_in[kPipeBufs], ev_cmp[kPipeBufs], ev_free[kPipeBufs];
 };
 static HostPipe g_pipes[kMaxDevices];
 
@@ -353,7 +355,7 @@ static int pipe_for(int dev, HostPipe **out)
             cudaStreamCreateWithFlags(&P.s_cmp, cudaStreamNonBlocking) != cudaSuccess ||
             cudaStreamCreateWithFlags(&P.s_d2h, cudaStreamNonBlocking) != cudaSuccess)
             return GF_ECUDA;
-        for (int b = 0; b < 2; b++)
+        for (int b = 0; b < kPipeBufs; b++)
             if (cudaEventCreateWithFlags(&P.ev_in[b], cudaEventDisableTiming) != cudaSuccess ||
                 cudaEventCreateWithFlags(&P.ev_cmp[b], cudaEventDisableTiming) != cudaSuccess ||
                 cudaEventCreateWithFlags(&P.ev_free[b], cudaEventDisableTiming) != cudaSuccess)
@@ -493,15 +495,15 @@ int gf_encode_batch_host(int field, const uint8_t *A_host, const uint8_t *C_host
     const size_t per_gen_a = (size_t)N * M, per_gen_c = (size_t)N * K, per_gen_b = (size_t)K * M;
     // keep every chunk 16-B aligned inside the workspace
     auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
-    size_t chunk = ws_bytes / (2 * (per_gen_a + per_gen_c + per_gen_b) + 96);
+    size_t chunk = ws_bytes / (kPipeBufs * (per_gen_a + per_gen_c + per_gen_b) + 144);
     if (chunk < 1) return GF_EARG;
     if (chunk > batch) chunk = batch;
     HostPipe *P;
     if ((rc = pipe_for(dev, &P)) != GF_OK) return rc;
     uint8_t *ws = static_cast<uint8_t *>(dev_ws);
-    uint8_t *bufA[2], *bufC[2], *bufB[2];
+    uint8_t *bufA[kPipeBufs], *bufC[kPipeBufs], *bufB[kPipeBufs];
     size_t off = 0;
-    for (int b = 0; b < 2; b++) {
+    for (int b = 0; b < kPipeBufs; b++) {
         bufA[b] = ws + off; off = al(off + chunk * per_gen_a);
         bufC[b] = ws + off; off = al(off + chunk * per_gen_c);
         bufB[b] = ws + off; off = al(off + chunk * per_gen_b);
@@ -509,9 +511,9 @@ int gf_encode_batch_host(int field, const uint8_t *A_host, const uint8_t *C_host
     if (off > ws_bytes) return GF_EARG;
     const size_t nchunks = (batch + chunk - 1) / chunk;
     for (size_t j = 0; j < nchunks; j++) {
-        const int b = (int)(j & 1);
+        const int b = (int)(j % kPipeBufs);
         const size_t g0 = j * chunk, gn = (g0 + chunk <= batch) ? chunk : batch - g0;
-        if (j >= 2 && cudaStreamWaitEvent(P->s_h2d, P->ev_free[b], 0) != cudaSuccess) return GF_ECUDA;
+        if (j >= kPipeBufs && cudaStreamWaitEvent(P->s_h2d, P->ev_free[b], 0) != cudaSuccess) return GF_ECUDA;
         if (cudaMemcpyAsync(bufA[b], A_host + g0 * per_gen_a, gn * per_gen_a, cudaMemcpyHostToDevice,
                             P->s_h2d) != cudaSuccess ||
             cudaMemcpyAsync(bufC[b], C_host + g0 * per_gen_c, gn * per_gen_c, cudaMemcpyHostToDevice,
@@ -519,7 +521,7 @@ int gf_encode_batch_host(int field, const uint8_t *A_host, const uint8_t *C_host
             cudaEventRecord(P->ev_in[b], P->s_h2d) != cudaSuccess)
             return GF_ECUDA;
         if (cudaStreamWaitEvent(P->s_cmp, P->ev_in[b], 0) != cudaSuccess) return GF_ECUDA;
-        if (j >= 2 && cudaStreamWaitEvent(P->s_cmp, P->ev_free[b], 0) != cudaSuccess) return GF_ECUDA;
+        if (j >= kPipeBufs && cudaStreamWaitEvent(P->s_cmp, P->ev_free[b], 0) != cudaSuccess) return GF_ECUDA;
         if ((rc = encode_on_stream(field, fi, bufA[b], bufC[b], bufB[b], N, K, M, gn, P->s_cmp)) != GF_OK)
             return rc;
         if (cudaEventRecord(P->ev_cmp[b], P->s_cmp) != cudaSuccess ||

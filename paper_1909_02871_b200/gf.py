@@ -207,7 +207,7 @@ def encode_batch_host(field: int, A: torch.Tensor, C: torch.Tensor, B: torch.Ten
 
 def host_workspace_bytes(N: int, K: int, M: int, gens_per_chunk: int) -> int:
     """Device workspace for encode_batch_host with the given chunk size."""
-    return 2 * gens_per_chunk * (N * M + N * K + K * M) + 96
+    return 3 * gens_per_chunk * (N * M + N * K + K * M) + 144
 
 
 # ---- harness-only --------------------------------------------------------------
