@@ -94,6 +94,26 @@ int gf_encode_batch_host(int field, const uint8_t *A_host, const uint8_t *C_host
                          uint8_t *B_host, int N, int K, size_t M, size_t batch,
                          void *dev_ws, size_t ws_bytes);
 
+/* Batched inversion of the coefficient matrices (decoder support, SURVEY.md
+ * 8(f) NEXT-3; SPEC decode): for g < batch, D[g] = C[g]^{-1} over F_q, i.e.
+ * sum_k C[g][i][k] D[g][k][j] = [i == j], by Gauss-Jordan elimination with
+ * first-nonzero pivoting.  C, D: [batch][N][N] device bytes (entries masked
+ * with q-1), 1 <= N <= 256.  rank (device int[batch], may be NULL) receives
+ * the rank of each C[g]; where it is < N, D[g] is unspecified.  Returns
+ * GF_OK, GF_EFIELD, GF_ENOINIT, GF_EARG, GF_EOVERLAP, GF_ECUDA. */
+int gf_invert_batch(int field, const uint8_t *C, uint8_t *D, int *rank, int N, size_t batch);
+
+/* Batched RLNC decode: recover the N source packets of every generation from
+ * N coded packets, closing Eq. 2.  B[batch][N][M] holds the
+ * coded packets, C[batch][N][N] their coding vectors in the layout
+ * gf_encode_batch uses (C[g][i][k] = coefficient of source i in coded packet
+ * k), A[batch][N][M] receives the sources: A = encode(B, C^{-1}).  dev_ws is a
+ * device workspace of at least batch * N * N bytes (the inverses).  rank as in
+ * gf_invert_batch; rows of A[g] are unspecified where rank[g] < N.  Returns
+ * the codes of gf_encode_batch, or GF_EARG for a short workspace. */
+int gf_decode_batch(int field, const uint8_t *B, const uint8_t *C, uint8_t *A, int *rank, int N, size_t M,
+                    size_t batch, void *dev_ws, size_t ws_bytes);
+
 /* Set the calling thread's stream (a cudaStream_t; NULL = legacy default). */
 int gf_set_stream(void *cuda_stream);
 

@@ -1,0 +1,121 @@
+// decode_kernels.cuh -- batched decoding support:
+// per-generation inversion of the N x N coefficient matrix over F_q by
+// Gauss-Jordan elimination, one CTA per generation.
+//
+// Decoding closes the RLNC loop of Eq. 2: with
+// B[k] = sum_i C[i][k] a_i for k < N and D = C^{-1} (C D = I),
+//     sum_k D[k][j] B[k] = sum_i a_i sum_k C[i][k] D[k][j] = a_j,
+// so decode(B, C) = encode(B, D): the batched encode kernels do the heavy
+// part, this kernel only inverts the small matrices.
+//
+// Row operations work on packed 32-bit words of 4 matrix entries with the
+// same byte-permute split tables as the encode kernels (every entry is a
+// single field element, so the packed byte product is the element product).
+// Columns left of the current pivot are already reduced (zero outside pivot
+// rows) and are skipped.
+#pragma once
+#include <cstdint>
+
+#include "gf_device.cuh"
+
+namespace gfr {
+
+struct InvertParams {
+    const uint8_t *C;      // [batch][N][N]
+    uint8_t *D;            // [batch][N][N]  inverse (undefined where rank < N)
+    int *rank;             // [batch] or nullptr
+    const uint32_t *tabs;  // table of tables of the field (16 words per coefficient)
+    const uint8_t *inv;    // multiplicative inverses of the field (256 bytes)
+    size_t batch;
+    int N;
+    int qmask;
+};
+
+__device__ __forceinline__ PrmtTab tab_of(const uint32_t *stab, uint32_t c)
+{
+    const uint32_t *t = stab + c * 8u;
+    PrmtTab T;
+    T.t0lo = t[0]; T.t0hi = t[1]; T.t1lo = t[2]; T.t1hi = t[3]; T.t2 = t[4];
+    return T;
+}
+
+__device__ __forceinline__ uint32_t mul_word(const PrmtTab &T, uint32_t x)
+{
+    return unperm(lookup_perm(T, make_sel(x)));
+}
+
+// one CTA (256 threads) per generation; dynamic smem: augmented matrix
+// [N][RW] words (RW = 2N/4 rounded up) + field tables (256 x 8 words) + inverses
+__global__ void __launch_bounds__(256) invert_kernel(InvertParams p)
+{
+    extern __shared__ __align__(16) uint32_t smem[];
+    const int N = p.N;
+    const int RW = (2 * N + 3) / 4;                   // words per augmented row
+    uint32_t *Mx = smem;                              // [N][RW]
+    uint32_t *stab = Mx + (size_t)N * RW;             // [256][8]: T0lo,T0hi,T1lo,T1hi,T2,...
+    uint8_t *sinv = reinterpret_cast<uint8_t *>(stab + 256 * 8);
+    __shared__ int s_piv;
+    __shared__ uint8_t s_fac[256];                    // column entries, read before elimination
+    const size_t g = blockIdx.x;
+    const int tid = threadIdx.x, nt = blockDim.x;
+
+    for (int e = tid; e < 256 * 8; e += nt) {
+        const int c = e >> 3, j = e & 7;
+        stab[e] = j < 5 ? __ldg(p.tabs + (size_t)c * 16u + j) : 0u;
+    }
+    for (int e = tid; e < 256; e += nt) sinv[e] = __ldg(p.inv + e);
+    uint8_t *Mb = reinterpret_cast<uint8_t *>(Mx);
+    const uint8_t *Cg = p.C + g * (size_t)N * N;
+    for (int e = tid; e < N * RW * 4; e += nt) {
+        const int r = e / (RW * 4), c = e - r * RW * 4;
+        uint8_t v = 0;
+        if (c < N) v = Cg[(size_t)r * N + c] & (uint8_t)p.qmask;
+        else if (c < 2 * N) v = (c - N == r) ? 1 : 0;
+        Mb[e] = v;
+    }
+    __syncthreads();
+
+    int rank = 0;
+    for (int col = 0; col < N; col++) {
+        // pivot: first row >= rank with a nonzero entry in this column
+        if (tid == 0) s_piv = N;
+        __syncthreads();
+        for (int r = rank + tid; r < N; r += nt)
+            if (Mb[(size_t)r * RW * 4 + col]) atomicMin(&s_piv, r);
+        __syncthreads();
+        const int piv = s_piv;
+        if (piv == N) continue;                       // column without pivot: rank deficient
+        const int w0 = col >> 2;                      // words left of w0 are reduced
+        // swap pivot row into place and scale it by the inverse of the pivot
+        const uint32_t pv = Mb[(size_t)piv * RW * 4 + col];
+        const PrmtTab Ts = tab_of(stab, sinv[pv]);
+        for (int w = w0 + tid; w < RW; w += nt) {
+            const uint32_t a = Mx[(size_t)piv * RW + w];
+            const uint32_t b = Mx[(size_t)rank * RW + w];
+            Mx[(size_t)piv * RW + w] = b;
+            Mx[(size_t)rank * RW + w] = mul_word(Ts, a);
+        }
+        __syncthreads();
+        for (int r = tid; r < N; r += nt) s_fac[r] = r == rank ? 0 : Mb[(size_t)r * RW * 4 + col];
+        __syncthreads();
+        // eliminate the column from every other row
+        const int span = RW - w0;
+        for (int e = tid; e < N * span; e += nt) {
+            const int r = e / span, w = w0 + (e - r * span);
+            const uint32_t f = s_fac[r];
+            if (f == 0) continue;
+            Mx[(size_t)r * RW + w] ^= mul_word(tab_of(stab, f), Mx[(size_t)rank * RW + w]);
+        }
+        __syncthreads();
+        rank++;
+    }
+    // D = right half
+    uint8_t *Dg = p.D + g * (size_t)N * N;
+    for (int e = tid; e < N * N; e += nt) {
+        const int r = e / N, c = e - r * N;
+        Dg[e] = Mb[(size_t)r * RW * 4 + N + c];
+    }
+    if (tid == 0 && p.rank) p.rank[g] = rank;
+}
+
+}  // namespace gfr

@@ -13,6 +13,7 @@
 #include "encode_kernels.cuh"
 #include "encode_lanek.cuh"
 #include "encode_fused.cuh"
+#include "decode_kernels.cuh"
 #include "region_kernels.cuh"
 #include "rng_kernels.cuh"
 #include "tables.h"
@@ -20,11 +21,13 @@
 namespace gfr {
 
 constexpr int kMaxDevices = 64;
-constexpr int kVersion = 122;   // 0.1.22: lane-k 128-packet CTAs for K > 64
+constexpr int kVersion = 130;   // 0.1.30: batched decode (matrix inversion + encode)
 
 __device__ uint32_t g_dev_tabs[4][256 * kTableWords];
+__device__ uint8_t g_dev_inv[4][256];
 
 static uint32_t g_host_tabs[4][256 * kTableWords];
+static uint8_t g_host_inv[4][256];
 static bool g_host_ready[4];
 static uint32_t g_dev_ready[kMaxDevices];     // bit f: field index f uploaded
 static int g_sm_count[kMaxDevices];
@@ -420,11 +423,14 @@ int gf_init(int field)
     if (!g_host_ready[fi]) {
         std::memset(g_host_tabs[fi], 0, sizeof(g_host_tabs[fi]));
         if (build_tables(field, g_host_tabs[fi], 256 * kTableWords) != 0) return GF_EFIELD;
+        if (build_inverses(field, g_host_inv[fi]) != 0) return GF_EFIELD;
         g_host_ready[fi] = true;
     }
     if (!(g_dev_ready[dev] >> fi & 1u)) {
         if (cudaMemcpyToSymbol(g_dev_tabs, g_host_tabs[fi], sizeof(g_host_tabs[fi]),
-                               (size_t)fi * sizeof(g_host_tabs[fi]), cudaMemcpyHostToDevice) != cudaSuccess)
+                               (size_t)fi * sizeof(g_host_tabs[fi]), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpyToSymbol(g_dev_inv, g_host_inv[fi], 256, (size_t)fi * 256, cudaMemcpyHostToDevice) !=
+                cudaSuccess)
             return GF_ECUDA;
         if (g_sm_count[dev] == 0) {
             int sms = 0;
@@ -533,6 +539,50 @@ int gf_encode_batch_host(int field, const uint8_t *A_host, const uint8_t *C_host
     }
     if (cudaStreamSynchronize(P->s_d2h) != cudaSuccess) return GF_ECUDA;
     return GF_OK;
+}
+
+int gf_invert_batch(int field, const uint8_t *C, uint8_t *D, int *rank, int N, size_t batch)
+{
+    int fi, dev;
+    const int rc = check_ready(field, &fi, &dev);
+    if (rc != GF_OK) return rc;
+    if (N < 1 || N > 256) return GF_EARG;
+    if (batch == 0) return GF_OK;
+    if (!C || !D) return GF_EARG;
+    size_t cb;
+    if (__builtin_mul_overflow((size_t)N * (size_t)N, batch, &cb) || batch > 0x7FFFFFFFu) return GF_EARG;
+    if (overlaps(C, cb, D, cb)) return GF_EOVERLAP;
+    void *tabs = nullptr, *inv = nullptr;
+    if (cudaGetSymbolAddress(&tabs, g_dev_tabs) != cudaSuccess ||
+        cudaGetSymbolAddress(&inv, g_dev_inv) != cudaSuccess)
+        return GF_ECUDA;
+    InvertParams p;
+    p.C = C; p.D = D; p.rank = rank; p.batch = batch; p.N = N; p.qmask = field - 1;
+    p.tabs = reinterpret_cast<const uint32_t *>(tabs) + (size_t)fi * 256 * kTableWords;
+    p.inv = reinterpret_cast<const uint8_t *>(inv) + (size_t)fi * 256;
+    const size_t rw = (2 * (size_t)N + 3) / 4;
+    const size_t smem = (size_t)N * rw * 4 + 256 * 8 * 4 + 256;
+    if (cudaFuncSetAttribute(invert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return GF_ECUDA;
+    invert_kernel<<<(unsigned)batch, 256, smem, tls_stream>>>(p);
+    return launch_status();
+}
+
+int gf_decode_batch(int field, const uint8_t *B, const uint8_t *C, uint8_t *A, int *rank, int N, size_t M,
+                    size_t batch, void *dev_ws, size_t ws_bytes)
+{
+    int fi, dev;
+    int rc = check_ready(field, &fi, &dev);
+    if (rc != GF_OK) return rc;
+    size_t ab, bb, cb;
+    rc = validate_encode(field, B, C, A, N, N, M, batch, &bb, &ab, &cb);
+    if (rc != GF_OK || M == 0 || batch == 0) return rc;
+    if (!dev_ws || ws_bytes < cb) return GF_EARG;
+    uint8_t *D = static_cast<uint8_t *>(dev_ws);
+    if (overlaps(D, cb, A, ab) || overlaps(D, cb, B, bb) || overlaps(D, cb, C, cb)) return GF_EOVERLAP;
+    if ((rc = gf_invert_batch(field, C, D, rank, N, batch)) != GF_OK) return rc;
+    return encode_on_stream(field, fi, B, D, A, N, N, M, batch, tls_stream);
 }
 
 int gf_fill_random2d(uint8_t *dst, size_t rows, size_t cols, uint64_t seed, uint64_t stream,

@@ -111,4 +111,14 @@ int build_tables(int field, uint32_t *out, size_t cap_words)
     return 0;
 }
 
+int build_inverses(int field, uint8_t *inv)
+{
+    if (field_width(field) < 0) return -1;
+    for (int a = 0; a < 256; a++) inv[a] = 0;
+    for (uint32_t a = 1; a < (uint32_t)field; a++)
+        for (uint32_t x = 1; x < (uint32_t)field; x++)
+            if (elem_mul(field, a, x) == 1u) { inv[a] = (uint8_t)x; break; }
+    return 0;
+}
+
 }  // namespace gfr

@@ -44,6 +44,9 @@ _lib.gf_fill_random2d.argtypes = [_u8p, _sz, _sz, _u64, _u64, _u64, _u64, ctypes
 _lib.gf_host_tables.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_uint32), _sz]
 _lib.gf_version.argtypes = []
 _lib.gf_encode_path.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _sz, _sz, _sz]
+_lib.gf_invert_batch.argtypes = [ctypes.c_int, _u8p, _u8p, ctypes.c_void_p, ctypes.c_int, _sz]
+_lib.gf_decode_batch.argtypes = [ctypes.c_int, _u8p, _u8p, _u8p, ctypes.c_void_p, ctypes.c_int, _sz, _sz,
+                                 _u8p, _sz]
 
 GF_OK, GF_EFIELD, GF_ECOEFF, GF_EARG, GF_EOVERLAP, GF_ENOINIT, GF_ECUDA = 0, -1, -2, -3, -4, -5, -6
 FIELDS = (2, 4, 16, 256)
@@ -52,7 +55,7 @@ TABLE_WORDS = 16          # uint32 words per coefficient in gf_host_tables
 # every symbol include/gfrlnc.h declares (tests check the library exports them)
 ABI_SYMBOLS = ("gf_init", "gf_maddrc", "gf_mulrc", "gf_encode_batch", "gf_encode_batch_host",
                "gf_set_stream", "gf_strerror", "gf_fill_random", "gf_fill_random2d",
-               "gf_host_tables", "gf_version", "gf_encode_path")
+               "gf_host_tables", "gf_version", "gf_encode_path", "gf_invert_batch", "gf_decode_batch")
 
 
 class GFError(RuntimeError):
@@ -189,6 +192,39 @@ def encode_batch(field: int, A: torch.Tensor, C: torch.Tensor, B: torch.Tensor |
         _use_stream(A.device)
         _check(_lib.gf_encode_batch(field, pa, pc, pb, N, K, M, batch), "gf_encode_batch")
     return B
+
+
+def invert_batch(field: int, C: torch.Tensor):
+    """D[g] = C[g]^{-1} over F_field for C uint8 [batch, N, N]; returns (D, rank)
+    with rank an int32 tensor (D[g] unspecified where rank[g] < N)."""
+    if C.dim() != 3 or C.shape[1] != C.shape[2]:
+        raise ValueError("expected C [batch, N, N]")
+    batch, N, _ = C.shape
+    D = torch.empty_like(C)
+    rank = torch.empty(batch, dtype=torch.int32, device=C.device)
+    pc, pd = _dev_u8(C, "C"), _dev_u8(D, "D")
+    with _on_device(C.device):
+        _use_stream(C.device)
+        _check(_lib.gf_invert_batch(field, pc, pd, rank.data_ptr(), N, batch), "gf_invert_batch")
+    return D, rank
+
+
+def decode_batch(field: int, B: torch.Tensor, C: torch.Tensor, workspace: torch.Tensor | None = None):
+    """Sources A [batch, N, M] from N coded packets B [batch, N, M] and their
+    coding vectors C [batch, N, N] (encode layout); returns (A, rank)."""
+    if B.dim() != 3 or C.dim() != 3 or C.shape[1] != C.shape[2] or B.shape[:2] != C.shape[:2]:
+        raise ValueError("expected B [batch, N, M] and C [batch, N, N]")
+    batch, N, M = B.shape
+    A = torch.empty_like(B)
+    rank = torch.empty(batch, dtype=torch.int32, device=B.device)
+    if workspace is None:
+        workspace = torch.empty(batch * N * N, dtype=torch.uint8, device=B.device)
+    pb, pc, pa, pw = _dev_u8(B, "B"), _dev_u8(C, "C"), _dev_u8(A, "A"), _dev_u8(workspace, "workspace")
+    with _on_device(B.device):
+        _use_stream(B.device)
+        _check(_lib.gf_decode_batch(field, pb, pc, pa, rank.data_ptr(), N, M, batch, pw, workspace.numel()),
+               "gf_decode_batch")
+    return A, rank
 
 
 def encode_batch_host(field: int, A: torch.Tensor, C: torch.Tensor, B: torch.Tensor,

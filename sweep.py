@@ -171,6 +171,30 @@ def main():
         del A, B, C
         torch.cuda.empty_cache()
 
+    if "DEC" in todo:
+        # NEXT-3: batched decode of C3-shaped generations (N = K = 64, 1500 B):
+        # invert 64 x 64 coefficient matrices, then encode with the inverses
+        cfg = si.C3
+        G = 16384
+        for q in (16, 256):
+            A = torch.empty((G, cfg.N, cfg.M), dtype=torch.uint8, device=dev)
+            C = torch.empty((G, cfg.N, cfg.N), dtype=torch.uint8, device=dev)
+            gf.fill_random(A, 5, si.STREAM_A, 0)
+            gf.fill_random(C, 5, si.STREAM_C, 0, mask=q - 1)
+            B = gf.encode_batch(q, A, C)
+            ws = torch.empty(G * cfg.N * cfg.N, dtype=torch.uint8, device=dev)
+            inv_med, _, _ = timed(torch, lambda: gf.invert_batch(q, C), st, min_reps=5, min_s=0.5)
+            dec_med, _, _ = timed(torch, lambda: gf.decode_batch(q, B, C, ws), st, min_reps=5, min_s=0.5)
+            A2, rank = gf.decode_batch(q, B, C, ws)
+            ok = bool(torch.equal(A2[rank == cfg.N], A[rank == cfg.N]))
+            emit({"config": "DEC", "field": q, "N": cfg.N, "M": cfg.M, "gens": G,
+                  "invert_ms": round(inv_med, 3), "decode_ms": round(dec_med, 3),
+                  "decoded_GBps": round(G * cfg.N * cfg.M / (dec_med / 1e3) / 1e9, 2),
+                  "matrices_per_s_M": round(G / (inv_med / 1e3) / 1e6, 3),
+                  "full_rank": int((rank == cfg.N).sum()), "round_trip_ok": ok})
+            del A, B, C, ws, A2
+        torch.cuda.empty_cache()
+
     if "NEXT2" in todo:
         # paper-shaped sweep (Fig. 2): random linear
         # combinations of N=16 packets, K=1 coded packet, packet sizes 128 B ..
