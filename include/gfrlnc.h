@@ -114,6 +114,20 @@ int gf_invert_batch(int field, const uint8_t *C, uint8_t *D, int *rank, int N, s
 int gf_decode_batch(int field, const uint8_t *B, const uint8_t *C, uint8_t *A, int *rank, int N, size_t M,
                     size_t batch, void *dev_ws, size_t ws_bytes);
 
+/* On-device Freivalds check of an encode result (SURVEY.md 8(c) step 7,
+ * 8(f) NEXT-4): for every generation and each of t projection vectors
+ * r_j = R[g][:, j] (R: [batch][K][t] device bytes < q, t <= 32),
+ *     y1 = sum_i (C r_j)_i a_i   and   y2 = sum_k (r_j)_k b_k
+ * are formed with the encode kernels (K' = t, so the column kernel) and
+ * compared; mismatch[g] (device unsigned long long[batch]) receives the number
+ * of differing bytes.  B == A C implies zero; a wrong byte survives one
+ * projection with probability <= 1/q.  dev_ws must hold
+ * batch*N*t + 2*batch*t*M bytes (+48 for alignment).  Returns the codes of
+ * gf_encode_batch, or GF_EARG (t out of range, short workspace). */
+int gf_verify_batch(int field, const uint8_t *A, const uint8_t *C, const uint8_t *B, const uint8_t *R, int t,
+                    int N, int K, size_t M, size_t batch, unsigned long long *mismatch, void *dev_ws,
+                    size_t ws_bytes);
+
 /* Set the calling thread's stream (a cudaStream_t; NULL = legacy default). */
 int gf_set_stream(void *cuda_stream);
 

@@ -119,3 +119,40 @@ __global__ void __launch_bounds__(256) invert_kernel(InvertParams p)
 }
 
 }  // namespace gfr
+
+namespace gfr {
+
+// ---- on-device Freivalds projections -------------
+// U[g][i][j] = sum_k C[g][i][k] * R[g][k][j]  (element products from a q x q
+// table).  One thread per (g, i, j).
+__global__ void __launch_bounds__(256) project_coeffs_kernel(const uint8_t *C, const uint8_t *R, uint8_t *U,
+                                                             const uint8_t *__restrict__ mul, int N, int K,
+                                                             int t, size_t batch, int qmask)
+{
+    const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t per = (size_t)N * t;
+    if (e >= per * batch) return;
+    const size_t g = e / per;
+    const int i = (int)((e % per) / t), j = (int)(e % t);
+    const uint8_t *Cg = C + (g * N + i) * (size_t)K;
+    const uint8_t *Rg = R + g * (size_t)K * t;
+    uint32_t acc = 0;
+    for (int k = 0; k < K; k++)
+        acc ^= __ldg(mul + (size_t)(Cg[k] & qmask) * 256u + (Rg[(size_t)k * t + j] & qmask));
+    U[e] = (uint8_t)acc;
+}
+
+// mismatch[g] += #{ positions where Y1[g] and Y2[g] differ }, Y: [batch][len]
+__global__ void __launch_bounds__(256) count_mismatch_kernel(const uint8_t *Y1, const uint8_t *Y2, size_t len,
+                                                             unsigned long long *mismatch)
+{
+    const size_t g = blockIdx.y;
+    const uint8_t *a = Y1 + g * len, *b = Y2 + g * len;
+    unsigned long long n = 0;
+    for (size_t x = (size_t)blockIdx.x * blockDim.x + threadIdx.x; x < len; x += (size_t)gridDim.x * blockDim.x)
+        n += a[x] != b[x];
+    for (int o = 16; o > 0; o >>= 1) n += __shfl_down_sync(0xffffffffu, n, o);
+    if ((threadIdx.x & 31) == 0 && n) atomicAdd(mismatch + g, n);
+}
+
+}  // namespace gfr

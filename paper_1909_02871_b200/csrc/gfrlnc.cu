@@ -21,13 +21,15 @@
 namespace gfr {
 
 constexpr int kMaxDevices = 64;
-constexpr int kVersion = 130;   // 0.1.30: batched decode (matrix inversion + encode)
+constexpr int kVersion = 131;   // 0.1.31: + on-device Freivalds verification
 
 __device__ uint32_t g_dev_tabs[4][256 * kTableWords];
 __device__ uint8_t g_dev_inv[4][256];
+__device__ uint8_t g_dev_mul[4][256 * 256];
 
 static uint32_t g_host_tabs[4][256 * kTableWords];
 static uint8_t g_host_inv[4][256];
+static uint8_t g_host_mul[4][256 * 256];
 static bool g_host_ready[4];
 static uint32_t g_dev_ready[kMaxDevices];     // bit f: field index f uploaded
 static int g_sm_count[kMaxDevices];
@@ -424,12 +426,15 @@ int gf_init(int field)
         std::memset(g_host_tabs[fi], 0, sizeof(g_host_tabs[fi]));
         if (build_tables(field, g_host_tabs[fi], 256 * kTableWords) != 0) return GF_EFIELD;
         if (build_inverses(field, g_host_inv[fi]) != 0) return GF_EFIELD;
+        if (build_products(field, g_host_mul[fi]) != 0) return GF_EFIELD;
         g_host_ready[fi] = true;
     }
     if (!(g_dev_ready[dev] >> fi & 1u)) {
         if (cudaMemcpyToSymbol(g_dev_tabs, g_host_tabs[fi], sizeof(g_host_tabs[fi]),
                                (size_t)fi * sizeof(g_host_tabs[fi]), cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemcpyToSymbol(g_dev_inv, g_host_inv[fi], 256, (size_t)fi * 256, cudaMemcpyHostToDevice) !=
+                cudaSuccess ||
+            cudaMemcpyToSymbol(g_dev_mul, g_host_mul[fi], 65536, (size_t)fi * 65536, cudaMemcpyHostToDevice) !=
                 cudaSuccess)
             return GF_ECUDA;
         if (g_sm_count[dev] == 0) {
@@ -583,6 +588,46 @@ int gf_decode_batch(int field, const uint8_t *B, const uint8_t *C, uint8_t *A, i
     if (overlaps(D, cb, A, ab) || overlaps(D, cb, B, bb) || overlaps(D, cb, C, cb)) return GF_EOVERLAP;
     if ((rc = gf_invert_batch(field, C, D, rank, N, batch)) != GF_OK) return rc;
     return encode_on_stream(field, fi, B, D, A, N, N, M, batch, tls_stream);
+}
+
+int gf_verify_batch(int field, const uint8_t *A, const uint8_t *C, const uint8_t *B, const uint8_t *R, int t,
+                    int N, int K, size_t M, size_t batch, unsigned long long *mismatch, void *dev_ws,
+                    size_t ws_bytes)
+{
+    int fi, dev;
+    int rc = check_ready(field, &fi, &dev);
+    if (rc != GF_OK) return rc;
+    size_t ab, bb, cb;
+    rc = validate_encode(field, A, C, B, N, K, M, batch, &ab, &bb, &cb);
+    if (rc != GF_OK || M == 0 || batch == 0) return rc;
+    if (t < 1 || t > 32 || !R || !mismatch || !dev_ws) return GF_EARG;
+    auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+    const size_t u_bytes = al(batch * (size_t)N * t), y_bytes = al(batch * (size_t)t * M);
+    if (ws_bytes < u_bytes + 2 * y_bytes) return GF_EARG;
+    uint8_t *U = static_cast<uint8_t *>(dev_ws), *Y1 = U + u_bytes, *Y2 = Y1 + y_bytes;
+    void *mul = nullptr;
+    if (cudaGetSymbolAddress(&mul, g_dev_mul) != cudaSuccess) return GF_ECUDA;
+    const cudaStream_t st = tls_stream;
+    const size_t nu = batch * (size_t)N * t;
+    project_coeffs_kernel<<<(unsigned)((nu + 255) / 256), 256, 0, st>>>(
+        C, R, U, reinterpret_cast<const uint8_t *>(mul) + (size_t)fi * 65536, N, K, t, batch, field - 1);
+    if ((rc = launch_status()) != GF_OK) return rc;
+    if ((rc = encode_on_stream(field, fi, A, U, Y1, N, t, M, batch, st)) != GF_OK) return rc;   // sum_i u_i a_i
+    if ((rc = encode_on_stream(field, fi, B, R, Y2, K, t, M, batch, st)) != GF_OK) return rc;   // sum_k r_k b_k
+    if (cudaMemsetAsync(mismatch, 0, batch * sizeof(unsigned long long), st) != cudaSuccess) return GF_ECUDA;
+    const size_t len = (size_t)t * M;
+    unsigned gx = (unsigned)((len + 255) / 256);
+    if (gx > 64) gx = 64;
+    if (batch > 65535) {
+        for (size_t g0 = 0; g0 < batch; g0 += 65535) {
+            const size_t gn = batch - g0 < 65535 ? batch - g0 : 65535;
+            count_mismatch_kernel<<<dim3(gx, (unsigned)gn), 256, 0, st>>>(Y1 + g0 * len, Y2 + g0 * len, len,
+                                                                         mismatch + g0);
+        }
+    } else {
+        count_mismatch_kernel<<<dim3(gx, (unsigned)batch), 256, 0, st>>>(Y1, Y2, len, mismatch);
+    }
+    return launch_status();
 }
 
 int gf_fill_random2d(uint8_t *dst, size_t rows, size_t cols, uint64_t seed, uint64_t stream,

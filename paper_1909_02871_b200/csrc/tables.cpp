@@ -111,6 +111,15 @@ int build_tables(int field, uint32_t *out, size_t cap_words)
     return 0;
 }
 
+int build_products(int field, uint8_t *mul)
+{
+    if (field_width(field) < 0) return -1;
+    for (uint32_t a = 0; a < 256; a++)
+        for (uint32_t b = 0; b < 256; b++)
+            mul[a * 256 + b] = (a < (uint32_t)field && b < (uint32_t)field) ? (uint8_t)elem_mul(field, a, b) : 0;
+    return 0;
+}
+
 int build_inverses(int field, uint8_t *inv)
 {
     if (field_width(field) < 0) return -1;

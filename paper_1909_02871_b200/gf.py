@@ -44,6 +44,8 @@ _lib.gf_fill_random2d.argtypes = [_u8p, _sz, _sz, _u64, _u64, _u64, _u64, ctypes
 _lib.gf_host_tables.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_uint32), _sz]
 _lib.gf_version.argtypes = []
 _lib.gf_encode_path.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _sz, _sz, _sz]
+_lib.gf_verify_batch.argtypes = [ctypes.c_int, _u8p, _u8p, _u8p, _u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                 _sz, _sz, ctypes.c_void_p, _u8p, _sz]
 _lib.gf_invert_batch.argtypes = [ctypes.c_int, _u8p, _u8p, ctypes.c_void_p, ctypes.c_int, _sz]
 _lib.gf_decode_batch.argtypes = [ctypes.c_int, _u8p, _u8p, _u8p, ctypes.c_void_p, ctypes.c_int, _sz, _sz,
                                  _u8p, _sz]
@@ -55,7 +57,8 @@ TABLE_WORDS = 16          # uint32 words per coefficient in gf_host_tables
 # every symbol include/gfrlnc.h declares (tests check the library exports them)
 ABI_SYMBOLS = ("gf_init", "gf_maddrc", "gf_mulrc", "gf_encode_batch", "gf_encode_batch_host",
                "gf_set_stream", "gf_strerror", "gf_fill_random", "gf_fill_random2d",
-               "gf_host_tables", "gf_version", "gf_encode_path", "gf_invert_batch", "gf_decode_batch")
+               "gf_host_tables", "gf_version", "gf_encode_path", "gf_invert_batch", "gf_decode_batch",
+               "gf_verify_batch")
 
 
 class GFError(RuntimeError):
@@ -225,6 +228,26 @@ def decode_batch(field: int, B: torch.Tensor, C: torch.Tensor, workspace: torch.
         _check(_lib.gf_decode_batch(field, pb, pc, pa, rank.data_ptr(), N, M, batch, pw, workspace.numel()),
                "gf_decode_batch")
     return A, rank
+
+
+def verify_batch(field: int, A: torch.Tensor, C: torch.Tensor, B: torch.Tensor, R: torch.Tensor,
+                 workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """Freivalds check of B == encode(A, C) on the device with projections
+    R [batch, K, t]; returns mismatching byte counts per generation (int64)."""
+    batch, N, M = A.shape
+    K, t = R.shape[1], R.shape[2]
+    if tuple(C.shape) != (batch, N, K) or tuple(B.shape) != (batch, K, M) or R.shape[0] != batch:
+        raise ValueError("shape mismatch")
+    need = batch * N * t + 2 * batch * t * M + 48
+    if workspace is None:
+        workspace = torch.empty(need, dtype=torch.uint8, device=A.device)
+    mism = torch.empty(batch, dtype=torch.int64, device=A.device)
+    ptrs = [_dev_u8(x, n) for x, n in ((A, "A"), (C, "C"), (B, "B"), (R, "R"), (workspace, "workspace"))]
+    with _on_device(A.device):
+        _use_stream(A.device)
+        _check(_lib.gf_verify_batch(field, ptrs[0], ptrs[1], ptrs[2], ptrs[3], t, N, K, M, batch,
+                                    mism.data_ptr(), ptrs[4], workspace.numel()), "gf_verify_batch")
+    return mism
 
 
 def encode_batch_host(field: int, A: torch.Tensor, C: torch.Tensor, B: torch.Tensor,
