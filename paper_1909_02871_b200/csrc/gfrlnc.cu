@@ -13,6 +13,7 @@
 #include "encode_kernels.cuh"
 #include "encode_lanek.cuh"
 #include "encode_fused.cuh"
+#include "encode_prow.cuh"
 #include "decode_kernels.cuh"
 #include "region_kernels.cuh"
 #include "rng_kernels.cuh"
@@ -230,6 +231,60 @@ static int launch_fused(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, i
     return launch_status();
 }
 
+// shared-window address of the first dynamic shared-memory byte (the product-
+// row kernel places its tables at fixed addresses above it), probed once per device
+__global__ void smem_base_probe(uint32_t *out)
+{
+    extern __shared__ __align__(16) uint8_t dsm[];
+    if (threadIdx.x == 0) *out = (uint32_t)__cvta_generic_to_shared(dsm);
+}
+static uint32_t g_smem_base[kMaxDevices];
+static bool g_smem_base_ok[kMaxDevices];
+
+static int dyn_smem_base(uint32_t *base)
+{
+    int dev;
+    if (current_device(&dev) != GF_OK) return GF_ECUDA;
+    std::lock_guard<std::mutex> g(g_lock);
+    if (!g_smem_base_ok[dev]) {
+        uint32_t *d = nullptr;
+        if (cudaMalloc(&d, 4) != cudaSuccess) return GF_ECUDA;
+        smem_base_probe<<<1, 32, 16>>>(d);
+        uint32_t h = 0;
+        const bool ok = cudaMemcpy(&h, d, 4, cudaMemcpyDeviceToHost) == cudaSuccess;
+        cudaFree(d);
+        if (!ok) return GF_ECUDA;
+        g_smem_base[dev] = h;
+        g_smem_base_ok[dev] = true;
+    }
+    *base = g_smem_base[dev];
+    return GF_OK;
+}
+
+template <int F, int R>
+static int launch_prow(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M,
+                       size_t batch, cudaStream_t st)
+{
+    ProwParams p;
+    p.A = A; p.C = C; p.B = B; p.M = M; p.Mw = (uint32_t)(M / 4);
+    p.N = N; p.K = K; p.NG = (N + kPrS - 1) / kPrS;
+    p.tiles = (int)((p.Mw + PrGeom<R>::TW - 1) / PrGeom<R>::TW);
+    p.k_tiles = (K + kPrKC - 1) / kPrKC;
+    p.qmask4 = (uint32_t)(F - 1) * 0x01010101u;
+    const size_t grid = batch * (size_t)p.tiles * (size_t)p.k_tiles;
+    if (grid > 0x7FFFFFFFu) return GF_EARG;
+    uint32_t base;
+    int rc = dyn_smem_base(&base);
+    if (rc != GF_OK) return rc;
+    if (base + pr_low_bytes(p.NG) > kPrTable0) return GF_EARG;
+    const size_t smem = kPrTable0 + 0x20000u - base;
+    if (cudaFuncSetAttribute(encode_prow_kernel<F, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return GF_ECUDA;
+    encode_prow_kernel<F, R><<<(unsigned)grid, kPrThreads, smem, st>>>(p);
+    return launch_status();
+}
+
 template <int F>
 static int launch_lanek_kg(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M,
                            size_t batch, cudaStream_t st)
@@ -255,16 +310,18 @@ static int encode_path_override()
         if (!strcmp(e, "column")) return 1;
         if (!strcmp(e, "lanek")) return 2;
         if (!strcmp(e, "fused")) return 3;
+        if (!strcmp(e, "prow")) return 4;
         return 0;
     }();
     return v;
 }
 
 // 0 column (words), 1 column (bytes), 2 lane-k KG=1, 3 lane-k KG=2,
-// 4 fused KG=1, 5 fused KG=2.  The fused kernel (lane-k + column warps on one
+// 4 fused KG=1, 5 fused KG=2, 6 product-row (3 words per lane), 7 product-row
+// (4 words per lane: long packets).  The fused kernel (lane-k + column warps on one
 // tile) is correct but measured slower than lane-k alone (per-step barrier
 // coupling of the two roles): opt-in via GFRLNC_ENCODE_PATH=fused.
-static int encode_path(int field, int K, size_t M, const void *A, const void *B)
+static int encode_path(int field, int N, int K, size_t M, const void *A, const void *B)
 {
     const bool aligned = M % 4 == 0 && (reinterpret_cast<uintptr_t>(A) & 3u) == 0 &&
                          (reinterpret_cast<uintptr_t>(B) & 3u) == 0 && M / 4 < 0xFFFFFFFFull;
@@ -272,8 +329,10 @@ static int encode_path(int field, int K, size_t M, const void *A, const void *B)
     if (!aligned) return 1;
     if (ov == 1 || (ov == 0 && K < 24)) return 0;
     const int kg2 = K > 32 ? 1 : 0;      // (K > 64 uses 128 coded packets per CTA)
-    (void)field;
     if (ov == 3) return 4 + kg2;
+    // product rows: the coefficient buffer (N x 64 B) must fit below the tables
+    const bool prow_ok = N <= 768;
+    if (prow_ok && (ov == 4 || (ov == 0 && field >= 16 && K > 32))) return M >= 4096 ? 7 : 6;
     return 2 + kg2;
 }
 
@@ -281,7 +340,17 @@ static int encode_on_stream(int field, int fi, const uint8_t *A, const uint8_t *
                             int N, int K, size_t M, size_t batch, cudaStream_t st)
 {
     {
-        const int path = encode_path(field, K, M, A, B);
+        const int path = encode_path(field, N, K, M, A, B);
+        if (path >= 6) {
+            const bool r4 = path == 7;
+            switch (field) {
+            case 256: return r4 ? launch_prow<256, 4>(A, C, B, N, K, M, batch, st) : launch_prow<256, 3>(A, C, B, N, K, M, batch, st);
+            case 16: return r4 ? launch_prow<16, 4>(A, C, B, N, K, M, batch, st) : launch_prow<16, 3>(A, C, B, N, K, M, batch, st);
+            case 4: return r4 ? launch_prow<4, 4>(A, C, B, N, K, M, batch, st) : launch_prow<4, 3>(A, C, B, N, K, M, batch, st);
+            case 2: return r4 ? launch_prow<2, 4>(A, C, B, N, K, M, batch, st) : launch_prow<2, 3>(A, C, B, N, K, M, batch, st);
+            default: return GF_EFIELD;
+            }
+        }
         if (path >= 4) {
             void *tabs = nullptr;
             if (cudaGetSymbolAddress(&tabs, g_dev_tabs) != cudaSuccess) return GF_ECUDA;
@@ -383,7 +452,7 @@ int gf_encode_path(int field, int N, int K, size_t M, size_t a_align, size_t b_a
 {
     if (field_index(field) < 0) return GF_EFIELD;
     if (N < 1 || K < 1) return GF_EARG;
-    return encode_path(field, K, M, reinterpret_cast<const void *>(a_align & 15u),
+    return encode_path(field, N, K, M, reinterpret_cast<const void *>(a_align & 15u),
                        reinterpret_cast<const void *>(b_align & 15u));
 }
 

@@ -30,7 +30,7 @@ print("ok", want)
 ''' % ROOT
 
 
-@pytest.mark.parametrize("path", ["column", "lanek", "fused"])
+@pytest.mark.parametrize("path", ["column", "lanek", "fused", "prow"])
 def test_forced_encode_path(path):
     import torch
     if not torch.cuda.is_available():
