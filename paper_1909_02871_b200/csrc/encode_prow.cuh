@@ -1,48 +1,48 @@
 // encode_prow.cuh -- batched RLNC encode through per-source "product rows":
 // one shared-memory row per possible source BYTE value holding that byte's
-// products with all coded-packet coefficients.
+// products with 64 coded-packet coefficients.
 //
 //   B[g][k][m] = sum_i C[g][i][k] * A[g][i][m]          (Eq. 2)
 //
 // The paper multiplies a region by one coefficient with split lookup tables
 // indexed by source nibbles (Alg. 1).  Encode multiplies
 // each source byte by K coefficients, so here the table is indexed by the
-// whole source byte and returns K products at once:
+// whole source byte and returns 64 products at once:
 //     P_i[a][k] = C[g][i][k] * a          a = 0..255, k in the CTA's 64
 // (for GF(16)/GF(4)/GF(2) `*` is the packed product of every w-bit slot of the
 // byte, so one byte-indexed row serves every field).  One 16-byte shared-
 // memory load returns 16 finished products (16 byte-madds), against 4 bytes
 // per load and two loads per GF(256) product for the nibble-table layouts
-// (encode_lanek.cuh): the LSU pipe (128 B/clk/SM) then delivers 128
-// byte-madds/clk/SM.
+// (encode_lanek.cuh): the LSU pipe (128 B/clk/SM) delivers 128 byte-madds per
+// clock and SM.
 //
-// Layout and conflict freedom.  A "group" is S = 4 source packets; its table
-// is 256 rows x 256 B = 64 KiB: row a = [P_{4s}[a] | P_{4s+1}[a] | P_{4s+2}[a]
-// | P_{4s+3}[a]], 64 B (= 64 coded packets) each.  Because a row spans two
-// full bank sweeps, the bank of a 16-B chunk depends only on (source s mod 2,
-// chunk kc) and never on the data byte a.  The 8 lanes of a quarter-warp (one
-// LDS.128 wavefront) are 2 words x 4 chunks and the two words read sources of
-// opposite parity (lane word jw reads source (jw + t) mod 4 at step t), so
-// every LDS.128 is exactly 4 wavefronts for ANY data.
+// Steps, tables and conflict freedom.  A "step" consumes 4 source packets.
+// Its table is 256 rows x 256 B = 64 KiB, row a = [P_{4s}[a] | .. | P_{4s+3}[a]]
+// (64 B each).  A row spans two full bank sweeps, so the bank of a 16-B chunk
+// depends only on (source parity, coefficient chunk), never on the data byte
+// a.  The 8 lanes of a quarter-warp (one LDS.128 wavefront) are 2 words x 4
+// coefficient chunks, and the two words read sources of opposite parity
+// (lane word jw reads source (jw + t) mod 4 at sub-step t): every LDS.128 is
+// exactly 4 wavefronts for ANY data.  Address: prmt(a_word, col, 0x55j4) =
+// a * 256 + col, plus the table base as the LDS immediate -- one PRMT per
+// 16-byte gather.
 //
-// Address generation: the two tables live at shared-window addresses 0x10000
-// and 0x20000, so  addr = prmt(a_word, off, 0x76j4)  = [off.b0 = chunk offset,
-// a_word.byte j = row, off.b2 = table] is one PRMT per 16-byte gather.
-//
-// Table build (per group, all 512 threads, overlapped with the previous
-// group's gathers: double-buffered tables, one __syncthreads per group):
-//   * basis rows P_i[2^b] (b < 8) from C by the packed xtime chain
-//     (GF(2)-linearity: P[a] = XOR_{b in a} P[2^b]), staged one group ahead;
-//   * thread (chunk, hi) writes rows hi*8 .. hi*8+7 in Gray-code order, one
-//     16-byte XOR per row.
-// Build traffic per group: 64 KiB of stores against TW * 4 * 64 B... gathers,
-// i.e. 256 / (4 TW) of the gather traffic (17% for M = 1500).
-//
-// Work split: CTA = (generation, 64 coded packets, tile of TW words); lane =
-// (word, 16-coefficient chunk); R words per lane (48 / 64 accumulator
-// registers).  Source words are prefetched one group ahead straight from
-// global memory into registers (no staging).  Epilogue: 4x4 byte transpose
-// (8 PRMT) per 16 accumulator bytes, 4-byte stores (full 32-B sectors).
+// Pipeline.  Persistent CTAs (one per SM, 16 warps) walk a flattened sequence
+// of steps over their tiles; three table buffers (at compile-time shared
+// addresses, the loop is unrolled three times) and two basis buffers, with
+// mbarrier rings instead of CTA-wide barriers.  Step s of every warp:
+//   wait DONE(s-2), BASIS(s+1)  build table s+1          arrive BUILT(s+1)
+//   wait BUILT(s)               basis rows of step s+2   arrive BASIS(s+2)
+//   gather step s (LDS.128 product rows -> register accumulators)
+//   write back when step s ends a tile (4x4 byte transpose)   arrive DONE(s)
+// so a warp may run up to a step ahead of the slowest one.  Basis rows P[2^b]
+// = C * x^b come from the packed xtime chain (one coefficient word per thread,
+// loaded a step ahead); thread (chunk c16, hi) writes rows 8 hi .. 8 hi + 7 in
+// Gray-code order, one 16-B XOR per row (P[a] = XOR_{b in a} P[2^b],
+// GF(2)-linearity of the product).  Source words are prefetched one step
+// ahead into registers straight from global memory.
+// Build + basis traffic per step: 64 KiB + 16 KiB against 4 x 4 TW x 64 B of
+// gathers (21% for TW = 384 words).
 #pragma once
 #include <cstdint>
 
@@ -51,14 +51,18 @@
 namespace gfr {
 
 constexpr int kPrThreads = 512;
-constexpr int kPrKC = 64;                   // coded packets per CTA
-constexpr int kPrS = 4;                     // source packets per group (table)
-constexpr uint32_t kPrTable0 = 0x10000u;    // shared-window address of table 0 (table 1 at 0x20000)
-constexpr int kPrBasisBytes = 8 * 256;      // basis rows of one group
+constexpr int kPrWarps = kPrThreads / 32;
+constexpr int kPrKC = 64;                     // coded packets per CTA
+constexpr int kPrS = 4;                       // source packets per step
+constexpr uint32_t kPrBar = 0x0400u;          // mbarriers (6 x 8 B) at the dynamic window base
+constexpr uint32_t kPrTab0 = 0x1000u;         // tables u = 0, 1, 2 at kPrTab0 + u * 0x10000
+constexpr uint32_t kPrBasis = 0x31000u;       // basis rows: 2 buffers x 8 x 256 B
+constexpr int kPrBasisBytes = 8 * 256;
+constexpr uint32_t kPrSmemEnd = kPrBasis + 2 * kPrBasisBytes;
 
 template <int R> struct PrGeom {
-    static constexpr int WPW = 8;                       // words per warp per round
-    static constexpr int TW = R * (kPrThreads / 32) * WPW;   // words per tile
+    static constexpr int WPW = 8;                              // words per warp per round
+    static constexpr int TW = R * kPrWarps * WPW;              // words per tile
 };
 
 struct ProwParams {
@@ -68,10 +72,12 @@ struct ProwParams {
     size_t M;          // bytes per packet (multiple of 4)
     uint32_t Mw;       // words per packet
     int N, K;
-    int NG;            // groups: ceil(N / 4)
+    int NS;            // steps per tile: ceil(N / 4)
     int tiles;         // word tiles per packet
     int k_tiles;       // ceil(K / 64)
-    uint32_t qmask4;   // (q - 1) replicated in every byte
+    size_t ntiles;     // batch * tiles * k_tiles
+    uint32_t qmask4;   // q - 1 in every byte
+    int cword;         // coefficient rows can be read as 32-bit words
 };
 
 // x * v for packed elements (every w-bit slot of every byte, elements < q)
@@ -109,9 +115,12 @@ __device__ __forceinline__ uint4 lds128(uint32_t a)
     asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
     return v;
 }
-__device__ __forceinline__ uint32_t u4c(const uint4 &v, int q)
+template <uint32_t OFF> __device__ __forceinline__ uint4 lds128_at(uint32_t a)
 {
-    return q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w;
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4+%5];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a), "n"(OFF));
+    return v;
 }
 __device__ __forceinline__ uint32_t xor3(uint32_t a, uint32_t b, uint32_t c)
 {
@@ -119,104 +128,174 @@ __device__ __forceinline__ uint32_t xor3(uint32_t a, uint32_t b, uint32_t c)
     asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
     return d;
 }
+__device__ __forceinline__ uint32_t u4c(const uint4 &v, int q)
+{
+    return q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w;
+}
 __device__ __forceinline__ void xor4(uint4 &a, const uint4 &b)
 {
     a.x ^= b.x; a.y ^= b.y; a.z ^= b.z; a.w ^= b.w;
 }
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a)
+{
+    asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" :: "r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity)
+{
+    asm volatile("{ .reg .pred p;\n"
+                 "PR_WAIT_%=:\n"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                 "@!p bra PR_WAIT_%=;\n}" :: "r"(a), "r"(parity) : "memory");
+}
+
+// one work tile: generation g, coded packets k0 .. k0+63, words w0 .. w0+TW-1
+struct PrTile {
+    size_t g;
+    int k0;
+    uint32_t w0;
+};
+
+template <uint32_t V> struct PrU { static constexpr uint32_t value = V; };
 
 template <int F, int R>
 __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p)
 {
-    using G = PrGeom<R>;
-    constexpr int TW = G::TW;
-    extern __shared__ __align__(16) uint8_t pr_smem[];
-    const int NP = p.NG * kPrS;                                // padded source count
-    uint8_t *Cs = pr_smem;                                       // [NP][64] coefficients (masked)
-    const uint32_t bas_s = (uint32_t)__cvta_generic_to_shared(pr_smem) + (uint32_t)NP * kPrKC;   // [2][8][256]
+    constexpr int TW = PrGeom<R>::TW;
+    // mbarrier rings (2 objects each, by step parity).  Phases: DONE(x), x >= 0,
+    // on object x & 1 is phase x >> 1; BUILT(x), x >= 1, phase (x - 1) >> 1;
+    // BASIS(x), x >= 2, phase (x - 2) >> 1 (tables / basis rows of steps 0 and 1
+    // come from the prologue, ordered by __syncthreads).
+    constexpr uint32_t kDone = kPrBar, kBuilt = kPrBar + 16, kBas = kPrBar + 32;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const size_t bid = blockIdx.x;
-    const int kt = (int)(bid % (size_t)p.k_tiles);
-    const size_t rest = bid / (size_t)p.k_tiles;
-    const int tile = (int)(rest % (size_t)p.tiles);
-    const size_t g = rest / (size_t)p.tiles;
-    const int k0 = kt * kPrKC;
-    const uint32_t w0 = (uint32_t)tile * TW;
-    const uint8_t *Ag = p.A + g * (size_t)p.N * p.M;
+    const size_t ntile_cta = p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const uint32_t ntj = (uint32_t)ntile_cta;                 // tiles of this CTA
+    const uint32_t total = ntj * (uint32_t)p.NS;             // steps of this CTA
 
-    // ---- gather-lane geometry
+    auto tile_of = [&](uint32_t j) {                          // j-th tile of this CTA
+        const size_t t = blockIdx.x + (size_t)j * gridDim.x;
+        PrTile r;
+        const int kt = (int)(t % (size_t)p.k_tiles);
+        const size_t rest = t / (size_t)p.k_tiles;
+        r.w0 = (uint32_t)(rest % (size_t)p.tiles) * TW;
+        r.g = rest / (size_t)p.tiles;
+        r.k0 = kt * kPrKC;
+        return r;
+    };
+    // step cursors (tile j, step st of the tile): divisions only at tile changes
+    struct Cur {
+        uint32_t j;
+        int st;
+        PrTile T;
+    };
+    auto cur_next = [&](Cur &c) {
+        if (++c.st == p.NS) {
+            c.st = 0;
+            c.j++;
+            c.T = tile_of(c.j);
+        }
+    };
+
+    // ---- gather-lane geometry: quarter-warp = 2 words x 4 coefficient chunks
     const int qw = lane >> 3, ql = lane & 7;
     const int jw = ql >> 2, kc = ql & 3;
-    uint32_t wd[R];
-    bool wv[R];
+    uint32_t wofs[R];
 #pragma unroll
-    for (int r = 0; r < R; r++) {
-        wd[r] = w0 + (uint32_t)(r * (kPrThreads / 32 * 8) + warp * 8 + qw * 2 + jw);
-        wv[r] = wd[r] < p.Mw;
-    }
-    uint32_t areg[R][kPrS];
-    auto load_a = [&](int grp) {
+    for (int r = 0; r < R; r++) wofs[r] = (uint32_t)(r * kPrWarps * 8 + warp * 8 + qw * 2 + jw);
+
+    // source words of the cursor's step (4 sources x R words; sub-step t reads
+    // source (jw + t) & 3), 0 past N / Mw
+    auto load_a = [&](const Cur &c, uint32_t (&a)[R][kPrS]) {
+        if (c.j >= ntj) return;
+        const uint8_t *Ag = p.A + c.T.g * (size_t)p.N * p.M;
 #pragma unroll
         for (int t = 0; t < kPrS; t++) {
-            const int i = grp * kPrS + ((jw + t) & 3);
+            const int i = kPrS * c.st + ((jw + t) & 3);
             const uint32_t *row = reinterpret_cast<const uint32_t *>(Ag + (size_t)min(i, p.N - 1) * p.M);
 #pragma unroll
-            for (int r = 0; r < R; r++) areg[r][t] = (wv[r] && i < p.N) ? __ldg(row + wd[r]) : 0u;
+            for (int r = 0; r < R; r++) {
+                const uint32_t wd = c.T.w0 + wofs[r];
+                a[r][t] = (i < p.N && wd < p.Mw) ? __ldg(row + wd) : 0u;
+            }
         }
     };
-    load_a(0);
 
-    // ---- coefficients of this CTA's 64 coded packets, zero past N / K
-    {
-        const uint8_t *Cg = p.C + g * (size_t)p.N * p.K;
-        for (int e = tid; e < NP * kPrKC; e += kPrThreads) {
-            const int i = e >> 6, kk = e & 63;
-            Cs[e] = (i < p.N && k0 + kk < p.K) ? (uint8_t)(Cg[(size_t)i * p.K + k0 + kk] & p.qmask4) : (uint8_t)0;
-        }
-    }
-    __syncthreads();
-
-    // basis rows of group grp into basis buffer buf: thread = (bit b, 16-B
-    // chunk c16, word wq), 512 threads, one coefficient word each
-    auto basis = [&](int grp, int buf) {
-        const int wq = tid & 3, c16 = (tid >> 2) & 15, b = tid >> 6;
-        const uint32_t c =
-            *reinterpret_cast<const uint32_t *>(Cs + (grp * kPrS + (c16 >> 2)) * kPrKC + (c16 & 3) * 16 + wq * 4);
-        const uint32_t v = pr_basis<F>(c, b);
-        asm volatile("st.shared.u32 [%0], %1;" :: "r"(bas_s + buf * kPrBasisBytes + b * 256 + c16 * 16 + wq * 4),
-                     "r"(v) : "memory");
+    // basis thread geometry: word wq of 16-B chunk c16 (source c16 >> 2,
+    // coefficients 16 (c16 & 3) + 4 wq .. +3), bit b
+    const int bwq = tid & 3, bc16 = (tid >> 2) & 15, bb = tid >> 6;
+    // raw coefficient word of the cursor's step (masked to F_q at use, so the
+    // load is consumed a step later)
+    auto load_c = [&](const Cur &cc) -> uint32_t {
+        if (cc.j >= ntj) return 0u;
+        const int i = kPrS * cc.st + (bc16 >> 2);
+        if (i >= p.N) return 0u;
+        const uint8_t *crow = p.C + (cc.T.g * (size_t)p.N + (size_t)i) * p.K;
+        const int k = cc.T.k0 + 16 * (bc16 & 3) + 4 * bwq;
+        if (p.cword) return k < p.K ? __ldg(reinterpret_cast<const uint32_t *>(crow + k)) : 0u;
+        uint32_t c = 0;
+#pragma unroll
+        for (int e = 0; e < 4; e++)
+            if (k + e < p.K) c |= (uint32_t)__ldg(crow + k + e) << (8 * e);
+        return c;
     };
-    // table of one group from basis buffer bbuf into table tbuf: thread
-    // (chunk c16, hi) writes rows hi*8 .. hi*8+7 in Gray-code order
-    auto build = [&](int bbuf, int tbuf) {
+    auto basis = [&](uint32_t s, uint32_t c) {
+        if (s < total)
+            asm volatile("st.shared.u32 [%0], %1;" :: "r"(kPrBasis + (s & 1u) * kPrBasisBytes + bb * 256 +
+                                                         bc16 * 16 + bwq * 4),
+                         "r"(pr_basis<F>(c & p.qmask4, bb)) : "memory");
+    };
+    // table of step s at shared address tab: thread (chunk c16, hi) -> rows 8 hi + Gray(0..7)
+    auto build = [&](uint32_t s, uint32_t tab) {
+        if (s >= total) return;
         const int c16 = tid & 15, hi = tid >> 4;
-        const uint32_t bb = bas_s + bbuf * kPrBasisBytes + c16 * 16;
+        const uint32_t bsrc = kPrBasis + (s & 1u) * kPrBasisBytes + c16 * 16;
         uint4 v = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
         for (int j = 0; j < 5; j++) {
-            const uint4 b = lds128(bb + (3 + j) * 256);
+            const uint4 b = lds128(bsrc + (3 + j) * 256);
             const uint32_t m = 0u - ((uint32_t)(hi >> j) & 1u);
             v.x ^= b.x & m; v.y ^= b.y & m; v.z ^= b.z & m; v.w ^= b.w & m;
         }
-        uint4 bv[3];
-#pragma unroll
-        for (int b = 0; b < 3; b++) bv[b] = lds128(bb + b * 256);
-        const uint32_t tb = kPrTable0 + (uint32_t)tbuf * 0x10000u + (uint32_t)hi * 8u * 256u + (uint32_t)c16 * 16u;
-        sts128(tb + 0 * 256, v); xor4(v, bv[0]);
-        sts128(tb + 1 * 256, v); xor4(v, bv[1]);
-        sts128(tb + 3 * 256, v); xor4(v, bv[0]);
-        sts128(tb + 2 * 256, v); xor4(v, bv[2]);
-        sts128(tb + 6 * 256, v); xor4(v, bv[0]);
-        sts128(tb + 7 * 256, v); xor4(v, bv[1]);
-        sts128(tb + 5 * 256, v); xor4(v, bv[0]);
+        const uint4 b0 = lds128(bsrc), b1 = lds128(bsrc + 256), b2 = lds128(bsrc + 512);
+        const uint32_t tb = tab + (uint32_t)hi * 8u * 256u + (uint32_t)c16 * 16u;
+        sts128(tb + 0 * 256, v); xor4(v, b0);
+        sts128(tb + 1 * 256, v); xor4(v, b1);
+        sts128(tb + 3 * 256, v); xor4(v, b0);
+        sts128(tb + 2 * 256, v); xor4(v, b2);
+        sts128(tb + 6 * 256, v); xor4(v, b0);
+        sts128(tb + 7 * 256, v); xor4(v, b1);
+        sts128(tb + 5 * 256, v); xor4(v, b0);
         sts128(tb + 4 * 256, v);
     };
 
-    basis(0, 0);
-    if (p.NG > 1) basis(1, 1);
+    if (tid == 0) {
+#pragma unroll
+        for (int b = 0; b < 6; b++) mbar_init(kPrBar + 8 * b, kPrWarps);
+    }
+    // ---- prologue: basis rows of steps 0 and 1, table 0, source words of step 0
+    Cur ca;
+    ca.j = 0; ca.st = 0; ca.T = tile_of(0);
+    Cur cc = ca;
+    uint32_t areg[R][kPrS];
+    load_a(ca, areg);
+    cur_next(ca);                                             // ca at step 1
+    uint32_t creg;
+    {
+        const uint32_t c0 = load_c(cc); cur_next(cc);
+        const uint32_t c1 = load_c(cc); cur_next(cc);
+        creg = load_c(cc); cur_next(cc);                      // step 2; cc at step 3
+        basis(0, c0);
+        basis(1, c1);
+    }
     __syncthreads();
-    build(0, 0);
+    build(0, kPrTab0);
     __syncthreads();
+    int st_g = 0;                                             // step-in-tile of the gather step
+    uint32_t j_g = 0;
 
     uint4 acc[R][4];
 #pragma unroll
@@ -224,32 +303,36 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
 #pragma unroll
         for (int j = 0; j < 4; j++) acc[r][j] = make_uint4(0u, 0u, 0u, 0u);
 
-#pragma unroll 1
-    for (int it = 0; it < p.NG; it++) {
-        if (it + 2 < p.NG) basis(it + 2, it & 1);
-        if (it + 1 < p.NG) build((it + 1) & 1, (it + 1) & 1);
-        const uint32_t tsel = (1u + (uint32_t)(it & 1)) << 16;
-        const bool more = it + 1 < p.NG;
+    auto step = [&](uint32_t s, auto U) {
+        constexpr uint32_t u = decltype(U)::value;            // table buffer of step s
+        constexpr uint32_t un = (u + 1) % 3;                  // table buffer of step s + 1
+        const uint32_t par = s & 1u;
+        // ---- build table s + 1
+        if (s >= 2) mbar_wait(kDone + par * 8u, ((s - 2) >> 1) & 1u);          // gathers of s-2 done
+        if (s >= 1) mbar_wait(kBas + (par ^ 1u) * 8u, ((s - 1) >> 1) & 1u);   // basis rows of s+1
+        build(s + 1, kPrTab0 + un * 0x10000u);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(kBuilt + (par ^ 1u) * 8u);
+        // ---- basis rows of step s + 2 (their buffer held step s's, read by build(s))
+        if (s >= 1) mbar_wait(kBuilt + par * 8u, ((s - 1) >> 1) & 1u);
+        basis(s + 2, creg);
+        creg = load_c(cc);                                    // step s + 3
+        cur_next(cc);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(kBas + par * 8u);
+        // ---- gathers of step s
 #pragma unroll
         for (int tp = 0; tp < kPrS; tp += 2) {
-            // sources (jw + tp) and (jw + tp + 1) mod 4 of the group: two gathers per
-            // accumulator, folded with one 3-input XOR
-            const uint32_t off0 = tsel | (uint32_t)(((jw + tp) & 3) * 64 + kc * 16);
-            const uint32_t off1 = tsel | (uint32_t)(((jw + tp + 1) & 3) * 64 + kc * 16);
-            const int in0 = (it + 1) * kPrS + ((jw + tp) & 3), in1 = (it + 1) * kPrS + ((jw + tp + 1) & 3);
-            const uint32_t *nrow0 = reinterpret_cast<const uint32_t *>(Ag + (size_t)min(in0, p.N - 1) * p.M);
-            const uint32_t *nrow1 = reinterpret_cast<const uint32_t *>(Ag + (size_t)min(in1, p.N - 1) * p.M);
+            const uint32_t col0 = (uint32_t)(((jw + tp) & 3) * 64 + kc * 16);
+            const uint32_t col1 = (uint32_t)(((jw + tp + 1) & 3) * 64 + kc * 16);
 #pragma unroll
             for (int r = 0; r < R; r++) {
-                const uint32_t a0 = areg[r][tp], a1 = areg[r][tp + 1];
-                if (more) {
-                    areg[r][tp] = (wv[r] && in0 < p.N) ? __ldg(nrow0 + wd[r]) : 0u;
-                    areg[r][tp + 1] = (wv[r] && in1 < p.N) ? __ldg(nrow1 + wd[r]) : 0u;
-                }
 #pragma unroll
                 for (int j = 0; j < 4; j++) {
-                    const uint4 v0 = lds128(prmt(a0, off0, 0x7604u | (j << 4)));
-                    const uint4 v1 = lds128(prmt(a1, off1, 0x7604u | (j << 4)));
+                    const uint4 v0 =
+                        lds128_at<kPrTab0 + u * 0x10000u>(prmt(areg[r][tp], col0, 0x5504u | (j << 4)));
+                    const uint4 v1 =
+                        lds128_at<kPrTab0 + u * 0x10000u>(prmt(areg[r][tp + 1], col1, 0x5504u | (j << 4)));
                     acc[r][j].x = xor3(acc[r][j].x, v0.x, v1.x);
                     acc[r][j].y = xor3(acc[r][j].y, v0.y, v1.y);
                     acc[r][j].z = xor3(acc[r][j].z, v0.z, v1.z);
@@ -257,37 +340,47 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
                 }
             }
         }
-        __syncthreads();
-    }
-
-    // ---- epilogue: acc[r][j] word q holds B[k0 + 16 kc + 4q + e][4 wd + j], e = byte;
-    // transpose 4x4 bytes so that each output word is one coded packet's 4 bytes
+        load_a(ca, areg);                                     // step s + 1
+        cur_next(ca);
+        if (++st_g == p.NS) {
+            st_g = 0;
+            // ---- write back the tile: acc[r][j] word q holds B[k0 + 16 kc + 4q + e][4 wd + j]
+            // (e = byte); a 4x4 byte transpose makes each word one coded packet's 4 bytes
+            const PrTile T = tile_of(j_g++);
 #pragma unroll
-    for (int r = 0; r < R; r++) {
-        if (!wv[r]) continue;
+            for (int r = 0; r < R; r++) {
+                const uint32_t wd = T.w0 + wofs[r];
+                if (wd < p.Mw) {
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
-            const uint32_t x0 = u4c(acc[r][0], q), x1 = u4c(acc[r][1], q);
-            const uint32_t x2 = u4c(acc[r][2], q), x3 = u4c(acc[r][3], q);
-            const uint32_t t0 = prmt(x0, x1, 0x5140u), t1 = prmt(x0, x1, 0x7362u);
-            const uint32_t t2 = prmt(x2, x3, 0x5140u), t3 = prmt(x2, x3, 0x7362u);
-            const uint32_t y[4] = {prmt(t0, t2, 0x5410u), prmt(t0, t2, 0x7632u), prmt(t1, t3, 0x5410u),
-                                   prmt(t1, t3, 0x7632u)};
+                    for (int q = 0; q < 4; q++) {
+                        const uint32_t x0 = u4c(acc[r][0], q), x1 = u4c(acc[r][1], q);
+                        const uint32_t x2 = u4c(acc[r][2], q), x3 = u4c(acc[r][3], q);
+                        const uint32_t t0 = prmt(x0, x1, 0x5140u), t1 = prmt(x0, x1, 0x7362u);
+                        const uint32_t t2 = prmt(x2, x3, 0x5140u), t3 = prmt(x2, x3, 0x7362u);
+                        const uint32_t y[4] = {prmt(t0, t2, 0x5410u), prmt(t0, t2, 0x7632u),
+                                               prmt(t1, t3, 0x5410u), prmt(t1, t3, 0x7632u)};
 #pragma unroll
-            for (int e = 0; e < 4; e++) {
-                const int k = k0 + kc * 16 + q * 4 + e;
-                if (k < p.K)
-                    reinterpret_cast<uint32_t *>(p.B + (g * (size_t)p.K + (size_t)k) * p.M)[wd[r]] = y[e];
+                        for (int e = 0; e < 4; e++) {
+                            const int k = T.k0 + kc * 16 + q * 4 + e;
+                            if (k < p.K)
+                                reinterpret_cast<uint32_t *>(p.B + (T.g * (size_t)p.K + (size_t)k) * p.M)[wd] = y[e];
+                        }
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < 4; j++) acc[r][j] = make_uint4(0u, 0u, 0u, 0u);
             }
         }
-    }
-}
+        __syncwarp();
+        if (lane == 0) mbar_arrive(kDone + par * 8u);
+    };
 
-// dynamic shared memory: everything from the window base up to the end of
-// table 1 (0x30000); the coefficient and basis buffers sit below table 0
-__host__ __device__ constexpr size_t pr_low_bytes(int NG)
-{
-    return (size_t)NG * kPrS * kPrKC + 2 * (size_t)kPrBasisBytes;
+#pragma unroll 1
+    for (uint32_t s = 0; s < total; s += 3) {
+        step(s, PrU<0>{});
+        if (s + 1 < total) step(s + 1, PrU<1>{});
+        if (s + 2 < total) step(s + 2, PrU<2>{});
+    }
 }
 
 }  // namespace gfr

@@ -267,17 +267,23 @@ static int launch_prow(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, in
 {
     ProwParams p;
     p.A = A; p.C = C; p.B = B; p.M = M; p.Mw = (uint32_t)(M / 4);
-    p.N = N; p.K = K; p.NG = (N + kPrS - 1) / kPrS;
+    p.N = N; p.K = K; p.NS = (N + kPrS - 1) / kPrS;
     p.tiles = (int)((p.Mw + PrGeom<R>::TW - 1) / PrGeom<R>::TW);
     p.k_tiles = (K + kPrKC - 1) / kPrKC;
     p.qmask4 = (uint32_t)(F - 1) * 0x01010101u;
-    const size_t grid = batch * (size_t)p.tiles * (size_t)p.k_tiles;
-    if (grid > 0x7FFFFFFFu) return GF_EARG;
+    p.cword = (K % 4 == 0 && (reinterpret_cast<uintptr_t>(C) & 3u) == 0) ? 1 : 0;
+    p.ntiles = batch * (size_t)p.tiles * (size_t)p.k_tiles;
+    int dev;
+    if (current_device(&dev) != GF_OK) return GF_ECUDA;
+    const size_t sms = (size_t)(g_sm_count[dev] > 0 ? g_sm_count[dev] : 148);
+    const size_t grid = p.ntiles < sms ? p.ntiles : sms;      // persistent: one CTA per SM
+    // steps per CTA must fit 32 bits
+    if ((p.ntiles + grid - 1) / grid * (size_t)p.NS > 0x7FFFFFF0u) return GF_EARG;
     uint32_t base;
     int rc = dyn_smem_base(&base);
     if (rc != GF_OK) return rc;
-    if (base + pr_low_bytes(p.NG) > kPrTable0) return GF_EARG;
-    const size_t smem = kPrTable0 + 0x20000u - base;
+    if (base > kPrBar) return GF_EARG;                        // layout needs the window to start at <= 0x400
+    const size_t smem = kPrSmemEnd - base;
     if (cudaFuncSetAttribute(encode_prow_kernel<F, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
         return GF_ECUDA;
@@ -317,8 +323,7 @@ static int encode_path_override()
 }
 
 // 0 column (words), 1 column (bytes), 2 lane-k KG=1, 3 lane-k KG=2,
-// 4 fused KG=1, 5 fused KG=2, 6 product-row (3 words per lane), 7 product-row
-// (4 words per lane: long packets).  The fused kernel (lane-k + column warps on one
+// 4 fused KG=1, 5 fused KG=2, 6 product-row.  The fused kernel (lane-k + column warps on one
 // tile) is correct but measured slower than lane-k alone (per-step barrier
 // coupling of the two roles): opt-in via GFRLNC_ENCODE_PATH=fused.
 static int encode_path(int field, int N, int K, size_t M, const void *A, const void *B)
@@ -330,9 +335,7 @@ static int encode_path(int field, int N, int K, size_t M, const void *A, const v
     if (ov == 1 || (ov == 0 && K < 24)) return 0;
     const int kg2 = K > 32 ? 1 : 0;      // (K > 64 uses 128 coded packets per CTA)
     if (ov == 3) return 4 + kg2;
-    // product rows: the coefficient buffer (N x 64 B) must fit below the tables
-    const bool prow_ok = N <= 768;
-    if (prow_ok && (ov == 4 || (ov == 0 && field >= 16 && K > 32))) return M >= 4096 ? 7 : 6;
+    if ((ov == 4 || (ov == 0 && field >= 16 && K > 32))) return 6;
     return 2 + kg2;
 }
 
@@ -342,12 +345,11 @@ static int encode_on_stream(int field, int fi, const uint8_t *A, const uint8_t *
     {
         const int path = encode_path(field, N, K, M, A, B);
         if (path >= 6) {
-            const bool r4 = path == 7;
             switch (field) {
-            case 256: return r4 ? launch_prow<256, 4>(A, C, B, N, K, M, batch, st) : launch_prow<256, 3>(A, C, B, N, K, M, batch, st);
-            case 16: return r4 ? launch_prow<16, 4>(A, C, B, N, K, M, batch, st) : launch_prow<16, 3>(A, C, B, N, K, M, batch, st);
-            case 4: return r4 ? launch_prow<4, 4>(A, C, B, N, K, M, batch, st) : launch_prow<4, 3>(A, C, B, N, K, M, batch, st);
-            case 2: return r4 ? launch_prow<2, 4>(A, C, B, N, K, M, batch, st) : launch_prow<2, 3>(A, C, B, N, K, M, batch, st);
+            case 256: return launch_prow<256, 3>(A, C, B, N, K, M, batch, st);
+            case 16: return launch_prow<16, 3>(A, C, B, N, K, M, batch, st);
+            case 4: return launch_prow<4, 3>(A, C, B, N, K, M, batch, st);
+            case 2: return launch_prow<2, 3>(A, C, B, N, K, M, batch, st);
             default: return GF_EFIELD;
             }
         }

@@ -79,7 +79,7 @@ def version() -> int:
     return _lib.gf_version()
 
 
-ENCODE_PATHS = {0: "column-words", 1: "column-bytes", 2: "lanek-32", 3: "lanek-64", 4: "fused-32", 6: "prow-3", 7: "prow-4",
+ENCODE_PATHS = {0: "column-words", 1: "column-bytes", 2: "lanek-32", 3: "lanek-64", 4: "fused-32", 6: "prow",
                 5: "fused-64"}
 
 
