@@ -29,17 +29,17 @@
 //
 // Pipeline.  Persistent CTAs (one per SM, 16 warps) walk a flattened sequence
 // of steps over their tiles; three table buffers (at compile-time shared
-// addresses, the loop is unrolled three times) and two basis buffers, with
+// addresses, the loop is unrolled three times) and three basis buffers, with
 // mbarrier rings instead of CTA-wide barriers.  Step s of every warp:
 //   wait DONE(s-2), BASIS(s+1)  build table s+1          arrive BUILT(s+1)
-//   wait BUILT(s)               basis rows of step s+2   arrive BASIS(s+2)
+//   wait BUILT(s)               basis rows of step s+3   arrive BASIS(s+3)
 //   gather step s (LDS.128 product rows -> register accumulators)
 //   write back when step s ends a tile (4x4 byte transpose)   arrive DONE(s)
 // so a warp may run up to a step ahead of the slowest one.  Basis rows P[2^b]
 // = C * x^b come from the packed xtime chain (one coefficient word per thread,
-// loaded a step ahead); thread (chunk c16, hi) writes rows 8 hi .. 8 hi + 7 in
-// Gray-code order, one 16-B XOR per row (P[a] = XOR_{b in a} P[2^b],
-// GF(2)-linearity of the product).  Source words are prefetched one step
+// loaded a step ahead, rows computed two steps ahead of their table); thread
+// (chunk c16, hi) writes rows 8 hi .. 8 hi + 7 in Gray-code order, one 16-B
+// XOR per row (P[a] = XOR_{b in a} P[2^b], GF(2)-linearity of the product).  Source words are prefetched one step
 // ahead into registers straight from global memory.
 // Build + basis traffic per step: 64 KiB + 16 KiB against 4 x 4 TW x 64 B of
 // gathers (21% for TW = 384 words).
@@ -56,9 +56,9 @@ constexpr int kPrKC = 64;                     // coded packets per CTA
 constexpr int kPrS = 4;                       // source packets per step
 constexpr uint32_t kPrBar = 0x0400u;          // mbarriers (6 x 8 B) at the dynamic window base
 constexpr uint32_t kPrTab0 = 0x1000u;         // tables u = 0, 1, 2 at kPrTab0 + u * 0x10000
-constexpr uint32_t kPrBasis = 0x31000u;       // basis rows: 2 buffers x 8 x 256 B
+constexpr uint32_t kPrBasis = 0x31000u;       // basis rows: 3 buffers x 8 x 256 B
 constexpr int kPrBasisBytes = 8 * 256;
-constexpr uint32_t kPrSmemEnd = kPrBasis + 2 * kPrBasisBytes;
+constexpr uint32_t kPrSmemEnd = kPrBasis + 3 * kPrBasisBytes;
 
 template <int R> struct PrGeom {
     static constexpr int WPW = 8;                              // words per warp per round
@@ -148,7 +148,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity)
 {
     asm volatile("{ .reg .pred p;\n"
                  "PR_WAIT_%=:\n"
-                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
                  "@!p bra PR_WAIT_%=;\n}" :: "r"(a), "r"(parity) : "memory");
 }
 
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
     constexpr int TW = PrGeom<R>::TW;
     // mbarrier rings (2 objects each, by step parity).  Phases: DONE(x), x >= 0,
     // on object x & 1 is phase x >> 1; BUILT(x), x >= 1, phase (x - 1) >> 1;
-    // BASIS(x), x >= 2, phase (x - 2) >> 1 (tables / basis rows of steps 0 and 1
+    // BASIS(x), x >= 3, phase (x - 3) >> 1 (table 0 and basis rows of steps 0..2
     // come from the prologue, ordered by __syncthreads).
     constexpr uint32_t kDone = kPrBar, kBuilt = kPrBar + 16, kBas = kPrBar + 32;
 
@@ -242,17 +242,18 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
             if (k + e < p.K) c |= (uint32_t)__ldg(crow + k + e) << (8 * e);
         return c;
     };
-    auto basis = [&](uint32_t s, uint32_t c) {
+    auto basis = [&](uint32_t s, uint32_t c, uint32_t buf) {  // buf = s % 3
         if (s < total)
-            asm volatile("st.shared.u32 [%0], %1;" :: "r"(kPrBasis + (s & 1u) * kPrBasisBytes + bb * 256 +
+            asm volatile("st.shared.u32 [%0], %1;" :: "r"(kPrBasis + buf * kPrBasisBytes + bb * 256 +
                                                          bc16 * 16 + bwq * 4),
                          "r"(pr_basis<F>(c & p.qmask4, bb)) : "memory");
     };
     // table of step s at shared address tab: thread (chunk c16, hi) -> rows 8 hi + Gray(0..7)
-    auto build = [&](uint32_t s, uint32_t tab) {
+    auto build = [&](uint32_t s, uint32_t buf) {               // buf = s % 3
         if (s >= total) return;
         const int c16 = tid & 15, hi = tid >> 4;
-        const uint32_t bsrc = kPrBasis + (s & 1u) * kPrBasisBytes + c16 * 16;
+        const uint32_t bsrc = kPrBasis + buf * kPrBasisBytes + c16 * 16;
+        const uint32_t tab = kPrTab0 + buf * 0x10000u;
         uint4 v = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
         for (int j = 0; j < 5; j++) {
@@ -276,7 +277,7 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
 #pragma unroll
         for (int b = 0; b < 6; b++) mbar_init(kPrBar + 8 * b, kPrWarps);
     }
-    // ---- prologue: basis rows of steps 0 and 1, table 0, source words of step 0
+    // ---- prologue: basis rows of steps 0..2, table 0, source words of step 0
     Cur ca;
     ca.j = 0; ca.st = 0; ca.T = tile_of(0);
     Cur cc = ca;
@@ -287,12 +288,14 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
     {
         const uint32_t c0 = load_c(cc); cur_next(cc);
         const uint32_t c1 = load_c(cc); cur_next(cc);
-        creg = load_c(cc); cur_next(cc);                      // step 2; cc at step 3
-        basis(0, c0);
-        basis(1, c1);
+        const uint32_t c2 = load_c(cc); cur_next(cc);
+        creg = load_c(cc); cur_next(cc);                      // step 3; cc at step 4
+        basis(0, c0, 0);
+        basis(1, c1, 1);
+        basis(2, c2, 2);
     }
     __syncthreads();
-    build(0, kPrTab0);
+    build(0, 0);
     __syncthreads();
     int st_g = 0;                                             // step-in-tile of the gather step
     uint32_t j_g = 0;
@@ -309,17 +312,17 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
         const uint32_t par = s & 1u;
         // ---- build table s + 1
         if (s >= 2) mbar_wait(kDone + par * 8u, ((s - 2) >> 1) & 1u);          // gathers of s-2 done
-        if (s >= 1) mbar_wait(kBas + (par ^ 1u) * 8u, ((s - 1) >> 1) & 1u);   // basis rows of s+1
-        build(s + 1, kPrTab0 + un * 0x10000u);
+        if (s >= 2) mbar_wait(kBas + (par ^ 1u) * 8u, ((s - 2) >> 1) & 1u);   // basis rows of s+1
+        build(s + 1, un);
         __syncwarp();
         if (lane == 0) mbar_arrive(kBuilt + (par ^ 1u) * 8u);
-        // ---- basis rows of step s + 2 (their buffer held step s's, read by build(s))
+        // ---- basis rows of step s + 3 (their buffer held step s's, read by build(s))
         if (s >= 1) mbar_wait(kBuilt + par * 8u, ((s - 1) >> 1) & 1u);
-        basis(s + 2, creg);
-        creg = load_c(cc);                                    // step s + 3
+        basis(s + 3, creg, u);
+        creg = load_c(cc);                                    // step s + 4
         cur_next(cc);
         __syncwarp();
-        if (lane == 0) mbar_arrive(kBas + par * 8u);
+        if (lane == 0) mbar_arrive(kBas + (par ^ 1u) * 8u);
         // ---- gathers of step s
 #pragma unroll
         for (int tp = 0; tp < kPrS; tp += 2) {
