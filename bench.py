@@ -375,6 +375,9 @@ LANEK = {2: (4, 1, 15), 4: (2, 1, 15), 16: (1, 1, 15), 256: (1, 2, 30)}   # SG, 
 def dominant_roofline(q, N, K, Ms, gens, path, kernel_s, peaks):
     """Roofline of the encode launch.
 
+    The product-row kernel is bound by the shared-memory pipe: algorithmic
+    smem bytes = one gathered byte per byte-madd + the product tables written
+    (256 x 64 B per source, coded-packet tile and 384-word tile).
     lane-k kernels are bound by the shared-memory pipe: algorithmic smem bytes
     = gathers (4 B per gathered word, G per (step, k, word)) + table build
     (R rows x 4 B per (step, word), once per CTA k-tile); peak = 148 SMs x
@@ -387,7 +390,22 @@ def dominant_roofline(q, N, K, Ms, gens, path, kernel_s, peaks):
     hbm_ach = hbm_bytes / kernel_s / 1e9
     hbm = {"achieved": round(hbm_ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
            "frac": round(hbm_ach / peaks["hbm_gbs"], 4), "peak_source": peaks["source"]}
-    if path.startswith("lanek"):
+    if path == "prow":
+        # product-row kernel: every byte-madd is one gathered product byte;
+        # tables: 256 rows x 64 B per (source, 64-coded-packet tile, word tile)
+        tw = 384
+        m_tiles = -(-(Ms // 4) // tw)
+        k_tiles = -(-K // 64)
+        n_pad = -(-N // 4) * 4
+        smem_bytes = bm + gens * n_pad * k_tiles * m_tiles * 256 * 64
+        peak = N_SM * SMEM_BYTES_PER_SM_CLK * clk
+        ach = smem_bytes / kernel_s
+        roof = {"bound": "smem", "achieved": round(ach / 1e12, 3), "peak": round(peak / 1e12, 3),
+                "unit": "TB/s", "frac": round(ach / peak, 4),
+                "peak_source": f"{N_SM} SMs x {SMEM_BYTES_PER_SM_CLK} B/clk shared-memory pipe x "
+                               f"{peaks['sm_max_mhz']:.0f} MHz (DESIGN.md 'roofline')",
+                "smem_bytes_per_launch": smem_bytes}
+    elif path.startswith("lanek"):
         SG, G, R = LANEK[q]
         ktl = 64 if path == "lanek-64" else 32
         steps = -(-N // SG)
