@@ -167,6 +167,13 @@ int gf_host_tables(int field, uint32_t *out, size_t cap_words);
  * kernel with 32 / 64, or GF_EFIELD / GF_EARG. */
 int gf_encode_path(int field, int N, int K, size_t M, size_t a_align, size_t b_align);
 
+/* Harness-only (experiments, forced-path tests): force the encode kernel of
+ * the calling thread's gf_encode_batch calls.  0 = automatic (default), 1 =
+ * column kernel, 2 = lane-k, 3 = fused lane-k + column, 4 = product-row.
+ * Thread-local; returns GF_OK or GF_EARG.  Takes precedence over the
+ * GFRLNC_ENCODE_PATH environment variable. */
+int gf_set_encode_path(int path);
+
 /* Library version (major * 10000 + minor * 100 + patch). */
 int gf_version(void);
 

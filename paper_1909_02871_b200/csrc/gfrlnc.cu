@@ -36,6 +36,7 @@ static uint32_t g_dev_ready[kMaxDevices];     // bit f: field index f uploaded
 static int g_sm_count[kMaxDevices];
 static std::mutex g_lock;
 static thread_local cudaStream_t tls_stream = nullptr;
+static thread_local int tls_path = 0;          // harness: forced encode path (gf_set_encode_path)
 
 // experiment knobs (never needed in production): integer environment variable
 static int env_int(const char *name, int dflt)
@@ -310,6 +311,7 @@ static int launch_lanek_kg(const uint8_t *A, const uint8_t *C, uint8_t *B, int N
 // GFRLNC_ENCODE_PATH=column|lanek overrides (experiments).
 static int encode_path_override()
 {
+    if (tls_path) return tls_path;
     static const int v = [] {
         const char *e = getenv("GFRLNC_ENCODE_PATH");
         if (!e) return 0;
@@ -470,6 +472,13 @@ const char *gf_strerror(int status)
     case GF_ECUDA: return "CUDA launch or runtime failure";
     default: return "unknown status";
     }
+}
+
+int gf_set_encode_path(int path)
+{
+    if (path < 0 || path > 4) return GF_EARG;
+    tls_path = path;
+    return GF_OK;
 }
 
 int gf_set_stream(void *cuda_stream)

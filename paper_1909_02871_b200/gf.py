@@ -43,6 +43,7 @@ _lib.gf_fill_random.argtypes = [_u8p, _sz, _u64, _u64, _u64, ctypes.c_uint8]
 _lib.gf_fill_random2d.argtypes = [_u8p, _sz, _sz, _u64, _u64, _u64, _u64, ctypes.c_uint8]
 _lib.gf_host_tables.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_uint32), _sz]
 _lib.gf_version.argtypes = []
+_lib.gf_set_encode_path.argtypes = [ctypes.c_int]
 _lib.gf_encode_path.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _sz, _sz, _sz]
 _lib.gf_verify_batch.argtypes = [ctypes.c_int, _u8p, _u8p, _u8p, _u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                  _sz, _sz, ctypes.c_void_p, _u8p, _sz]
@@ -58,7 +59,7 @@ TABLE_WORDS = 16          # uint32 words per coefficient in gf_host_tables
 ABI_SYMBOLS = ("gf_init", "gf_maddrc", "gf_mulrc", "gf_encode_batch", "gf_encode_batch_host",
                "gf_set_stream", "gf_strerror", "gf_fill_random", "gf_fill_random2d",
                "gf_host_tables", "gf_version", "gf_encode_path", "gf_invert_batch", "gf_decode_batch",
-               "gf_verify_batch")
+               "gf_verify_batch", "gf_set_encode_path")
 
 
 class GFError(RuntimeError):
@@ -81,6 +82,14 @@ def version() -> int:
 
 ENCODE_PATHS = {0: "column-words", 1: "column-bytes", 2: "lanek-32", 3: "lanek-64", 4: "fused-32", 6: "prow",
                 5: "fused-64"}
+
+
+FORCE_PATHS = {"auto": 0, "column": 1, "lanek": 2, "fused": 3, "prow": 4}
+
+
+def set_encode_path(name: str) -> None:
+    """Harness-only: force the encode kernel of this thread's encode calls."""
+    _check(_lib.gf_set_encode_path(FORCE_PATHS[name]), "gf_set_encode_path")
 
 
 def encode_path(field: int, N: int, K: int, M: int, a_align: int = 0, b_align: int = 0) -> str:
