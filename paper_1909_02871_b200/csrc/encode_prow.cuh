@@ -27,22 +27,25 @@
 // a * 256 + col, plus the table base as the LDS immediate -- one PRMT per
 // 16-byte gather.
 //
-// Pipeline.  Persistent CTAs (one per SM, 16 warps) walk a flattened sequence
-// of steps over their tiles; three table buffers (at compile-time shared
-// addresses, the loop is unrolled three times) and three basis buffers, with
-// mbarrier rings instead of CTA-wide barriers.  Step s of every warp:
-//   wait DONE(s-2), BASIS(s+1)  build table s+1          arrive BUILT(s+1)
-//   wait BUILT(s)               basis rows of step s+3   arrive BASIS(s+3)
-//   gather step s (LDS.128 product rows -> register accumulators)
-//   write back when step s ends a tile (4x4 byte transpose)   arrive DONE(s)
-// so a warp may run up to a step ahead of the slowest one.  Basis rows P[2^b]
-// = C * x^b come from the packed xtime chain (one coefficient word per thread,
-// loaded a step ahead, rows computed two steps ahead of their table); thread
-// (chunk c16, hi) writes rows 8 hi .. 8 hi + 7 in Gray-code order, one 16-B
-// XOR per row (P[a] = XOR_{b in a} P[2^b], GF(2)-linearity of the product).  Source words are prefetched one step
-// ahead into registers straight from global memory.
-// Build + basis traffic per step: 64 KiB + 16 KiB against 4 x 4 TW x 64 B of
-// gathers (21% for TW = 384 words).
+// Warp specialisation.  Persistent CTAs (one per SM) of 16 warps walk a
+// flattened sequence of steps over their tiles (generation x 64 coded packets
+// x 384 words):
+//   * 12 gatherer warps (152 registers each, setmaxnreg): lane = (word,
+//     16-coefficient chunk), 4 words per lane, 64 accumulator registers;
+//     wait BUILT(s), gather step s from table s % 3, prefetch the source words
+//     of step s+1 straight from global memory, write the tile back when s ends
+//     it (4x4 byte transpose, 4-byte stores), arrive DONE(s);
+//   * 4 producer warps (56 registers): wait DONE(s-2) (table buffer free),
+//     basis rows P[2^b] = C * x^b of step s+1 (packed xtime chain, coefficient
+//     words prefetched a step ahead), named barrier among the producers, then
+//     thread (chunk c16, h) writes rows 32 h .. 32 h + 31 in Gray-code order,
+//     one 16-B XOR per row (P[a] = XOR_{b in a} P[2^b], GF(2)-linearity of the
+//     product); arrive BUILT(s+1).
+// Three table buffers at compile-time shared addresses (the gatherer loop is
+// unrolled three times so the table base is the LDS immediate), mbarrier
+// rings of four objects; producers may run two steps ahead.
+// Build + basis traffic per step: 64 KiB + 4 KiB against 4 x 4 x 384 x 64 B
+// of gathers (17%).
 #pragma once
 #include <cstdint>
 
@@ -51,19 +54,18 @@
 namespace gfr {
 
 constexpr int kPrThreads = 512;
-constexpr int kPrWarps = kPrThreads / 32;
+constexpr int kPrGW = 12;                     // gatherer warps (warps 0..11)
+constexpr int kPrPW = 4;                      // producer warps (warps 12..15, one warpgroup)
+constexpr int kPrGRegs = 152, kPrPRegs = 56;  // setmaxnreg budgets: 12*32*152 + 4*32*56 = 65536
+constexpr int kPrR = 4;                       // words per gatherer lane
+constexpr int kPrTW = kPrR * kPrGW * 8;       // words per tile (384)
 constexpr int kPrKC = 64;                     // coded packets per CTA
 constexpr int kPrS = 4;                       // source packets per step
-constexpr uint32_t kPrBar = 0x0400u;          // mbarriers (6 x 8 B) at the dynamic window base
+constexpr uint32_t kPrBar = 0x0400u;          // mbarriers: BUILT[4], DONE[4] at the dynamic window base
 constexpr uint32_t kPrTab0 = 0x1000u;         // tables u = 0, 1, 2 at kPrTab0 + u * 0x10000
-constexpr uint32_t kPrBasis = 0x31000u;       // basis rows: 3 buffers x 8 x 256 B
+constexpr uint32_t kPrBasis = 0x31000u;       // basis rows: 2 buffers x 8 x 256 B
 constexpr int kPrBasisBytes = 8 * 256;
-constexpr uint32_t kPrSmemEnd = kPrBasis + 3 * kPrBasisBytes;
-
-template <int R> struct PrGeom {
-    static constexpr int WPW = 8;                              // words per warp per round
-    static constexpr int TW = R * kPrWarps * WPW;              // words per tile
-};
+constexpr uint32_t kPrSmemEnd = kPrBasis + 2 * kPrBasisBytes;
 
 struct ProwParams {
     const uint8_t *A;
@@ -144,12 +146,21 @@ __device__ __forceinline__ void mbar_arrive(uint32_t a)
 {
     asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" :: "r"(a) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_n(uint32_t a, uint32_t n)
+{
+    asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0], %1; }" :: "r"(a), "r"(n) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity)
 {
     asm volatile("{ .reg .pred p;\n"
                  "PR_WAIT_%=:\n"
                  "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
                  "@!p bra PR_WAIT_%=;\n}" :: "r"(a), "r"(parity) : "memory");
+}
+
+__device__ __forceinline__ void nbar_sync_n(int id, int n)
+{
+    asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(n) : "memory");
 }
 
 // one work tile: generation g, coded packets k0 .. k0+63, words w0 .. w0+TW-1
@@ -161,15 +172,13 @@ struct PrTile {
 
 template <uint32_t V> struct PrU { static constexpr uint32_t value = V; };
 
-template <int F, int R>
+template <int F>
 __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p)
 {
-    constexpr int TW = PrGeom<R>::TW;
-    // mbarrier rings (2 objects each, by step parity).  Phases: DONE(x), x >= 0,
-    // on object x & 1 is phase x >> 1; BUILT(x), x >= 1, phase (x - 1) >> 1;
-    // BASIS(x), x >= 3, phase (x - 3) >> 1 (table 0 and basis rows of steps 0..2
-    // come from the prologue, ordered by __syncthreads).
-    constexpr uint32_t kDone = kPrBar, kBuilt = kPrBar + 16, kBas = kPrBar + 32;
+    // mbarrier rings, object x & 3 for step x: BUILT(x) (4 producer-warp
+    // arrivals) is phase x >> 2; DONE(x) (12 gatherer-warp arrivals) is phase
+    // (x + 4) >> 2, the virtual steps -4..-1 pre-arrived.
+    constexpr uint32_t kBuilt = kPrBar, kDone = kPrBar + 32;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const size_t ntile_cta = p.ntiles > blockIdx.x ? (p.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
@@ -177,174 +186,197 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
     const uint32_t total = ntj * (uint32_t)p.NS;             // steps of this CTA
 
     auto tile_of = [&](uint32_t j) {                          // j-th tile of this CTA
-        const size_t t = blockIdx.x + (size_t)j * gridDim.x;
+        const size_t t = blockIdx.x + (size_t)(j < ntj ? j : 0u) * gridDim.x;
         PrTile r;
         const int kt = (int)(t % (size_t)p.k_tiles);
         const size_t rest = t / (size_t)p.k_tiles;
-        r.w0 = (uint32_t)(rest % (size_t)p.tiles) * TW;
+        r.w0 = (uint32_t)(rest % (size_t)p.tiles) * kPrTW;
         r.g = rest / (size_t)p.tiles;
         r.k0 = kt * kPrKC;
         return r;
     };
-    // step cursors (tile j, step st of the tile): divisions only at tile changes
-    struct Cur {
-        uint32_t j;
-        int st;
-        PrTile T;
-    };
-    auto cur_next = [&](Cur &c) {
-        if (++c.st == p.NS) {
-            c.st = 0;
-            c.j++;
-            c.T = tile_of(c.j);
-        }
-    };
-
-    // ---- gather-lane geometry: quarter-warp = 2 words x 4 coefficient chunks
-    const int qw = lane >> 3, ql = lane & 7;
-    const int jw = ql >> 2, kc = ql & 3;
-    uint32_t wofs[R];
-#pragma unroll
-    for (int r = 0; r < R; r++) wofs[r] = (uint32_t)(r * kPrWarps * 8 + warp * 8 + qw * 2 + jw);
-
-    // source words of the cursor's step (4 sources x R words; sub-step t reads
-    // source (jw + t) & 3), 0 past N / Mw
-    auto load_a = [&](const Cur &c, uint32_t (&a)[R][kPrS]) {
-        if (c.j >= ntj) return;
-        const uint8_t *Ag = p.A + c.T.g * (size_t)p.N * p.M;
-#pragma unroll
-        for (int t = 0; t < kPrS; t++) {
-            const int i = kPrS * c.st + ((jw + t) & 3);
-            const uint32_t *row = reinterpret_cast<const uint32_t *>(Ag + (size_t)min(i, p.N - 1) * p.M);
-#pragma unroll
-            for (int r = 0; r < R; r++) {
-                const uint32_t wd = c.T.w0 + wofs[r];
-                a[r][t] = (i < p.N && wd < p.Mw) ? __ldg(row + wd) : 0u;
-            }
-        }
-    };
-
-    // basis thread geometry: word wq of 16-B chunk c16 (source c16 >> 2,
-    // coefficients 16 (c16 & 3) + 4 wq .. +3), bit b
-    const int bwq = tid & 3, bc16 = (tid >> 2) & 15, bb = tid >> 6;
-    // raw coefficient word of the cursor's step (masked to F_q at use, so the
-    // load is consumed a step later)
-    auto load_c = [&](const Cur &cc) -> uint32_t {
-        if (cc.j >= ntj) return 0u;
-        const int i = kPrS * cc.st + (bc16 >> 2);
-        if (i >= p.N) return 0u;
-        const uint8_t *crow = p.C + (cc.T.g * (size_t)p.N + (size_t)i) * p.K;
-        const int k = cc.T.k0 + 16 * (bc16 & 3) + 4 * bwq;
-        if (p.cword) return k < p.K ? __ldg(reinterpret_cast<const uint32_t *>(crow + k)) : 0u;
-        uint32_t c = 0;
-#pragma unroll
-        for (int e = 0; e < 4; e++)
-            if (k + e < p.K) c |= (uint32_t)__ldg(crow + k + e) << (8 * e);
-        return c;
-    };
-    auto basis = [&](uint32_t s, uint32_t c, uint32_t buf) {  // buf = s % 3
-        if (s < total)
-            asm volatile("st.shared.u32 [%0], %1;" :: "r"(kPrBasis + buf * kPrBasisBytes + bb * 256 +
-                                                         bc16 * 16 + bwq * 4),
-                         "r"(pr_basis<F>(c & p.qmask4, bb)) : "memory");
-    };
-    // table of step s at shared address tab: thread (chunk c16, hi) -> rows 8 hi + Gray(0..7)
-    auto build = [&](uint32_t s, uint32_t buf) {               // buf = s % 3
-        if (s >= total) return;
-        const int c16 = tid & 15, hi = tid >> 4;
-        const uint32_t bsrc = kPrBasis + buf * kPrBasisBytes + c16 * 16;
-        const uint32_t tab = kPrTab0 + buf * 0x10000u;
-        uint4 v = make_uint4(0u, 0u, 0u, 0u);
-#pragma unroll
-        for (int j = 0; j < 5; j++) {
-            const uint4 b = lds128(bsrc + (3 + j) * 256);
-            const uint32_t m = 0u - ((uint32_t)(hi >> j) & 1u);
-            v.x ^= b.x & m; v.y ^= b.y & m; v.z ^= b.z & m; v.w ^= b.w & m;
-        }
-        const uint4 b0 = lds128(bsrc), b1 = lds128(bsrc + 256), b2 = lds128(bsrc + 512);
-        const uint32_t tb = tab + (uint32_t)hi * 8u * 256u + (uint32_t)c16 * 16u;
-        sts128(tb + 0 * 256, v); xor4(v, b0);
-        sts128(tb + 1 * 256, v); xor4(v, b1);
-        sts128(tb + 3 * 256, v); xor4(v, b0);
-        sts128(tb + 2 * 256, v); xor4(v, b2);
-        sts128(tb + 6 * 256, v); xor4(v, b0);
-        sts128(tb + 7 * 256, v); xor4(v, b1);
-        sts128(tb + 5 * 256, v); xor4(v, b0);
-        sts128(tb + 4 * 256, v);
-    };
 
     if (tid == 0) {
 #pragma unroll
-        for (int b = 0; b < 6; b++) mbar_init(kPrBar + 8 * b, kPrWarps);
+        for (int b = 0; b < 4; b++) {
+            mbar_init(kBuilt + 8 * b, kPrPW);
+            mbar_init(kDone + 8 * b, kPrGW);
+        }
+#pragma unroll
+        for (int b = 0; b < 4; b++) mbar_arrive_n(kDone + 8 * b, kPrGW);   // DONE(-4 .. -1)
     }
-    // ---- prologue: basis rows of steps 0..2, table 0, source words of step 0
-    Cur ca;
-    ca.j = 0; ca.st = 0; ca.T = tile_of(0);
-    Cur cc = ca;
+    __syncthreads();
+
+    if (warp >= kPrGW) {
+        // ======================= producers: basis rows + tables
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" :: "n"(kPrPRegs));
+        const int pt = tid - kPrGW * 32;                       // 0 .. 127
+        // basis geometry: coefficient word (chunk cc16, word cwq), bits b0, b0+2, b0+4, b0+6
+        const int cwq = pt & 3, cc16 = (pt >> 2) & 15, b0 = pt >> 6;
+        // coefficient cursor: &C[g][4 st + (cc16 >> 2)][k0 + 16 (cc16 & 3) + 4 cwq]
+        uint32_t cj = 0;
+        int cst = 0;
+        const uint8_t *cptr = nullptr;
+        bool kok = false;
+        auto setc = [&]() {
+            const PrTile T = tile_of(cj);
+            const int k = T.k0 + 16 * (cc16 & 3) + 4 * cwq;
+            cptr = p.C + (T.g * (size_t)p.N + (size_t)(cc16 >> 2)) * p.K + k;
+            kok = cj < ntj && k < p.K;
+        };
+        auto load_c = [&]() -> uint32_t {                      // raw word of the cursor's step
+            uint32_t c = 0;
+            if (kok && kPrS * cst + (cc16 >> 2) < p.N) {
+                if (p.cword) {
+                    c = __ldg(reinterpret_cast<const uint32_t *>(cptr));
+                } else {
+                    const int k = (int)((size_t)(cptr - p.C) % (size_t)p.K);   // K % 4 != 0: rare
+#pragma unroll
+                    for (int e = 0; e < 4; e++)
+                        if (k + e < p.K) c |= (uint32_t)__ldg(cptr + e) << (8 * e);
+                }
+            }
+            if (++cst == p.NS) {
+                cst = 0;
+                cj++;
+                setc();
+            } else {
+                cptr += (size_t)kPrS * p.K;
+            }
+            return c;
+        };
+        auto basis = [&](uint32_t craw, uint32_t buf) {
+            constexpr int w = F == 256 ? 8 : F == 16 ? 4 : F == 4 ? 2 : 1;
+            uint32_t xt[w];
+            xt[0] = craw & p.qmask4;
+#pragma unroll
+            for (int e = 1; e < w; e++) xt[e] = pr_xtime<F>(xt[e - 1]);
+            const uint32_t dst = kPrBasis + buf * kPrBasisBytes + cc16 * 16 + cwq * 4;
+#pragma unroll
+            for (int v = 0; v < 4; v++) {
+                // bit b = b0 + 2v: slot b / w, power b % w (b0 is warp-uniform)
+                const int be = 2 * v, bo = 2 * v + 1;
+                const uint32_t ve = xt[be % w] << ((be / w) * w), vo = xt[bo % w] << ((bo / w) * w);
+                asm volatile("st.shared.u32 [%0], %1;" :: "r"(dst + (b0 + 2 * v) * 256), "r"(b0 ? vo : ve)
+                             : "memory");
+            }
+        };
+        // table of step x: thread (chunk c16, h) -> rows 32 h + Gray(0..31)
+        const int c16 = pt & 15, h3 = pt >> 4;
+        auto build = [&](uint32_t bbuf, uint32_t tab) {
+            const uint32_t bsrc = kPrBasis + bbuf * kPrBasisBytes + c16 * 16;
+            uint4 v = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+            for (int j = 0; j < 3; j++) {
+                const uint4 b = lds128(bsrc + (5 + j) * 256);
+                const uint32_t m = 0u - ((uint32_t)(h3 >> j) & 1u);
+                v.x ^= b.x & m; v.y ^= b.y & m; v.z ^= b.z & m; v.w ^= b.w & m;
+            }
+            uint4 bv[5];
+#pragma unroll
+            for (int j = 0; j < 5; j++) bv[j] = lds128(bsrc + j * 256);
+            const uint32_t tb = tab + (uint32_t)h3 * 32u * 256u + (uint32_t)c16 * 16u;
+            sts128(tb, v);
+#pragma unroll
+            for (int n = 1; n < 32; n++) {
+                const int flip = (n & 1) ? 0 : (n & 2) ? 1 : (n & 4) ? 2 : (n & 8) ? 3 : 4;   // Gray code: bit flipped at step n
+                xor4(v, bv[flip]);
+                sts128(tb + (uint32_t)(n ^ (n >> 1)) * 256u, v);
+            }
+        };
+
+        setc();
+        basis(load_c(), 0);                                     // step 0
+        uint32_t creg = load_c();                               // step 1
+        nbar_sync_n(1, kPrPW * 32);
+        build(0, kPrTab0);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(kBuilt);                     // BUILT(0)
+#pragma unroll 1
+        for (uint32_t x = 1; x < total; x++) {                  // table of step x
+            mbar_wait(kDone + ((x - 3) & 3u) * 8u, ((x + 1) >> 2) & 1u);   // DONE(x-3): buffer free
+            const uint32_t c = creg;
+            creg = load_c();                                    // step x + 1
+            basis(c, x & 1u);
+            nbar_sync_n(1, kPrPW * 32);
+            build(x & 1u, kPrTab0 + (x % 3u) * 0x10000u);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(kBuilt + (x & 3u) * 8u);
+        }
+        return;
+    }
+
+    // ======================= gatherers
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" :: "n"(kPrGRegs));
+    constexpr int R = kPrR;
+    const int qw = lane >> 3, ql = lane & 7;
+    const int jw = ql >> 2, kc = ql & 3;
+    const uint32_t wbase = (uint32_t)(warp * 8 + qw * 2 + jw);   // word r of the lane: wbase + 96 r
+    constexpr uint32_t kRW = kPrGW * 8;
+
+    // source-word cursor: a = &A[g][4 st][w0 + wbase] (bytes), vmask bit r = word r valid
+    uint32_t aj = 0;
+    int ast = 0;
+    const uint8_t *aptr = nullptr;
+    uint32_t vmask = 0;
+    auto seta = [&]() {
+        const PrTile T = tile_of(aj);
+        aptr = p.A + T.g * (size_t)p.N * p.M + 4 * (size_t)(T.w0 + wbase);
+        vmask = 0;
+#pragma unroll
+        for (int r = 0; r < R; r++)
+            if (aj < ntj && T.w0 + wbase + kRW * r < p.Mw) vmask |= 1u << r;
+    };
     uint32_t areg[R][kPrS];
-    load_a(ca, areg);
-    cur_next(ca);                                             // ca at step 1
-    uint32_t creg;
-    {
-        const uint32_t c0 = load_c(cc); cur_next(cc);
-        const uint32_t c1 = load_c(cc); cur_next(cc);
-        const uint32_t c2 = load_c(cc); cur_next(cc);
-        creg = load_c(cc); cur_next(cc);                      // step 3; cc at step 4
-        basis(0, c0, 0);
-        basis(1, c1, 1);
-        basis(2, c2, 2);
-    }
-    __syncthreads();
-    build(0, 0);
-    __syncthreads();
-    int st_g = 0;                                             // step-in-tile of the gather step
-    uint32_t j_g = 0;
+    auto load_a = [&]() {                                      // the cursor's step, then advance
+#pragma unroll
+        for (int t = 0; t < kPrS; t++) {
+            const int sidx = (jw + t) & 3;
+            const bool iok = kPrS * ast + sidx < p.N;
+            const uint32_t *row = reinterpret_cast<const uint32_t *>(aptr + (size_t)sidx * p.M);
+#pragma unroll
+            for (int r = 0; r < R; r++) areg[r][t] = (iok && (vmask >> r & 1u)) ? __ldg(row + kRW * r) : 0u;
+        }
+        if (++ast == p.NS) {
+            ast = 0;
+            aj++;
+            seta();
+        } else {
+            aptr += (size_t)kPrS * p.M;
+        }
+    };
+    seta();
+    load_a();                                                  // step 0
 
     uint4 acc[R][4];
 #pragma unroll
     for (int r = 0; r < R; r++)
 #pragma unroll
         for (int j = 0; j < 4; j++) acc[r][j] = make_uint4(0u, 0u, 0u, 0u);
+    int st_g = 0;                                              // step-in-tile of the gather step
+    uint32_t j_g = 0;
 
     auto step = [&](uint32_t s, auto U) {
-        constexpr uint32_t u = decltype(U)::value;            // table buffer of step s
-        constexpr uint32_t un = (u + 1) % 3;                  // table buffer of step s + 1
-        const uint32_t par = s & 1u;
-        // ---- build table s + 1
-        if (s >= 2) mbar_wait(kDone + par * 8u, ((s - 2) >> 1) & 1u);          // gathers of s-2 done
-        if (s >= 2) mbar_wait(kBas + (par ^ 1u) * 8u, ((s - 2) >> 1) & 1u);   // basis rows of s+1
-        build(s + 1, un);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(kBuilt + (par ^ 1u) * 8u);
-        // ---- basis rows of step s + 3 (their buffer held step s's, read by build(s))
-        if (s >= 1) mbar_wait(kBuilt + par * 8u, ((s - 1) >> 1) & 1u);
-        basis(s + 3, creg, u);
-        creg = load_c(cc);                                    // step s + 4
-        cur_next(cc);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(kBas + (par ^ 1u) * 8u);
-        // ---- gathers of step s
+        constexpr uint32_t u = decltype(U)::value;             // table buffer of step s
+        mbar_wait(kBuilt + (s & 3u) * 8u, (s >> 2) & 1u);
+        const uint32_t col0 = (uint32_t)(jw * 64 + kc * 16), col1 = (uint32_t)(((jw + 1) & 3) * 64 + kc * 16);
+        const uint32_t col2 = (uint32_t)(((jw + 2) & 3) * 64 + kc * 16), col3 = (uint32_t)(((jw + 3) & 3) * 64 + kc * 16);
 #pragma unroll
-        for (int tp = 0; tp < kPrS; tp += 2) {
-            const uint32_t col0 = (uint32_t)(((jw + tp) & 3) * 64 + kc * 16);
-            const uint32_t col1 = (uint32_t)(((jw + tp + 1) & 3) * 64 + kc * 16);
+        for (int r = 0; r < R; r++) {
 #pragma unroll
-            for (int r = 0; r < R; r++) {
-#pragma unroll
-                for (int j = 0; j < 4; j++) {
-                    const uint4 v0 =
-                        lds128_at<kPrTab0 + u * 0x10000u>(prmt(areg[r][tp], col0, 0x5504u | (j << 4)));
-                    const uint4 v1 =
-                        lds128_at<kPrTab0 + u * 0x10000u>(prmt(areg[r][tp + 1], col1, 0x5504u | (j << 4)));
-                    acc[r][j].x = xor3(acc[r][j].x, v0.x, v1.x);
-                    acc[r][j].y = xor3(acc[r][j].y, v0.y, v1.y);
-                    acc[r][j].z = xor3(acc[r][j].z, v0.z, v1.z);
-                    acc[r][j].w = xor3(acc[r][j].w, v0.w, v1.w);
-                }
+            for (int j = 0; j < 4; j++) {
+                const uint32_t sel = 0x5504u | (j << 4);
+                const uint4 v0 = lds128_at<kPrTab0 + u * 0x10000u>(prmt(areg[r][0], col0, sel));
+                const uint4 v1 = lds128_at<kPrTab0 + u * 0x10000u>(prmt(areg[r][1], col1, sel));
+                const uint4 v2 = lds128_at<kPrTab0 + u * 0x10000u>(prmt(areg[r][2], col2, sel));
+                const uint4 v3 = lds128_at<kPrTab0 + u * 0x10000u>(prmt(areg[r][3], col3, sel));
+                acc[r][j].x = xor3(acc[r][j].x, v0.x, v1.x) ^ (v2.x ^ v3.x);
+                acc[r][j].y = xor3(acc[r][j].y, v0.y, v1.y) ^ (v2.y ^ v3.y);
+                acc[r][j].z = xor3(acc[r][j].z, v0.z, v1.z) ^ (v2.z ^ v3.z);
+                acc[r][j].w = xor3(acc[r][j].w, v0.w, v1.w) ^ (v2.w ^ v3.w);
             }
         }
-        load_a(ca, areg);                                     // step s + 1
-        cur_next(ca);
+        load_a();                                              // step s + 1
         if (++st_g == p.NS) {
             st_g = 0;
             // ---- write back the tile: acc[r][j] word q holds B[k0 + 16 kc + 4q + e][4 wd + j]
@@ -352,7 +384,7 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
             const PrTile T = tile_of(j_g++);
 #pragma unroll
             for (int r = 0; r < R; r++) {
-                const uint32_t wd = T.w0 + wofs[r];
+                const uint32_t wd = T.w0 + wbase + kRW * r;
                 if (wd < p.Mw) {
 #pragma unroll
                     for (int q = 0; q < 4; q++) {
@@ -375,7 +407,7 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
             }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(kDone + par * 8u);
+        if (lane == 0) mbar_arrive(kDone + (s & 3u) * 8u);
     };
 
 #pragma unroll 1

@@ -262,14 +262,14 @@ static int dyn_smem_base(uint32_t *base)
     return GF_OK;
 }
 
-template <int F, int R>
+template <int F>
 static int launch_prow(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M,
                        size_t batch, cudaStream_t st)
 {
     ProwParams p;
     p.A = A; p.C = C; p.B = B; p.M = M; p.Mw = (uint32_t)(M / 4);
     p.N = N; p.K = K; p.NS = (N + kPrS - 1) / kPrS;
-    p.tiles = (int)((p.Mw + PrGeom<R>::TW - 1) / PrGeom<R>::TW);
+    p.tiles = (int)((p.Mw + kPrTW - 1) / kPrTW);
     p.k_tiles = (K + kPrKC - 1) / kPrKC;
     p.qmask4 = (uint32_t)(F - 1) * 0x01010101u;
     p.cword = (K % 4 == 0 && (reinterpret_cast<uintptr_t>(C) & 3u) == 0) ? 1 : 0;
@@ -285,10 +285,10 @@ static int launch_prow(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, in
     if (rc != GF_OK) return rc;
     if (base > kPrBar) return GF_EARG;                        // layout needs the window to start at <= 0x400
     const size_t smem = kPrSmemEnd - base;
-    if (cudaFuncSetAttribute(encode_prow_kernel<F, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(encode_prow_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
         return GF_ECUDA;
-    encode_prow_kernel<F, R><<<(unsigned)grid, kPrThreads, smem, st>>>(p);
+    encode_prow_kernel<F><<<(unsigned)grid, kPrThreads, smem, st>>>(p);
     return launch_status();
 }
 
@@ -348,10 +348,10 @@ static int encode_on_stream(int field, int fi, const uint8_t *A, const uint8_t *
         const int path = encode_path(field, N, K, M, A, B);
         if (path >= 6) {
             switch (field) {
-            case 256: return launch_prow<256, 3>(A, C, B, N, K, M, batch, st);
-            case 16: return launch_prow<16, 3>(A, C, B, N, K, M, batch, st);
-            case 4: return launch_prow<4, 3>(A, C, B, N, K, M, batch, st);
-            case 2: return launch_prow<2, 3>(A, C, B, N, K, M, batch, st);
+            case 256: return launch_prow<256>(A, C, B, N, K, M, batch, st);
+            case 16: return launch_prow<16>(A, C, B, N, K, M, batch, st);
+            case 4: return launch_prow<4>(A, C, B, N, K, M, batch, st);
+            case 2: return launch_prow<2>(A, C, B, N, K, M, batch, st);
             default: return GF_EFIELD;
             }
         }
