@@ -328,12 +328,16 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
             if (aj < ntj && T.w0 + wbase + kRW * r < p.Mw) vmask |= 1u << r;
     };
     uint32_t areg[R][kPrS];
+    // byte offset of sub-step t's source row within the step: ((jw + t) & 3) * M
+    size_t soff[kPrS];
+#pragma unroll
+    for (int t = 0; t < kPrS; t++) soff[t] = (size_t)((jw + t) & 3) * p.M;
     auto load_a = [&]() {                                      // the cursor's step, then advance
+        const int nsrc = p.N - kPrS * ast;                     // sources of the step that exist
 #pragma unroll
         for (int t = 0; t < kPrS; t++) {
-            const int sidx = (jw + t) & 3;
-            const bool iok = kPrS * ast + sidx < p.N;
-            const uint32_t *row = reinterpret_cast<const uint32_t *>(aptr + (size_t)sidx * p.M);
+            const bool iok = ((jw + t) & 3) < nsrc;
+            const uint32_t *row = reinterpret_cast<const uint32_t *>(aptr + soff[t]);
 #pragma unroll
             for (int r = 0; r < R; r++) areg[r][t] = (iok && (vmask >> r & 1u)) ? __ldg(row + kRW * r) : 0u;
         }
