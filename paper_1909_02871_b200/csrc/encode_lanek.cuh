@@ -25,8 +25,9 @@
 //     distinct banks: one wavefront); WT words per lane accumulate in
 //     registers;
 //   * Q is triple-buffered between builders and gatherers (named barriers
-//     FULL / EMPTY); builders also stream the source tile HBM -> smem with a
-//     cp.async ring several steps deep.
+//     FULL / EMPTY); builders load the source words of a step straight into
+//     registers three steps ahead (no shared-memory staging: the smem pipe is
+//     the binding resource, so staging would cost ~11% of its wavefronts).
 // Per (step, k, word): 1 LDS + 1 LOP3 (GF(256): 2 LDS + 1 LOP3); the table
 // build (15 or 30 words per source word) is shared by the CTA's 32*KG lanes.
 //
@@ -68,6 +69,8 @@ struct LanekParams {
     int qmask;
     int tiles;         // word tiles per packet
     int k_tiles;       // ceil(K / (32 KG))
+    int direct;        // epilogue: each lane stores its own run of its coded packet (16-B stores)
+    int aligned16;     // M % 16 == 0 and B 16-byte aligned
 };
 
 template <int F> struct LkField;
@@ -150,11 +153,9 @@ __global__ void __launch_bounds__(LkGeom<KG>::THREADS, LkGeom<KG>::MINB) encode_
     constexpr int GW = KG * G::WG;                             // gatherer warps
     constexpr int NT = G::THREADS;
     constexpr int kQWords = L::kRows * QS;
-    constexpr int kRingRows = SG * kLkSteps;
     extern __shared__ __align__(16) uint32_t smem[];
     uint32_t *Q = smem;                                        // [NQ][rows][QS]
-    uint32_t *ring = Q + kLkNQ * kQWords;                      // [ring rows][TW]
-    uint8_t *ccache = reinterpret_cast<uint8_t *>(ring + kRingRows * TW);   // [steps][KTL]
+    uint8_t *ccache = reinterpret_cast<uint8_t *>(Q + kLkNQ * kQWords);    // [steps][KTL]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t bid = blockIdx.x;
@@ -193,54 +194,47 @@ __global__ void __launch_bounds__(LkGeom<KG>::THREADS, LkGeom<KG>::MINB) encode_
     constexpr int BAR_FULL = 1, BAR_EMPTY = 1 + kLkNQ, BAR_EPI = 1 + 2 * kLkNQ;   // named barrier ids
 
     if (warp >= GW) {
-        // ---------------- builders: stream the step's sources into the ring, write Q[s & 1]
+        // ---------------- builders: source words straight into registers three
+        // steps ahead (no shared-memory staging), write Q[s % NQ]
         const int bt = threadIdx.x - 32 * GW;                  // 0 .. 127
-        const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
-        auto issue = [&](int s) {
-            if (s < NS) {
+        constexpr int D = kLkNQ;                               // prefetch distance (= NQ: one unrolled round)
+        uint32_t ar[D][G::BWORDS][SG];
+        auto load = [&](int s, uint32_t (&a)[G::BWORDS][SG]) {
 #pragma unroll
-                for (int j = 0; j < SG; j++) {
-                    const int i = s * SG + j;
-                    const uint32_t *row = reinterpret_cast<const uint32_t *>(Ag + (size_t)min(i, p.N - 1) * p.M);
-                    const uint32_t slot = (uint32_t)((s % kLkSteps) * SG + j) * TW;
+            for (int j = 0; j < SG; j++) {
+                const int i = s * SG + j;
+                const uint32_t *row = reinterpret_cast<const uint32_t *>(Ag + (size_t)min(i, p.N - 1) * p.M);
 #pragma unroll
-                    for (int u = 0; u < G::BWORDS; u++) {
-                        const uint32_t tw = (uint32_t)bt + 128u * u;
-                        if (tw < (uint32_t)TW) {
-                            const uint32_t wd = w0 + tw;
-                            const bool v = i < p.N && wd < p.Mw;
-                            cp_async4(ring_s + (slot + tw) * 4u, v ? row + wd : row, v);
-                        }
-                    }
+                for (int u = 0; u < G::BWORDS; u++) {
+                    const uint32_t tw = (uint32_t)bt + 128u * u;
+                    const uint32_t wd = w0 + tw;
+                    a[u][j] = (s < NS && i < p.N && tw < (uint32_t)TW && wd < p.Mw) ? __ldg(row + wd) : 0u;
                 }
             }
-            asm volatile("cp.async.commit_group;" ::: "memory");
         };
-#pragma unroll 1
-        for (int s = 0; s < kLkSteps - 1; s++) issue(s);
-#pragma unroll 1
-        for (int s = 0; s < NS; s++) {
-            issue(s + kLkSteps - 1);
-            asm volatile("cp.async.wait_group %0;" :: "n"(kLkSteps - 1) : "memory");
-            const int b = s % kLkNQ;
+        auto bstep = [&](int s, int b, uint32_t (&a)[G::BWORDS][SG]) {
+            if (s >= NS) return;
             if (s >= kLkNQ) nbar_sync(BAR_EMPTY + b, NT);       // gatherers done with step s-NQ
             uint32_t *q = Q + b * kQWords;
-            const uint32_t *slot = ring + (s % kLkSteps) * SG * TW;
 #pragma unroll
             for (int u = 0; u < G::BWORDS; u++) {
                 const int tw = bt + 128 * u;
-                if (tw < TW) {
-                    uint32_t a[SG];
-#pragma unroll
-                    for (int j = 0; j < SG; j++) a[j] = slot[j * TW + tw];
-                    build_word<F, QS>(q + tw, a);
-                }
+                if (tw < TW) build_word<F, QS>(q + tw, a[u]);
             }
             nbar_arrive(BAR_FULL + b, NT);
+            load(s + D, a);
+        };
+#pragma unroll
+        for (int d = 0; d < D; d++) load(d, ar[d]);
+#pragma unroll 1
+        for (int s = 0; s < NS; s += D) {
+            bstep(s, 0, ar[0]);
+            bstep(s + 1, 1, ar[1]);
+            bstep(s + 2, 2, ar[2]);
         }
+        static_assert(D == 3, "builder loop unrolled for three Q buffers");
         // consume the gatherers' last NQ EMPTY signals
         for (int s = max(NS, kLkNQ); s < NS + kLkNQ; s++) nbar_sync(BAR_EMPTY + s % kLkNQ, NT);
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
         return;
     }
 
@@ -271,6 +265,26 @@ __global__ void __launch_bounds__(LkGeom<KG>::THREADS, LkGeom<KG>::MINB) encode_
         nbar_arrive(BAR_EMPTY + b, NT);
     }
 
+    if (p.direct) {
+        // ---- epilogue without shared memory: lane kl holds words wb .. wb+WT-1 of
+        // coded packet k0 + kl; WT/4 16-byte stores per lane (32 rows per warp
+        // instruction, every 128-B line completed by the same lane's stores)
+        const int k = k0 + kl;
+        if (k < p.K) {
+            const uint32_t wb = w0 + (uint32_t)(wg * WT);
+            uint32_t *row = reinterpret_cast<uint32_t *>(p.B + (g * (size_t)p.K + (size_t)k) * p.M) + wb;
+            if (p.aligned16 && wb + WT <= p.Mw) {
+#pragma unroll
+                for (int v = 0; v < WT / 4; v++)
+                    reinterpret_cast<uint4 *>(row)[v] = make_uint4(acc[4 * v], acc[4 * v + 1], acc[4 * v + 2], acc[4 * v + 3]);
+            } else {
+#pragma unroll
+                for (int w = 0; w < WT; w++)
+                    if (wb + w < p.Mw) row[w] = acc[w];
+            }
+        }
+        return;
+    }
     // ---- epilogue: transpose through shared memory so that each warp writes
     // contiguous runs of one coded packet (the Q buffers are free once every
     // gatherer passed its last step: named barrier over the gatherers only)
@@ -305,7 +319,7 @@ template <int F, int KG>
 __host__ __device__ constexpr size_t lk_smem_bytes(int N)
 {
     using G = LkGeom<KG>;
-    return (size_t)kLkNQ * LkField<F>::kRows * G::QS * 4 + (size_t)LkField<F>::kSG * kLkSteps * G::TW * 4 +
+    return (size_t)kLkNQ * LkField<F>::kRows * G::QS * 4 +
            (size_t)32 * KG * ((N + LkField<F>::kSG - 1) / LkField<F>::kSG);
 }
 

@@ -195,11 +195,14 @@ static int launch_lanek(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, i
                         size_t batch, cudaStream_t st)
 {
     using G = LkGeom<KG>;
-    LanekParams p;
+    LanekParams p{};
     p.A = A; p.C = C; p.B = B; p.M = M; p.Mw = (uint32_t)(M / 4); p.batch = batch;
     p.N = N; p.K = K; p.qmask = F - 1;
     p.tiles = (int)((p.Mw + G::TW - 1) / G::TW);
     p.k_tiles = (K + 32 * KG - 1) / (32 * KG);
+    static const int direct = env_int("GFRLNC_LANEK_DIRECT", 0);   // experiment knob
+    p.direct = direct;
+    p.aligned16 = (M % 16 == 0 && (reinterpret_cast<uintptr_t>(B) & 15u) == 0) ? 1 : 0;
     const size_t grid = batch * (size_t)p.tiles * (size_t)p.k_tiles;
     if (grid > 0x7FFFFFFFu) return GF_EARG;
     const size_t smem = lk_smem_bytes<F, KG>(N);
@@ -216,7 +219,7 @@ static int launch_fused(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, i
                         size_t batch, cudaStream_t st, const uint32_t *tabs)
 {
     using G = FuGeom<KG, WGL, CWS>;
-    LanekParams p;
+    LanekParams p{};
     p.A = A; p.C = C; p.B = B; p.M = M; p.Mw = (uint32_t)(M / 4); p.batch = batch;
     p.N = N; p.K = K; p.qmask = F - 1;
     p.tiles = (int)((p.Mw + G::TW - 1) / G::TW);
