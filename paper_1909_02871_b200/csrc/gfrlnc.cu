@@ -22,7 +22,7 @@
 namespace gfr {
 
 constexpr int kMaxDevices = 64;
-constexpr int kVersion = 132;   // 0.1.32: + product-row encode kernel
+constexpr int kVersion = 133;   // 0.1.33: warp-specialised product-row kernel, lane-k without staging ring
 
 __device__ uint32_t g_dev_tabs[4][256 * kTableWords];
 __device__ uint8_t g_dev_inv[4][256];
