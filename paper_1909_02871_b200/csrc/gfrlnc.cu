@@ -14,6 +14,7 @@
 #include "encode_lanek.cuh"
 #include "encode_fused.cuh"
 #include "encode_prow.cuh"
+#include "encode_lanek2.cuh"
 #include "decode_kernels.cuh"
 #include "region_kernels.cuh"
 #include "rng_kernels.cuh"
@@ -296,6 +297,27 @@ static int launch_prow(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, in
 }
 
 template <int F>
+static int launch_lanek2(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M, size_t batch,
+                         cudaStream_t st)
+{
+    Lk2Params p;
+    p.A = A; p.C = C; p.B = B; p.M = M; p.Mw = (uint32_t)(M / 4);
+    p.N = N; p.K = K; p.NS = (N + LkField<F>::kSG - 1) / LkField<F>::kSG;
+    p.tiles = (int)((p.Mw + kL2TW - 1) / kL2TW);
+    p.ntiles = batch * (size_t)p.tiles;
+    int dev;
+    if (current_device(&dev) != GF_OK) return GF_ECUDA;
+    const size_t sms = (size_t)(g_sm_count[dev] > 0 ? g_sm_count[dev] : 148);
+    const size_t grid = p.ntiles < sms ? p.ntiles : sms;      // persistent: one CTA per SM
+    if ((p.ntiles + grid - 1) / grid * (size_t)p.NS > 0x7FFFFFF0u) return GF_EARG;
+    if (cudaFuncSetAttribute(encode_lanek2_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kL2Smem) != cudaSuccess)
+        return GF_ECUDA;
+    encode_lanek2_kernel<F><<<(unsigned)grid, kL2Threads, kL2Smem, st>>>(p);
+    return launch_status();
+}
+
+template <int F>
 static int launch_lanek_kg(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M,
                            size_t batch, cudaStream_t st)
 {
@@ -322,15 +344,22 @@ static int encode_path_override()
         if (!strcmp(e, "lanek")) return 2;
         if (!strcmp(e, "fused")) return 3;
         if (!strcmp(e, "prow")) return 4;
+        if (!strcmp(e, "lanek2")) return 5;
         return 0;
     }();
     return v;
 }
 
 // 0 column (words), 1 column (bytes), 2 lane-k KG=1, 3 lane-k KG=2,
-// 4 fused KG=1, 5 fused KG=2, 6 product-row.  The fused kernel (lane-k + column warps on one
+// 4 fused KG=1, 5 fused KG=2, 6 product-row, 7 persistent lane-k (GF(2)/GF(4), K <= 32).  The fused kernel (lane-k + column warps on one
 // tile) is correct but measured slower than lane-k alone (per-step barrier
 // coupling of the two roles): opt-in via GFRLNC_ENCODE_PATH=fused.
+static bool lanek2_default()
+{
+    static const int v = env_int("GFRLNC_LANEK2", 0);          // experiment: persistent lane-k by default
+    return v != 0;
+}
+
 static int encode_path(int field, int N, int K, size_t M, const void *A, const void *B)
 {
     const bool aligned = M % 4 == 0 && (reinterpret_cast<uintptr_t>(A) & 3u) == 0 &&
@@ -341,6 +370,7 @@ static int encode_path(int field, int N, int K, size_t M, const void *A, const v
     const int kg2 = K > 32 ? 1 : 0;      // (K > 64 uses 128 coded packets per CTA)
     if (ov == 3) return 4 + kg2;
     if ((ov == 4 || (ov == 0 && field >= 16 && K > 32))) return 6;
+    if (field <= 4 && K <= 32 && (ov == 5 || (ov == 0 && lanek2_default()))) return 7;
     return 2 + kg2;
 }
 
@@ -349,6 +379,10 @@ static int encode_on_stream(int field, int fi, const uint8_t *A, const uint8_t *
 {
     {
         const int path = encode_path(field, N, K, M, A, B);
+        if (path == 7) {
+            return field == 2 ? launch_lanek2<2>(A, C, B, N, K, M, batch, st)
+                              : launch_lanek2<4>(A, C, B, N, K, M, batch, st);
+        }
         if (path >= 6) {
             switch (field) {
             case 256: return launch_prow<256>(A, C, B, N, K, M, batch, st);
@@ -479,7 +513,7 @@ const char *gf_strerror(int status)
 
 int gf_set_encode_path(int path)
 {
-    if (path < 0 || path > 4) return GF_EARG;
+    if (path < 0 || path > 5) return GF_EARG;
     tls_path = path;
     return GF_OK;
 }

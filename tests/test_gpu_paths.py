@@ -16,21 +16,25 @@ sys.path.insert(0, %r)
 import oracle, seeded_inputs as si
 from paper_1909_02871_b200 import gf
 want = sys.argv[1]
-for q in (2, 4, 16, 256):
+if want == "lanek2":       # persistent lane-k: GF(2)/GF(4), K <= 32
+    cases = [(q, s) for q in (2, 4) for s in ((17, 32, 1500, 3), (32, 32, 4100, 2), (5, 24, 400, 3),
+                                              (7, 9, 1540, 2), (33, 32, 2052, 2), (32, 32, 65536, 2), (4, 1, 2048, 300))]
+else:
+    cases = [(q, s) for q in (2, 4, 16, 256) for s in ((17, 33, 1500, 3), (64, 64, 1500, 2), (32, 32, 4100, 2),
+                                                       (5, 24, 400, 3), (33, 96, 3000, 2), (7, 65, 1540, 2))]
+for q, (N, K, M, batch) in cases:
     gf.init(q)
-    for (N, K, M, batch) in ((17, 33, 1500, 3), (64, 64, 1500, 2), (32, 32, 4100, 2), (5, 24, 400, 3),
-                             (33, 96, 3000, 2), (7, 65, 1540, 2)):
-        A = si.random_bytes(7 + N, 1, 0, batch * N * M).reshape(batch, N, M)
-        C = si.uniform_coeffs(q, 8 + K, 2, 0, batch * N * K).reshape(batch, N, K)
-        path = gf.encode_path(q, N, K, M)
-        assert path.startswith(want), (path, want)
-        got = gf.encode_batch(q, torch.from_numpy(A).cuda(), torch.from_numpy(C).cuda()).cpu().numpy()
-        assert np.array_equal(got, oracle.encode_batch(q, A, C)), (q, N, K, M, path)
+    A = si.random_bytes(7 + N, 1, 0, batch * N * M).reshape(batch, N, M)
+    C = si.uniform_coeffs(q, 8 + K, 2, 0, batch * N * K).reshape(batch, N, K)
+    path = gf.encode_path(q, N, K, M)
+    assert path.startswith(want), (path, want)
+    got = gf.encode_batch(q, torch.from_numpy(A).cuda(), torch.from_numpy(C).cuda()).cpu().numpy()
+    assert np.array_equal(got, oracle.encode_batch(q, A, C)), (q, N, K, M, path)
 print("ok", want)
 ''' % ROOT
 
 
-@pytest.mark.parametrize("path", ["column", "lanek", "fused", "prow"])
+@pytest.mark.parametrize("path", ["column", "lanek", "fused", "prow", "lanek2"])
 def test_forced_encode_path(path):
     import torch
     if not torch.cuda.is_available():
