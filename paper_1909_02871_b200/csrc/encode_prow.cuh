@@ -150,6 +150,20 @@ __device__ __forceinline__ void mbar_arrive_n(uint32_t a, uint32_t n)
 {
     asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0], %1; }" :: "r"(a), "r"(n) : "memory");
 }
+__device__ __forceinline__ bool mbar_test(uint32_t a, uint32_t parity)
+{
+    uint32_t ok;
+    asm volatile("{ .reg .pred p;\n"
+                 "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                 "selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+    return ok != 0;
+}
+// a waiter that is known to run ahead (the producers): poll rarely, every
+// failed poll is a shared-memory access on the pipe the gatherers are bound by
+__device__ __forceinline__ void mbar_wait_sleepy(uint32_t a, uint32_t parity)
+{
+    while (!mbar_test(a, parity)) __nanosleep(256);
+}
 __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity)
 {
     asm volatile("{ .reg .pred p;\n"
@@ -294,7 +308,7 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
         if (lane == 0) mbar_arrive(kBuilt);                     // BUILT(0)
 #pragma unroll 1
         for (uint32_t x = 1; x < total; x++) {                  // table of step x
-            mbar_wait(kDone + ((x - 3) & 3u) * 8u, ((x + 1) >> 2) & 1u);   // DONE(x-3): buffer free
+            mbar_wait_sleepy(kDone + ((x - 3) & 3u) * 8u, ((x + 1) >> 2) & 1u);   // DONE(x-3): buffer free
             const uint32_t c = creg;
             creg = load_c();                                    // step x + 1
             basis(c, x & 1u);
