@@ -15,6 +15,7 @@
 #include "encode_fused.cuh"
 #include "encode_prow.cuh"
 #include "encode_lanek2.cuh"
+#include "encode_stream.cuh"
 #include "decode_kernels.cuh"
 #include "region_kernels.cuh"
 #include "rng_kernels.cuh"
@@ -296,6 +297,44 @@ static int launch_prow(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, in
     return launch_status();
 }
 
+template <int F, int KT>
+static int launch_stream_t(const StreamParams &p, cudaStream_t st)
+{
+    int dev;
+    if (current_device(&dev) != GF_OK) return GF_ECUDA;
+    const size_t sms = (size_t)(g_sm_count[dev] > 0 ? g_sm_count[dev] : 148);
+    size_t grid = (p.total + kStThreads - 1) / kStThreads;
+    if (grid > sms * 8) grid = sms * 8;                       // grid-stride: 8 CTAs of 256 per SM
+    encode_stream_kernel<F, KT><<<(unsigned)grid, kStThreads, 0, st>>>(p);
+    return launch_status();
+}
+
+template <int F>
+static int launch_stream_f(const StreamParams &p, cudaStream_t st)
+{
+    if (p.K == 1) return launch_stream_t<F, 1>(p, st);
+    if (p.K == 2) return launch_stream_t<F, 2>(p, st);
+    return launch_stream_t<F, 4>(p, st);
+}
+
+static int launch_stream(int field, int fi, const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K,
+                         size_t M, size_t batch, cudaStream_t st)
+{
+    StreamParams p;
+    void *tabs = nullptr;
+    if (cudaGetSymbolAddress(&tabs, g_dev_tabs) != cudaSuccess) return GF_ECUDA;
+    p.tabs = reinterpret_cast<const uint32_t *>(tabs) + (size_t)fi * 256 * kTableWords;
+    p.A = A; p.C = C; p.B = B; p.M16 = M / 16; p.total = batch * p.M16; p.N = N; p.K = K;
+    p.qmask = (uint32_t)field - 1u;
+    switch (field) {
+    case 2: return launch_stream_f<2>(p, st);
+    case 4: return launch_stream_f<4>(p, st);
+    case 16: return launch_stream_f<16>(p, st);
+    case 256: return launch_stream_f<256>(p, st);
+    default: return GF_EFIELD;
+    }
+}
+
 template <int F>
 static int launch_lanek2(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M, size_t batch,
                          cudaStream_t st)
@@ -345,13 +384,15 @@ static int encode_path_override()
         if (!strcmp(e, "fused")) return 3;
         if (!strcmp(e, "prow")) return 4;
         if (!strcmp(e, "lanek2")) return 5;
+        if (!strcmp(e, "stream")) return 6;
         return 0;
     }();
     return v;
 }
 
 // 0 column (words), 1 column (bytes), 2 lane-k KG=1, 3 lane-k KG=2,
-// 4 fused KG=1, 5 fused KG=2, 6 product-row, 7 persistent lane-k (GF(2)/GF(4), K <= 32).  The fused kernel (lane-k + column warps on one
+// 4 fused KG=1, 5 fused KG=2, 6 product-row, 7 persistent lane-k (GF(2)/GF(4), K <= 32),
+// 8 streaming (K <= 4, 16-byte aligned packets).  The fused kernel (lane-k + column warps on one
 // tile) is correct but measured slower than lane-k alone (per-step barrier
 // coupling of the two roles): opt-in via GFRLNC_ENCODE_PATH=fused.
 static bool lanek2_default()
@@ -366,6 +407,9 @@ static int encode_path(int field, int N, int K, size_t M, const void *A, const v
                          (reinterpret_cast<uintptr_t>(B) & 3u) == 0 && M / 4 < 0xFFFFFFFFull;
     const int ov = encode_path_override();
     if (!aligned) return 1;
+    const bool aligned16 = M % 16 == 0 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0 &&
+                           (reinterpret_cast<uintptr_t>(B) & 15u) == 0;
+    if (aligned16 && K <= 4 && (ov == 6 || ov == 0)) return 8;
     if (ov == 1 || (ov == 0 && K < 24)) return 0;
     const int kg2 = K > 32 ? 1 : 0;      // (K > 64 uses 128 coded packets per CTA)
     if (ov == 3) return 4 + kg2;
@@ -379,6 +423,7 @@ static int encode_on_stream(int field, int fi, const uint8_t *A, const uint8_t *
 {
     {
         const int path = encode_path(field, N, K, M, A, B);
+        if (path == 8) return launch_stream(field, fi, A, C, B, N, K, M, batch, st);
         if (path == 7) {
             return field == 2 ? launch_lanek2<2>(A, C, B, N, K, M, batch, st)
                               : launch_lanek2<4>(A, C, B, N, K, M, batch, st);
@@ -513,7 +558,7 @@ const char *gf_strerror(int status)
 
 int gf_set_encode_path(int path)
 {
-    if (path < 0 || path > 5) return GF_EARG;
+    if (path < 0 || path > 6) return GF_EARG;
     tls_path = path;
     return GF_OK;
 }

@@ -19,6 +19,9 @@ want = sys.argv[1]
 if want == "lanek2":       # persistent lane-k: GF(2)/GF(4), K <= 32
     cases = [(q, s) for q in (2, 4) for s in ((17, 32, 1500, 3), (32, 32, 4100, 2), (5, 24, 400, 3),
                                               (7, 9, 1540, 2), (33, 32, 2052, 2), (32, 32, 65536, 2), (4, 1, 2048, 300))]
+elif want == "stream":    # few coded packets, 16-byte aligned packets (the paper's N = 16, K = 1)
+    cases = [(q, s) for q in (2, 4, 16, 256) for s in ((16, 1, 1024, 50), (16, 1, 128, 300), (5, 2, 4096, 3),
+                                                       (17, 3, 2064, 4), (64, 4, 16, 100), (1, 1, 16, 10))]
 else:
     cases = [(q, s) for q in (2, 4, 16, 256) for s in ((17, 33, 1500, 3), (64, 64, 1500, 2), (32, 32, 4100, 2),
                                                        (5, 24, 400, 3), (33, 96, 3000, 2), (7, 65, 1540, 2))]
@@ -34,7 +37,7 @@ print("ok", want)
 ''' % ROOT
 
 
-@pytest.mark.parametrize("path", ["column", "lanek", "fused", "prow", "lanek2"])
+@pytest.mark.parametrize("path", ["column", "lanek", "fused", "prow", "lanek2", "stream"])
 def test_forced_encode_path(path):
     import torch
     if not torch.cuda.is_available():
