@@ -17,8 +17,9 @@
 //   GF(4):   the paper's imul (Alg. 2): 2 IMAD + 1 LOP3
 //            (a & 0x55..)*c ^ ((a>>1) & 0x55..)*(x c)
 //   GF(16):  imul on the four nibble bit planes: 4 IMAD + 2 LOP3
-//   GF(256): bits 0-5 through two byte-permute split tables (Alg. 1's
-//            shuffle), bits 6-7 through two imul planes,
+//   GF(256): three byte-permute split tables over bit groups {0-2}, {3-5},
+//            {6-7} (Alg. 1's shuffle): 3 PRMT + 3 AND +
+//            2 LOP3 on the ALU pipe, selector packing on the FMA pipe;
 //            results in PRMT byte order, un-permuted once per output word.
 // Grid-stride over (generation, chunk); packets of 512 B or more give
 // warp-uniform coefficients (broadcast table loads).
@@ -90,21 +91,16 @@ template <> struct StreamOp<16> {
 };
 template <> struct StreamOp<256> {
     static constexpr bool kPermuted = true;
-    struct E { uint32_t t0lo, t0hi, t1lo, t1hi, p6, p7; };
+    struct E { PrmtTab T; };
     __device__ __forceinline__ static E entry(const uint32_t *t)
     {
         const uint4 v = __ldg(reinterpret_cast<const uint4 *>(t));
-        const uint2 w = __ldg(reinterpret_cast<const uint2 *>(t + 14));
-        return E{v.x, v.y, v.z, v.w, w.x, w.y};
+        E e;
+        e.T.t0lo = v.x; e.T.t0hi = v.y; e.T.t1lo = v.z; e.T.t1hi = v.w; e.T.t2 = __ldg(t + 4);
+        return e;
     }
-    __device__ __forceinline__ static uint32_t mul(uint32_t x, const E &e)
-    {
-        const uint32_t xp = prmt(x, x, 0x3120u);                // PRMT byte order [b0, b2, b1, b3]
-        const uint32_t t0 = x & 0x07070707u, t1 = mul_hi(x, 1u << 29) & 0x07070707u;
-        const uint32_t s0 = mad_hi(t0, 1u << 20, t0), s1 = mad_hi(t1, 1u << 20, t1);
-        const uint32_t b6 = mul_hi(xp, 1u << 26) & 0x01010101u, b7 = mul_hi(xp, 1u << 25) & 0x01010101u;
-        return prmt(e.t0lo, e.t0hi, s0) ^ prmt(e.t1lo, e.t1hi, s1) ^ (b6 * e.p6) ^ (b7 * e.p7);
-    }
+    // three split-table PRMTs (bit groups {0-2}, {3-5}, {6-7}): 8 ALU + 5 FMA-pipe ops
+    __device__ __forceinline__ static uint32_t mul(uint32_t x, const E &e) { return lookup_perm(e.T, make_sel(x)); }
 };
 
 template <int F, int KT>
