@@ -8,8 +8,9 @@
 // once and multiplied once, so it is bound by HBM (17 bytes of traffic per 16
 // source bytes for N = 16), not by arithmetic -- provided the multiply stays
 // under ~12 ALU operations per 32-bit word at HBM speed.  One thread owns one
-// 16-byte column chunk of one generation: it loads the chunks of eight source
-// packets at a time (16-byte non-allocating loads, all in flight together),
+// 16-byte column chunk of one generation: it loads the chunks of eight (GF(2),
+// GF(4)) or four source packets at a time (16-byte non-allocating loads, all
+// in flight together),
 // multiplies each by its coefficient and XORs into K accumulators.  Per-field
 // word arithmetic (coefficient tables from gf_init's table of tables,
 // L1-resident):
@@ -32,7 +33,6 @@
 namespace gfr {
 
 constexpr int kStThreads = 256;
-constexpr int kStBatch = 8;          // source chunks loaded together
 
 struct StreamParams {
     const uint8_t *A;
@@ -107,6 +107,7 @@ template <int F, int KT>
 __global__ void __launch_bounds__(kStThreads) encode_stream_kernel(StreamParams p)
 {
     using Op = StreamOp<F>;
+    constexpr int kStBatch = F <= 4 ? 8 : 4;                  // source chunks loaded together (measured)
     const size_t stride = (size_t)gridDim.x * kStThreads;
     for (size_t t = (size_t)blockIdx.x * kStThreads + threadIdx.x; t < p.total; t += stride) {
         const size_t g = t / p.M16, ch = t - g * p.M16;
