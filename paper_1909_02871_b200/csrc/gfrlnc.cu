@@ -73,6 +73,25 @@ static int check_ready(int field, int *fi, int *dev)
     return GF_OK;
 }
 
+// device addresses of the table symbols, cached per device (cudaGetSymbolAddress
+// costs microseconds, which matters for single-generation calls such as C1)
+static void *g_sym_cache[3][kMaxDevices];
+static int symbol_address(int which, void **out)
+{
+    int dev;
+    if (current_device(&dev) != GF_OK) return GF_ECUDA;
+    void *v = __atomic_load_n(&g_sym_cache[which][dev], __ATOMIC_ACQUIRE);
+    if (!v) {
+        const cudaError_t e = which == 0 ? cudaGetSymbolAddress(&v, g_dev_tabs)
+                            : which == 1 ? cudaGetSymbolAddress(&v, g_dev_inv)
+                                         : cudaGetSymbolAddress(&v, g_dev_mul);
+        if (e != cudaSuccess) return GF_ECUDA;
+        __atomic_store_n(&g_sym_cache[which][dev], v, __ATOMIC_RELEASE);
+    }
+    *out = v;
+    return GF_OK;
+}
+
 static bool overlaps(const void *a, size_t na, const void *b, size_t nb)
 {
     const uintptr_t x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
@@ -322,7 +341,7 @@ static int launch_stream(int field, int fi, const uint8_t *A, const uint8_t *C, 
 {
     StreamParams p;
     void *tabs = nullptr;
-    if (cudaGetSymbolAddress(&tabs, g_dev_tabs) != cudaSuccess) return GF_ECUDA;
+    if (symbol_address(0, &tabs) != GF_OK) return GF_ECUDA;
     p.tabs = reinterpret_cast<const uint32_t *>(tabs) + (size_t)fi * 256 * kTableWords;
     p.A = A; p.C = C; p.B = B; p.M16 = M / 16; p.total = batch * p.M16; p.N = N; p.K = K;
     p.qmask = (uint32_t)field - 1u;
@@ -439,7 +458,7 @@ static int encode_on_stream(int field, int fi, const uint8_t *A, const uint8_t *
         }
         if (path >= 4) {
             void *tabs = nullptr;
-            if (cudaGetSymbolAddress(&tabs, g_dev_tabs) != cudaSuccess) return GF_ECUDA;
+            if (symbol_address(0, &tabs) != GF_OK) return GF_ECUDA;
             const uint32_t *t = reinterpret_cast<const uint32_t *>(tabs) + (size_t)fi * 256 * kTableWords;
             const bool kg2 = path == 5;
             switch (field) {
@@ -468,7 +487,7 @@ static int encode_on_stream(int field, int fi, const uint8_t *A, const uint8_t *
     std::memset(&p, 0, sizeof(p));
     p.A = A; p.C = C; p.B = B;
     void *tabs = nullptr;
-    if (cudaGetSymbolAddress(&tabs, g_dev_tabs) != cudaSuccess) return GF_ECUDA;
+    if (symbol_address(0, &tabs) != GF_OK) return GF_ECUDA;
     p.tabs = reinterpret_cast<const uint32_t *>(tabs) + (size_t)fi * 256 * kTableWords;
     p.M = M; p.batch = batch; p.N = N; p.K = K; p.qmask = field - 1;
     const bool bytewise = (M % 4) != 0 || (reinterpret_cast<uintptr_t>(A) & 3u) ||
@@ -720,8 +739,7 @@ int gf_invert_batch(int field, const uint8_t *C, uint8_t *D, int *rank, int N, s
     if (__builtin_mul_overflow((size_t)N * (size_t)N, batch, &cb) || batch > 0x7FFFFFFFu) return GF_EARG;
     if (overlaps(C, cb, D, cb)) return GF_EOVERLAP;
     void *tabs = nullptr, *inv = nullptr;
-    if (cudaGetSymbolAddress(&tabs, g_dev_tabs) != cudaSuccess ||
-        cudaGetSymbolAddress(&inv, g_dev_inv) != cudaSuccess)
+    if (symbol_address(0, &tabs) != GF_OK || symbol_address(1, &inv) != GF_OK)
         return GF_ECUDA;
     InvertParams p;
     p.C = C; p.D = D; p.rank = rank; p.batch = batch; p.N = N; p.qmask = field - 1;
@@ -768,7 +786,7 @@ int gf_verify_batch(int field, const uint8_t *A, const uint8_t *C, const uint8_t
     if (ws_bytes < u_bytes + 2 * y_bytes) return GF_EARG;
     uint8_t *U = static_cast<uint8_t *>(dev_ws), *Y1 = U + u_bytes, *Y2 = Y1 + y_bytes;
     void *mul = nullptr;
-    if (cudaGetSymbolAddress(&mul, g_dev_mul) != cudaSuccess) return GF_ECUDA;
+    if (symbol_address(2, &mul) != GF_OK) return GF_ECUDA;
     const cudaStream_t st = tls_stream;
     const size_t nu = batch * (size_t)N * t;
     project_coeffs_kernel<<<(unsigned)((nu + 255) / 256), 256, 0, st>>>(
