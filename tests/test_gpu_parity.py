@@ -295,6 +295,30 @@ def test_c5_chunk_sampled(gfm, q):
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("q", (2, 256))
+def test_next2_full_size_sampled(gfm, q):
+    """The paper's own shape (N = 16 source packets, K = 1) at
+    the NEXT-2 sweep's launch size (2 GiB of source, 1 KiB packets) through the
+    streaming kernel: sampled generations recomputed by the oracle from
+    host-regenerated inputs (device fill by absolute index)."""
+    N, K, M = 16, 1, 1024
+    G = (2 << 30) // (N * M)
+    seed = 190902871 + 2 + 1000 * q
+    assert gfm.encode_path(q, N, K, M) == "stream"
+    A = torch.empty((G, N, M), dtype=torch.uint8, device="cuda")
+    C = torch.empty((G, N, K), dtype=torch.uint8, device="cuda")
+    gfm.fill_random(A, seed, si.STREAM_A, 0)
+    gfm.fill_random(C, seed, si.STREAM_C, 0, mask=q - 1)
+    B = gfm.encode_batch(q, A, C)
+    rng = np.random.default_rng(q)
+    for g in sorted({0, G - 1, *rng.integers(0, G, 14).tolist()}):
+        Ah = si.random_bytes(seed, si.STREAM_A, g * N * M, N * M).reshape(1, N, M)
+        Ch = si.uniform_coeffs(q, seed, si.STREAM_C, g * N * K, N * K).reshape(1, N, K)
+        assert np.array_equal(B[g].cpu().numpy(), oracle.encode_batch(q, Ah, Ch)[0]), g
+    del A, B, C
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("q", (4, 256))
 def test_encode_host_path(gfm, q):
     batch, N, K, M = 37, 16, 8, 1500
