@@ -1,5 +1,5 @@
-// encode_lanek2.cuh -- persistent, mbarrier-pipelined lane-k encode for the
-// small fields (GF(2), GF(4)) with up to 32 coded packets (C5).
+// encode_lanek2.cuh -- persistent lane-k encode for the small fields (GF(2),
+// GF(4)) with up to 32 coded packets (C5).
 //
 //   B[g][k][m] = sum_i C[g][i][k] * A[g][i][m]          (Eq. 2)
 //
@@ -9,37 +9,35 @@
 // Alg. 1, with data and coefficient exchanged: a "four
 // Russians" table over the coefficient bits), and lane k of a gatherer warp
 // reads the row of ITS coefficients (one LDS per 32 products, <= 16 distinct
-// rows in distinct banks: one wavefront) -- but organised for the memory-bound
-// C5 shape, where each CTA of the one-shot kernel lived for only N/SG = 8 steps:
-//   * persistent CTAs (one per SM, 32 warps) walk a flattened (tile, step)
-//     sequence; tile = generation x 512 words;
-//   * 16 producer warps: source words straight from global memory into
-//     registers six steps ahead, 16-row table of step s into Q[s % 3], and
-//     (warp 16) the per-lane row indices of step s into a small ring; arrive
-//     FULL(s) after waiting DONE(s-3);
-//   * 16 gatherer warps (lane = k, 32 words per lane): wait FULL(s), 32
-//     gathers + XORs, arrive DONE(s); at a tile end each warp transposes its
-//     32 x 32-word block through its own shared-memory scratch (no cross-warp
-//     barrier) and writes 128-byte rows.
-// mbarrier rings of four objects (producers may run three steps ahead).
+// rows in distinct banks: one wavefront).  The one-shot kernel's CTAs live for
+// only N/SG = 8 steps on C5, so every CTA pays its start (first source loads,
+// coefficient indices) and its write-back unoverlapped; here CTAs are
+// persistent (two per SM) and walk a flattened (tile, step) sequence:
+//   * 4 builder warps: source words straight from global memory into
+//     registers three steps ahead (across tile boundaries), the 16-row table
+//     of step s into Q[s % 3] and (first builder warp) the per-lane row
+//     indices of step s into a 3-slot ring; named barriers FULL / EMPTY per
+//     buffer hand the tables to the gatherers, as in the one-shot kernel;
+//   * 8 gatherer warps (lane = k, 32 words per lane): 32 gathers + XORs per
+//     step; at a tile end each warp transposes its 32 x 32-word block through
+//     its own shared-memory scratch (no cross-warp barrier) and writes
+//     128-byte rows, while the builders already fill the next tile's tables.
 #pragma once
 #include <cstdint>
 
 #include "encode_lanek.cuh"
-#include "encode_prow.cuh"   // mbarrier helpers
 
 namespace gfr {
 
-constexpr int kL2GW = 16;                        // gatherer warps (0..15)
-constexpr int kL2PW = 16;                        // producer warps (16..31)
-constexpr int kL2Threads = 32 * (kL2GW + kL2PW);
-constexpr int kL2TW = 32 * kL2GW;                // words per tile (512)
+constexpr int kL2GW = 8;                         // gatherer warps (0..7)
+constexpr int kL2BW = 4;                         // builder warps (8..11)
+constexpr int kL2Threads = 32 * (kL2GW + kL2BW);
+constexpr int kL2TW = 32 * kL2GW;                // words per tile (256)
 constexpr int kL2QS = kL2TW + 1;                 // Q row stride (odd: gathers conflict-free)
 constexpr int kL2NQ = 3;                         // table buffers
 constexpr int kL2QWords = 16 * kL2QS;
 constexpr int kL2ScrS = 33;                      // epilogue scratch row stride (words)
-constexpr int kL2BWords = kL2TW / (32 * kL2PW);  // words per producer thread per step (1)
-constexpr int kL2D = 6;                          // source-word prefetch distance (steps)
+constexpr int kL2BWords = kL2TW / (32 * kL2BW);  // words per builder thread per step (2)
 
 struct Lk2Params {
     const uint8_t *A;
@@ -53,22 +51,21 @@ struct Lk2Params {
     size_t ntiles;     // batch * tiles
 };
 
-// shared memory: mbarriers | Q[3][16][QS] | row-index ring [3][32] | scratch[16][32][33]
-constexpr size_t kL2OffQ = 64;
-constexpr size_t kL2OffIdx = kL2OffQ + (size_t)kL2NQ * kL2QWords * 4;
+// shared memory: Q[3][16][QS] | row-index ring [3][32] | scratch[8][32][33]
+constexpr size_t kL2OffIdx = (size_t)kL2NQ * kL2QWords * 4;
 constexpr size_t kL2OffScr = kL2OffIdx + (size_t)kL2NQ * 32;
 constexpr size_t kL2Smem = kL2OffScr + (size_t)kL2GW * 32 * kL2ScrS * 4;
 
 template <int F>
-__global__ void __launch_bounds__(kL2Threads, 1) encode_lanek2_kernel(Lk2Params p)
+__global__ void __launch_bounds__(kL2Threads, 2) encode_lanek2_kernel(Lk2Params p)
 {
     using L = LkField<F>;
     constexpr int SG = L::kSG;
     static_assert(F == 2 || F == 4, "small fields only");
+    constexpr int NT = kL2Threads;
+    constexpr int BAR_FULL = 1, BAR_EMPTY = 1 + kL2NQ;          // named barrier ids
     extern __shared__ __align__(16) uint8_t l2_smem[];
-    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(l2_smem);
-    const uint32_t kFull = sbase, kDone = sbase + 32;        // 4 + 4 mbarriers
-    uint32_t *Q = reinterpret_cast<uint32_t *>(l2_smem + kL2OffQ);
+    uint32_t *Q = reinterpret_cast<uint32_t *>(l2_smem);
     uint8_t *idx = l2_smem + kL2OffIdx;
     uint32_t *scr = reinterpret_cast<uint32_t *>(l2_smem + kL2OffScr);
 
@@ -83,25 +80,17 @@ __global__ void __launch_bounds__(kL2Threads, 1) encode_lanek2_kernel(Lk2Params 
         return t / (size_t)p.tiles;
     };
 
-    if (tid == 0) {
-#pragma unroll
-        for (int b = 0; b < 4; b++) {
-            mbar_init(kFull + 8 * b, kL2PW);
-            mbar_init(kDone + 8 * b, kL2GW);
-        }
-#pragma unroll
-        for (int b = 0; b < 4; b++) mbar_arrive_n(kDone + 8 * b, kL2GW);   // DONE(-4 .. -1)
-    }
+    // zero rows (row index 0 = no source selected) of every buffer
+    for (int t = tid; t < kL2NQ * kL2QS; t += NT) Q[(t / kL2QS) * kL2QWords + t % kL2QS] = 0u;
     __syncthreads();
 
     if (warp >= kL2GW) {
-        // ======================= producers
-        const int pt = tid - 32 * kL2GW;                       // 0 .. 32 * kL2PW - 1
-        // source cursor
-        uint32_t aj = 0, aw0 = 0;
+        // ======================= builders
+        const int bt = tid - 32 * kL2GW;                       // 0 .. 127
+        uint32_t aj = 0, aw0 = 0;                              // source cursor
         int ast = 0;
         size_t ag = tile_g(0, aw0);
-        uint32_t ar[kL2D][kL2BWords][SG];
+        uint32_t ar[kL2NQ][kL2BWords][SG];
         auto load = [&](uint32_t (&a)[kL2BWords][SG]) {      // the cursor's step, then advance
             const bool live = aj < ntj;
             const uint8_t *Ag = p.A + ag * (size_t)p.N * p.M;
@@ -111,7 +100,7 @@ __global__ void __launch_bounds__(kL2Threads, 1) encode_lanek2_kernel(Lk2Params 
                 const uint32_t *row = reinterpret_cast<const uint32_t *>(Ag + (size_t)min(i, p.N - 1) * p.M);
 #pragma unroll
                 for (int u = 0; u < kL2BWords; u++) {
-                    const uint32_t wd = aw0 + (uint32_t)pt + 32u * kL2PW * u;
+                    const uint32_t wd = aw0 + (uint32_t)bt + 32u * kL2BW * u;
                     a[u][j] = (live && i < p.N && wd < p.Mw) ? __ldg(row + wd) : 0u;
                 }
             }
@@ -121,67 +110,73 @@ __global__ void __launch_bounds__(kL2Threads, 1) encode_lanek2_kernel(Lk2Params 
                 ag = tile_g(aj, aw0);
             }
         };
-        // coefficient-index cursor (warp 16 only): lane k's row index of each step
-        uint32_t cj = 0, cw0 = 0;
+        uint32_t cj = 0, cw0 = 0;                              // coefficient cursor (first builder warp)
         int cst = 0;
         size_t cg = tile_g(0, cw0);
-        auto row_index = [&]() -> uint32_t {                  // the cursor's step, then advance
-            uint8_t c[SG];
+        // raw coefficient bytes of lane k for the cursor's step (first builder warp;
+        // prefetched three steps ahead like the source words), then advance
+        auto load_c = [&](uint32_t (&c)[SG]) {
             const uint8_t *Cg = p.C + cg * (size_t)p.N * p.K;
 #pragma unroll
             for (int j = 0; j < SG; j++) {
                 const int i = cst * SG + j;
-                c[j] = (cj < ntj && i < p.N && lane < p.K) ? __ldg(Cg + (size_t)i * p.K + lane) : (uint8_t)0;
+                c[j] = (cj < ntj && i < p.N && lane < p.K) ? (uint32_t)__ldg(Cg + (size_t)i * p.K + lane) : 0u;
             }
             if (++cst == p.NS) {
                 cst = 0;
                 cj++;
                 cg = tile_g(cj, cw0);
             }
-            return L::index(c);
         };
-        auto pstep = [&](uint32_t s, uint32_t b, uint32_t (&a)[kL2BWords][SG]) {
-            mbar_wait(kDone + ((s - 3) & 3u) * 8u, ((s + 1) >> 2) & 1u);   // DONE(s-3): buffer b free
+        uint32_t cr[kL2NQ][SG];
+        auto bstep = [&](uint32_t s, int b, uint32_t (&a)[kL2BWords][SG], uint32_t (&c)[SG]) {
+            if (s >= kL2NQ) nbar_sync(BAR_EMPTY + b, NT);       // gatherers done with step s-NQ
             uint32_t *q = Q + b * kL2QWords;
 #pragma unroll
-            for (int u = 0; u < kL2BWords; u++) build_word<F, kL2QS>(q + pt + 32 * kL2PW * u, a[u]);
-            if (warp == kL2GW) idx[b * 32 + lane] = (uint8_t)row_index();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(kFull + (s & 3u) * 8u);
-            load(a);                                           // step s + kL2D
-        };
-        // zero rows of every buffer (row index 0 = no source selected)
-        for (int t = pt; t < kL2NQ * kL2QS; t += 32 * kL2PW) Q[(t / kL2QS) * kL2QWords + t % kL2QS] = 0u;
+            for (int u = 0; u < kL2BWords; u++) build_word<F, kL2QS>(q + bt + 32 * kL2BW * u, a[u]);
+            if (warp == kL2GW) {
+                uint8_t cb[SG];
 #pragma unroll
-        for (int d = 0; d < kL2D; d++) load(ar[d]);
-        static_assert(kL2D == 6 && kL2NQ == 3, "producer loop unrolled 6 = 2 x NQ");
-#pragma unroll 1
-        for (uint32_t s = 0; s < total; s += 6) {
-            pstep(s, 0, ar[0]);
-            if (s + 1 < total) pstep(s + 1, 1, ar[1]);
-            if (s + 2 < total) pstep(s + 2, 2, ar[2]);
-            if (s + 3 < total) pstep(s + 3, 0, ar[3]);
-            if (s + 4 < total) pstep(s + 4, 1, ar[4]);
-            if (s + 5 < total) pstep(s + 5, 2, ar[5]);
+                for (int j = 0; j < SG; j++) cb[j] = (uint8_t)c[j];
+                idx[b * 32 + lane] = (uint8_t)L::index(cb);
+            }
+            nbar_arrive(BAR_FULL + b, NT);
+            load(a);                                           // step s + 3
+            if (warp == kL2GW) load_c(c);
+        };
+        load(ar[0]);
+        load(ar[1]);
+        load(ar[2]);
+        if (warp == kL2GW) {
+            load_c(cr[0]);
+            load_c(cr[1]);
+            load_c(cr[2]);
         }
+#pragma unroll 1
+        for (uint32_t s = 0; s < total; s += 3) {
+            bstep(s, 0, ar[0], cr[0]);
+            if (s + 1 < total) bstep(s + 1, 1, ar[1], cr[1]);
+            if (s + 2 < total) bstep(s + 2, 2, ar[2], cr[2]);
+        }
+        // consume the gatherers' last NQ EMPTY signals
+        for (uint32_t s = max(total, (uint32_t)kL2NQ); s < total + kL2NQ; s++) nbar_sync(BAR_EMPTY + s % kL2NQ, NT);
         return;
     }
 
-    // ======================= gatherers: lane = coded packet k, words 32 gw .. 32 gw + 31
+    // ======================= gatherers: lane = coded packet k, words 32 warp .. 32 warp + 31
     uint32_t *myscr = scr + warp * 32 * kL2ScrS;
     uint32_t acc[32];
 #pragma unroll
     for (int w = 0; w < 32; w++) acc[w] = 0u;
     int st_g = 0;
     uint32_t j_g = 0;
-    auto gstep = [&](uint32_t s, uint32_t b) {
-        mbar_wait(kFull + (s & 3u) * 8u, (s >> 2) & 1u);
+    auto gstep = [&](uint32_t s, int b) {
+        nbar_sync(BAR_FULL + b, NT);
         const uint32_t r = idx[b * 32 + lane];
         const uint32_t *row = Q + b * kL2QWords + r * kL2QS + warp * 32;
 #pragma unroll
         for (int w = 0; w < 32; w++) acc[w] ^= row[w];
-        __syncwarp();
-        if (lane == 0) mbar_arrive(kDone + (s & 3u) * 8u);
+        nbar_arrive(BAR_EMPTY + b, NT);
         if (++st_g == p.NS) {
             st_g = 0;
             // ---- write back: transpose the warp's 32 x 32-word block through its scratch

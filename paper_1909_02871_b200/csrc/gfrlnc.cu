@@ -366,7 +366,7 @@ static int launch_lanek2(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, 
     int dev;
     if (current_device(&dev) != GF_OK) return GF_ECUDA;
     const size_t sms = (size_t)(g_sm_count[dev] > 0 ? g_sm_count[dev] : 148);
-    const size_t grid = p.ntiles < sms ? p.ntiles : sms;      // persistent: one CTA per SM
+    const size_t grid = p.ntiles < 2 * sms ? p.ntiles : 2 * sms;   // persistent: two CTAs per SM
     if ((p.ntiles + grid - 1) / grid * (size_t)p.NS > 0x7FFFFFF0u) return GF_EARG;
     if (cudaFuncSetAttribute(encode_lanek2_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)kL2Smem) != cudaSuccess)
