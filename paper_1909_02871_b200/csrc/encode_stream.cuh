@@ -39,8 +39,8 @@ struct StreamParams {
     const uint8_t *C;
     uint8_t *B;
     const uint32_t *tabs;   // table of tables of the field (16 words per coefficient)
-    size_t M16;             // 16-byte chunks per packet
-    size_t total;           // batch * M16
+    size_t M16;             // chunks per packet (16-byte chunks, or 4-byte ones for word-aligned packets)
+    size_t total;           // batch * chunks per packet
     int N, K;
     uint32_t qmask;
 };
@@ -103,24 +103,50 @@ template <> struct StreamOp<256> {
     __device__ __forceinline__ static uint32_t mul(uint32_t x, const E &e) { return lookup_perm(e.T, make_sel(x)); }
 };
 
-template <int F, int KT>
+// V = 4: 16-byte chunks (packets 16-byte aligned, the fast path); V = 1:
+// 4-byte chunks for packets that are only word aligned (e.g. M = 1500)
+template <int V> __device__ __forceinline__ void st_load(uint32_t (&a)[V], const uint8_t *p)
+{
+    if constexpr (V == 4) {
+        const uint4 v = st_ld_stream(reinterpret_cast<const uint4 *>(p));
+        a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w;
+    } else {
+        a[0] = __ldg(reinterpret_cast<const uint32_t *>(p));
+    }
+}
+template <int V> __device__ __forceinline__ void st_store(uint8_t *p, const uint32_t (&r)[V])
+{
+    if constexpr (V == 4) *reinterpret_cast<uint4 *>(p) = make_uint4(r[0], r[1], r[2], r[3]);
+    else *reinterpret_cast<uint32_t *>(p) = r[0];
+}
+
+template <int F, int KT, int V>
 __global__ void __launch_bounds__(kStThreads) encode_stream_kernel(StreamParams p)
 {
     using Op = StreamOp<F>;
     constexpr int kStBatch = F <= 4 ? 8 : 4;                  // source chunks loaded together (measured)
+    constexpr size_t kChunk = 4 * V;                           // bytes per chunk
+    const size_t Mc = p.M16;                                   // chunks per packet
+    const size_t M = Mc * kChunk;
     const size_t stride = (size_t)gridDim.x * kStThreads;
     for (size_t t = (size_t)blockIdx.x * kStThreads + threadIdx.x; t < p.total; t += stride) {
-        const size_t g = t / p.M16, ch = t - g * p.M16;
-        const uint4 *Ag = reinterpret_cast<const uint4 *>(p.A + g * (size_t)p.N * (p.M16 * 16)) + ch;
+        const size_t g = t / Mc, ch = t - g * Mc;
+        const uint8_t *Ag = p.A + g * (size_t)p.N * M + ch * kChunk;
         const uint8_t *Cg = p.C + g * (size_t)p.N * p.K;
-        uint4 acc[KT];
+        uint32_t acc[KT][V];
 #pragma unroll
-        for (int k = 0; k < KT; k++) acc[k] = make_uint4(0u, 0u, 0u, 0u);
+        for (int k = 0; k < KT; k++)
+#pragma unroll
+            for (int v = 0; v < V; v++) acc[k][v] = 0u;
         for (int i0 = 0; i0 < p.N; i0 += kStBatch) {
-            uint4 a[kStBatch];
+            uint32_t a[kStBatch][V];
 #pragma unroll
-            for (int b = 0; b < kStBatch; b++)
-                a[b] = i0 + b < p.N ? st_ld_stream(Ag + (size_t)(i0 + b) * p.M16) : make_uint4(0u, 0u, 0u, 0u);
+            for (int b = 0; b < kStBatch; b++) {
+                if (i0 + b < p.N) st_load<V>(a[b], Ag + (size_t)(i0 + b) * M);
+                else
+#pragma unroll
+                    for (int v = 0; v < V; v++) a[b][v] = 0u;
+            }
 #pragma unroll
             for (int b = 0; b < kStBatch; b++) {
                 if (i0 + b >= p.N) break;
@@ -129,21 +155,20 @@ __global__ void __launch_bounds__(kStThreads) encode_stream_kernel(StreamParams 
                     if (k < p.K) {
                         const uint32_t c = __ldg(Cg + (size_t)(i0 + b) * p.K + k) & p.qmask;
                         const typename Op::E e = Op::entry(p.tabs + (size_t)c * kTableWords);
-                        acc[k].x ^= Op::mul(a[b].x, e);
-                        acc[k].y ^= Op::mul(a[b].y, e);
-                        acc[k].z ^= Op::mul(a[b].z, e);
-                        acc[k].w ^= Op::mul(a[b].w, e);
+#pragma unroll
+                        for (int v = 0; v < V; v++) acc[k][v] ^= Op::mul(a[b][v], e);
                     }
                 }
             }
         }
-        uint4 *Bg = reinterpret_cast<uint4 *>(p.B + g * (size_t)p.K * (p.M16 * 16)) + ch;
+        uint8_t *Bg = p.B + g * (size_t)p.K * M + ch * kChunk;
 #pragma unroll
         for (int k = 0; k < KT; k++) {
             if (k < p.K) {
-                uint4 r = acc[k];
-                if (Op::kPermuted) r = make_uint4(unperm(r.x), unperm(r.y), unperm(r.z), unperm(r.w));
-                Bg[(size_t)k * p.M16] = r;
+                uint32_t r[V];
+#pragma unroll
+                for (int v = 0; v < V; v++) r[v] = Op::kPermuted ? unperm(acc[k][v]) : acc[k][v];
+                st_store<V>(Bg + (size_t)k * M, r);
             }
         }
     }

@@ -316,7 +316,7 @@ static int launch_prow(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, in
     return launch_status();
 }
 
-template <int F, int KT>
+template <int F, int KT, int V>
 static int launch_stream_t(const StreamParams &p, cudaStream_t st)
 {
     int dev;
@@ -324,16 +324,22 @@ static int launch_stream_t(const StreamParams &p, cudaStream_t st)
     const size_t sms = (size_t)(g_sm_count[dev] > 0 ? g_sm_count[dev] : 148);
     size_t grid = (p.total + kStThreads - 1) / kStThreads;
     if (grid > sms * 8) grid = sms * 8;                       // grid-stride: 8 CTAs of 256 per SM
-    encode_stream_kernel<F, KT><<<(unsigned)grid, kStThreads, 0, st>>>(p);
+    encode_stream_kernel<F, KT, V><<<(unsigned)grid, kStThreads, 0, st>>>(p);
     return launch_status();
 }
 
-template <int F>
-static int launch_stream_f(const StreamParams &p, cudaStream_t st)
+template <int F, int V>
+static int launch_stream_v(const StreamParams &p, cudaStream_t st)
 {
-    if (p.K == 1) return launch_stream_t<F, 1>(p, st);
-    if (p.K == 2) return launch_stream_t<F, 2>(p, st);
-    return launch_stream_t<F, 4>(p, st);
+    if (p.K == 1) return launch_stream_t<F, 1, V>(p, st);
+    if (p.K == 2) return launch_stream_t<F, 2, V>(p, st);
+    return launch_stream_t<F, 4, V>(p, st);
+}
+
+template <int F>
+static int launch_stream_f(const StreamParams &p, bool wide, cudaStream_t st)
+{
+    return wide ? launch_stream_v<F, 4>(p, st) : launch_stream_v<F, 1>(p, st);
 }
 
 static int launch_stream(int field, int fi, const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K,
@@ -343,13 +349,16 @@ static int launch_stream(int field, int fi, const uint8_t *A, const uint8_t *C, 
     void *tabs = nullptr;
     if (symbol_address(0, &tabs) != GF_OK) return GF_ECUDA;
     p.tabs = reinterpret_cast<const uint32_t *>(tabs) + (size_t)fi * 256 * kTableWords;
-    p.A = A; p.C = C; p.B = B; p.M16 = M / 16; p.total = batch * p.M16; p.N = N; p.K = K;
+    // 16-byte chunks when packets are 16-byte aligned, else 4-byte chunks
+    const bool wide = M % 16 == 0 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0 &&
+                      (reinterpret_cast<uintptr_t>(B) & 15u) == 0;
+    p.A = A; p.C = C; p.B = B; p.M16 = wide ? M / 16 : M / 4; p.total = batch * p.M16; p.N = N; p.K = K;
     p.qmask = (uint32_t)field - 1u;
     switch (field) {
-    case 2: return launch_stream_f<2>(p, st);
-    case 4: return launch_stream_f<4>(p, st);
-    case 16: return launch_stream_f<16>(p, st);
-    case 256: return launch_stream_f<256>(p, st);
+    case 2: return launch_stream_f<2>(p, wide, st);
+    case 4: return launch_stream_f<4>(p, wide, st);
+    case 16: return launch_stream_f<16>(p, wide, st);
+    case 256: return launch_stream_f<256>(p, wide, st);
     default: return GF_EFIELD;
     }
 }
@@ -411,7 +420,7 @@ static int encode_path_override()
 
 // 0 column (words), 1 column (bytes), 2 lane-k KG=1, 3 lane-k KG=2,
 // 4 fused KG=1, 5 fused KG=2, 6 product-row, 7 persistent lane-k (GF(2)/GF(4), K <= 32),
-// 8 streaming (K <= 4, 16-byte aligned packets).  The fused kernel (lane-k + column warps on one
+// 8 streaming (K <= 4, word-aligned packets).  The fused kernel (lane-k + column warps on one
 // tile) is correct but measured slower than lane-k alone (per-step barrier
 // coupling of the two roles): opt-in via GFRLNC_ENCODE_PATH=fused.
 static bool lanek2_default()
@@ -426,9 +435,7 @@ static int encode_path(int field, int N, int K, size_t M, const void *A, const v
                          (reinterpret_cast<uintptr_t>(B) & 3u) == 0 && M / 4 < 0xFFFFFFFFull;
     const int ov = encode_path_override();
     if (!aligned) return 1;
-    const bool aligned16 = M % 16 == 0 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0 &&
-                           (reinterpret_cast<uintptr_t>(B) & 15u) == 0;
-    if (aligned16 && K <= 4 && (ov == 6 || ov == 0)) return 8;
+    if (K <= 4 && (ov == 6 || ov == 0)) return 8;                // streaming (16- or 4-byte chunks)
     if (ov == 1 || (ov == 0 && K < 24)) return 0;
     const int kg2 = K > 32 ? 1 : 0;      // (K > 64 uses 128 coded packets per CTA)
     if (ov == 3) return 4 + kg2;

@@ -202,9 +202,11 @@ def test_encode_path_query():
     assert gf.encode_path(2, 32, 32, 1 << 20) == "lanek-32"     # C5
     assert gf.encode_path(256, 16, 1, 1024) == "stream"         # NEXT-2 (paper: N = 16, K = 1)
     assert gf.encode_path(2, 16, 4, 65536) == "stream"
-    assert gf.encode_path(256, 16, 1, 1024, a_align=4) == "column-words"   # not 16-B aligned
+    assert gf.encode_path(256, 16, 1, 1024, a_align=4) == "stream"    # 4-byte chunks
+    assert gf.encode_path(256, 16, 1, 1500) == "stream"                # C1 (M % 16 != 0)
+    assert gf.encode_path(256, 16, 1, 1500, a_align=2) == "column-bytes"
     assert gf.encode_path(256, 16, 5, 1024) == "column-words"
-    assert gf.encode_path(256, 16, 1, 1500) == "column-words"
+    assert gf.encode_path(256, 16, 8, 1500) == "column-words"
     assert gf.encode_path(4, 3, 5, 13) == "column-bytes"
     assert gf.encode_path(256, 64, 64, 1500, a_align=1) == "column-bytes"
     with pytest.raises(gf.GFError):

@@ -21,7 +21,8 @@ if want == "lanek2":       # persistent lane-k: GF(2)/GF(4), K <= 32
                                               (7, 9, 1540, 2), (33, 32, 2052, 2), (32, 32, 65536, 2), (4, 1, 2048, 300))]
 elif want == "stream":    # few coded packets, 16-byte aligned packets (the paper's N = 16, K = 1)
     cases = [(q, s) for q in (2, 4, 16, 256) for s in ((16, 1, 1024, 50), (16, 1, 128, 300), (5, 2, 4096, 3),
-                                                       (17, 3, 2064, 4), (64, 4, 16, 100), (1, 1, 16, 10))]
+                                                       (17, 3, 2064, 4), (64, 4, 16, 100), (1, 1, 16, 10),
+                                                       (16, 1, 1500, 7), (9, 3, 1028, 5), (3, 4, 4, 33))]
 else:
     cases = [(q, s) for q in (2, 4, 16, 256) for s in ((17, 33, 1500, 3), (64, 64, 1500, 2), (32, 32, 4100, 2),
                                                        (5, 24, 400, 3), (33, 96, 3000, 2), (7, 65, 1540, 2))]
