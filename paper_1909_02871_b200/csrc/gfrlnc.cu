@@ -324,7 +324,8 @@ static int launch_stream_t(const StreamParams &p, cudaStream_t st)
     const size_t sms = (size_t)(g_sm_count[dev] > 0 ? g_sm_count[dev] : 148);
     size_t grid = (p.total + kStThreads - 1) / kStThreads;
     if (grid > sms * 8) grid = sms * 8;                       // grid-stride: 8 CTAs of 256 per SM
-    encode_stream_kernel<F, KT, V><<<(unsigned)grid, kStThreads, 0, st>>>(p);
+    if constexpr (V == 4) encode_stream_kernel<F, KT><<<(unsigned)grid, kStThreads, 0, st>>>(p);
+    else encode_stream_words_kernel<F, KT, V><<<(unsigned)grid, kStThreads, 0, st>>>(p);
     return launch_status();
 }
 
