@@ -75,6 +75,11 @@ __global__ void __launch_bounds__(256) invert_kernel(InvertParams p)
     }
     __syncthreads();
 
+    // elimination geometry: tpr threads per row (a power of two, tpr * N <= nt)
+    int tpr = 1;
+    while (tpr * 2 * N <= nt && tpr < 32) tpr *= 2;
+    const int rl = tid % tpr, r0 = tid / tpr, rstep = nt / tpr;
+
     int rank = 0;
     for (int col = 0; col < N; col++) {
         // pivot: first row >= rank with a nonzero entry in this column
@@ -98,13 +103,16 @@ __global__ void __launch_bounds__(256) invert_kernel(InvertParams p)
         __syncthreads();
         for (int r = tid; r < N; r += nt) s_fac[r] = r == rank ? 0 : Mb[(size_t)r * RW * 4 + col];
         __syncthreads();
-        // eliminate the column from every other row
-        const int span = RW - w0;
-        for (int e = tid; e < N * span; e += nt) {
-            const int r = e / span, w = w0 + (e - r * span);
+        // eliminate the column from every other row: TPR threads per row, each
+        // loads its row's factor table once per column (no per-element division
+        // or table reload)
+        for (int r = r0; r < N; r += rstep) {
             const uint32_t f = s_fac[r];
             if (f == 0) continue;
-            Mx[(size_t)r * RW + w] ^= mul_word(tab_of(stab, f), Mx[(size_t)rank * RW + w]);
+            const PrmtTab T = tab_of(stab, f);
+            uint32_t *row = Mx + (size_t)r * RW;
+            const uint32_t *prow = Mx + (size_t)rank * RW;
+            for (int w = w0 + rl; w < RW; w += tpr) row[w] ^= mul_word(T, prow[w]);
         }
         __syncthreads();
         rank++;
