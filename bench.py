@@ -454,13 +454,22 @@ def run_e2e(gf, torch, dist, cfg, q, sh, device, ws, args):
     out, host<->device copies inside the timed region every step."""
     N, K, M, Ms = cfg.N, cfg.K, cfg.M, sh.columns
     per_gen_host = N * Ms + N * K + K * Ms
-    G = min(sh.generations, max(1, int(14e9 // per_gen_host)))
+    # pinned host buffers: <= 14 GB per rank and <= 48 GB per node in total
+    G = min(sh.generations, max(1, int(min(14e9, 48e9 / ws) // per_gen_host)))
+    err = None
     try:
         Ah = torch.empty((G, N, Ms), dtype=torch.uint8).pin_memory()
         Ch = torch.empty((G, N, K), dtype=torch.uint8).pin_memory()
         Bh = torch.empty((G, K, Ms), dtype=torch.uint8).pin_memory()
     except Exception as e:  # pinned host memory exhausted
-        return {"value": None, "unit": "GB/s", "error": f"pinned alloc failed: {e}"}
+        err = f"pinned alloc failed: {e}"
+    if ws > 1:                       # every rank skips together (no rank left in a barrier)
+        ok = torch.tensor([0 if err else 1], device=device)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0 and err is None:
+            err = "pinned alloc failed on another rank"
+    if err:
+        return {"value": None, "unit": "GB/s", "error": err}
     seed = si.field_seed(cfg, q)
     step = max(1, min(G, int(2e9 // (N * Ms + N * K))))
     tmpA = torch.empty((step, N, Ms), dtype=torch.uint8, device=device)
