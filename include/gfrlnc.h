@@ -165,15 +165,16 @@ int gf_host_tables(int field, uint32_t *out, size_t cap_words);
  * kernel on bytes (unaligned or M % 4 != 0), 2 = lane-k kernel with 32 coded
  * packets per CTA, 3 = lane-k kernel with 64, 4 / 5 = fused lane-k + column
  * kernel with 32 / 64, 6 = product-row kernel (GF(16)/GF(256), K > 32: C3,
- * C4), 7 = persistent lane-k (opt-in, GF(2)/GF(4), K <= 32) (DESIGN.md
+ * C4), 7 = persistent lane-k (opt-in, GF(2)/GF(4), K <= 32), 8 = streaming
+ * kernel (K <= 4: C1 and the paper's N = 16, K = 1 shape) (DESIGN.md
  * section 6), or GF_EFIELD / GF_EARG. */
 int gf_encode_path(int field, int N, int K, size_t M, size_t a_align, size_t b_align);
 
 /* Harness-only (experiments, forced-path tests): force the encode kernel of
  * the calling thread's gf_encode_batch calls.  0 = automatic (default), 1 =
  * column kernel, 2 = lane-k, 3 = fused lane-k + column, 4 = product-row,
- * 5 = persistent lane-k (GF(2)/GF(4) with K <= 32; other shapes fall back to
- * lane-k).
+ * 5 = persistent lane-k (GF(2)/GF(4) with K <= 32), 6 = streaming (K <= 4);
+ * shapes a forced kernel cannot take fall back to lane-k.
  * Thread-local; returns GF_OK or GF_EARG.  Takes precedence over the
  * GFRLNC_ENCODE_PATH environment variable. */
 int gf_set_encode_path(int path);
