@@ -57,10 +57,20 @@ constexpr int kPrThreads = 512;
 constexpr int kPrGW = 12;                     // gatherer warps (warps 0..11)
 constexpr int kPrPW = 4;                      // producer warps (warps 12..15, one warpgroup)
 constexpr int kPrGRegs = 152, kPrPRegs = 56;  // setmaxnreg budgets: 12*32*152 + 4*32*56 = 65536
-constexpr int kPrR = 4;                       // words per gatherer lane
-constexpr int kPrTW = kPrR * kPrGW * 8;       // words per tile (384)
-constexpr int kPrKC = 64;                     // coded packets per CTA
-constexpr int kPrS = 4;                       // source packets per step
+constexpr int kPrTW = 384;                    // words per tile
+// Coded packets per CTA (KC = 64, or 32 for K <= 32): a table row (one source
+// byte value) is 256 B = S sources x KC products, so a step covers S = 256 / KC
+// source packets, a quarter-warp is WQ words x NKC 16-byte coefficient chunks
+// (8 lanes on 8 distinct bank slots) and a lane holds R words (64 or 32
+// accumulator registers).
+template <int KC> struct PrCfg {
+    static constexpr int S = 256 / KC;                         // sources per step (4 / 8)
+    static constexpr int NKC = KC / 16;                        // 16-B chunks per source row (4 / 2)
+    static constexpr int WQ = 8 / NKC;                         // words per quarter-warp (2 / 4)
+    static constexpr int WPW = 4 * WQ;                         // words per warp per round
+    static constexpr int R = kPrTW / (kPrGW * WPW);            // words per gatherer lane (4 / 2)
+    static_assert(R * kPrGW * WPW == kPrTW, "tile geometry");
+};
 constexpr uint32_t kPrBar = 0x0400u;          // mbarriers: BUILT[4], DONE[4] at the dynamic window base
 constexpr uint32_t kPrTab0 = 0x1000u;         // tables u = 0, 1, 2 at kPrTab0 + u * 0x10000
 constexpr uint32_t kPrBasis = 0x31000u;       // basis rows: 2 buffers x 8 x 256 B
@@ -74,9 +84,9 @@ struct ProwParams {
     size_t M;          // bytes per packet (multiple of 4)
     uint32_t Mw;       // words per packet
     int N, K;
-    int NS;            // steps per tile: ceil(N / 4)
+    int NS;            // steps per tile: ceil(N / S)
     int tiles;         // word tiles per packet
-    int k_tiles;       // ceil(K / 64)
+    int k_tiles;       // ceil(K / KC)
     size_t ntiles;     // batch * tiles * k_tiles
     uint32_t qmask4;   // q - 1 in every byte
     int cword;         // coefficient rows can be read as 32-bit words
@@ -186,9 +196,11 @@ struct PrTile {
 
 template <uint32_t V> struct PrU { static constexpr uint32_t value = V; };
 
-template <int F>
+template <int F, int KC>
 __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p)
 {
+    using Cf = PrCfg<KC>;
+    constexpr int kPrS = Cf::S, NKC = Cf::NKC;
     // mbarrier rings, object x & 3 for step x: BUILT(x) (4 producer-warp
     // arrivals) is phase x >> 2; DONE(x) (12 gatherer-warp arrivals) is phase
     // (x + 4) >> 2, the virtual steps -4..-1 pre-arrived.
@@ -206,7 +218,7 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
         const size_t rest = t / (size_t)p.k_tiles;
         r.w0 = (uint32_t)(rest % (size_t)p.tiles) * kPrTW;
         r.g = rest / (size_t)p.tiles;
-        r.k0 = kt * kPrKC;
+        r.k0 = kt * KC;
         return r;
     };
 
@@ -225,22 +237,23 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
         // ======================= producers: basis rows + tables
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" :: "n"(kPrPRegs));
         const int pt = tid - kPrGW * 32;                       // 0 .. 127
-        // basis geometry: coefficient word (chunk cc16, word cwq), bits b0, b0+2, b0+4, b0+6
+        // basis geometry: coefficient word (chunk cc16 = source cc16 / NKC, coefficient
+        // chunk cc16 % NKC; word cwq), bits b0, b0+2, b0+4, b0+6
         const int cwq = pt & 3, cc16 = (pt >> 2) & 15, b0 = pt >> 6;
-        // coefficient cursor: &C[g][4 st + (cc16 >> 2)][k0 + 16 (cc16 & 3) + 4 cwq]
+        // coefficient cursor: &C[g][S st + cc16 / NKC][k0 + 16 (cc16 % NKC) + 4 cwq]
         uint32_t cj = 0;
         int cst = 0;
         const uint8_t *cptr = nullptr;
         bool kok = false;
         auto setc = [&]() {
             const PrTile T = tile_of(cj);
-            const int k = T.k0 + 16 * (cc16 & 3) + 4 * cwq;
-            cptr = p.C + (T.g * (size_t)p.N + (size_t)(cc16 >> 2)) * p.K + k;
+            const int k = T.k0 + 16 * (cc16 % NKC) + 4 * cwq;
+            cptr = p.C + (T.g * (size_t)p.N + (size_t)(cc16 / NKC)) * p.K + k;
             kok = cj < ntj && k < p.K;
         };
         auto load_c = [&]() -> uint32_t {                      // raw word of the cursor's step
             uint32_t c = 0;
-            if (kok && kPrS * cst + (cc16 >> 2) < p.N) {
+            if (kok && kPrS * cst + (cc16 / NKC) < p.N) {
                 if (p.cword) {
                     c = __ldg(reinterpret_cast<const uint32_t *>(cptr));
                 } else {
@@ -322,11 +335,11 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
 
     // ======================= gatherers
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" :: "n"(kPrGRegs));
-    constexpr int R = kPrR;
+    constexpr int R = Cf::R;
     const int qw = lane >> 3, ql = lane & 7;
-    const int jw = ql >> 2, kc = ql & 3;
-    const uint32_t wbase = (uint32_t)(warp * 8 + qw * 2 + jw);   // word r of the lane: wbase + 96 r
-    constexpr uint32_t kRW = kPrGW * 8;
+    const int jw = ql / NKC, kc = ql % NKC;
+    const uint32_t wbase = (uint32_t)(warp * Cf::WPW + qw * Cf::WQ + jw);   // word r: wbase + kRW r
+    constexpr uint32_t kRW = kPrGW * Cf::WPW;
 
     // source-word cursor: a = &A[g][4 st][w0 + wbase] (bytes), vmask bit r = word r valid
     uint32_t aj = 0;
@@ -342,15 +355,15 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
             if (aj < ntj && T.w0 + wbase + kRW * r < p.Mw) vmask |= 1u << r;
     };
     uint32_t areg[R][kPrS];
-    // byte offset of sub-step t's source row within the step: ((jw + t) & 3) * M
+    // byte offset of sub-step t's source row within the step: ((jw + t) mod S) * M
     size_t soff[kPrS];
 #pragma unroll
-    for (int t = 0; t < kPrS; t++) soff[t] = (size_t)((jw + t) & 3) * p.M;
+    for (int t = 0; t < kPrS; t++) soff[t] = (size_t)((jw + t) & (kPrS - 1)) * p.M;
     auto load_a = [&]() {                                      // the cursor's step, then advance
         const int nsrc = p.N - kPrS * ast;                     // sources of the step that exist
 #pragma unroll
         for (int t = 0; t < kPrS; t++) {
-            const bool iok = ((jw + t) & 3) < nsrc;
+            const bool iok = ((jw + t) & (kPrS - 1)) < nsrc;
             const uint32_t *row = reinterpret_cast<const uint32_t *>(aptr + soff[t]);
 #pragma unroll
             for (int r = 0; r < R; r++) areg[r][t] = (iok && (vmask >> r & 1u)) ? __ldg(row + kRW * r) : 0u;
@@ -377,21 +390,24 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
     auto step = [&](uint32_t s, auto U) {
         constexpr uint32_t u = decltype(U)::value;             // table buffer of step s
         mbar_wait(kBuilt + (s & 3u) * 8u, (s >> 2) & 1u);
-        const uint32_t col0 = (uint32_t)(jw * 64 + kc * 16), col1 = (uint32_t)(((jw + 1) & 3) * 64 + kc * 16);
-        const uint32_t col2 = (uint32_t)(((jw + 2) & 3) * 64 + kc * 16), col3 = (uint32_t)(((jw + 3) & 3) * 64 + kc * 16);
+        // table column of sub-step t: source (jw + t) mod S, coefficient chunk kc
+        uint32_t col[kPrS];
+#pragma unroll
+        for (int t = 0; t < kPrS; t++) col[t] = (uint32_t)(((jw + t) & (kPrS - 1)) * KC + kc * 16);
 #pragma unroll
         for (int r = 0; r < R; r++) {
 #pragma unroll
             for (int j = 0; j < 4; j++) {
                 const uint32_t sel = 0x5504u | (j << 4);
-                const uint4 v0 = lds128_at<kPrTab0 + u * 0x10000u>(prmt(areg[r][0], col0, sel));
-                const uint4 v1 = lds128_at<kPrTab0 + u * 0x10000u>(prmt(areg[r][1], col1, sel));
-                const uint4 v2 = lds128_at<kPrTab0 + u * 0x10000u>(prmt(areg[r][2], col2, sel));
-                const uint4 v3 = lds128_at<kPrTab0 + u * 0x10000u>(prmt(areg[r][3], col3, sel));
-                acc[r][j].x = xor3(acc[r][j].x, v0.x, v1.x) ^ (v2.x ^ v3.x);
-                acc[r][j].y = xor3(acc[r][j].y, v0.y, v1.y) ^ (v2.y ^ v3.y);
-                acc[r][j].z = xor3(acc[r][j].z, v0.z, v1.z) ^ (v2.z ^ v3.z);
-                acc[r][j].w = xor3(acc[r][j].w, v0.w, v1.w) ^ (v2.w ^ v3.w);
+#pragma unroll
+                for (int t = 0; t < kPrS; t += 2) {
+                    const uint4 v0 = lds128_at<kPrTab0 + u * 0x10000u>(prmt(areg[r][t], col[t], sel));
+                    const uint4 v1 = lds128_at<kPrTab0 + u * 0x10000u>(prmt(areg[r][t + 1], col[t + 1], sel));
+                    acc[r][j].x = xor3(acc[r][j].x, v0.x, v1.x);
+                    acc[r][j].y = xor3(acc[r][j].y, v0.y, v1.y);
+                    acc[r][j].z = xor3(acc[r][j].z, v0.z, v1.z);
+                    acc[r][j].w = xor3(acc[r][j].w, v0.w, v1.w);
+                }
             }
         }
         load_a();                                              // step s + 1

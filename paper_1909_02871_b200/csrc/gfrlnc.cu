@@ -286,15 +286,15 @@ static int dyn_smem_base(uint32_t *base)
     return GF_OK;
 }
 
-template <int F>
+template <int F, int KC>
 static int launch_prow(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M,
                        size_t batch, cudaStream_t st)
 {
     ProwParams p;
     p.A = A; p.C = C; p.B = B; p.M = M; p.Mw = (uint32_t)(M / 4);
-    p.N = N; p.K = K; p.NS = (N + kPrS - 1) / kPrS;
+    p.N = N; p.K = K; p.NS = (N + PrCfg<KC>::S - 1) / PrCfg<KC>::S;
     p.tiles = (int)((p.Mw + kPrTW - 1) / kPrTW);
-    p.k_tiles = (K + kPrKC - 1) / kPrKC;
+    p.k_tiles = (K + KC - 1) / KC;
     p.qmask4 = (uint32_t)(F - 1) * 0x01010101u;
     p.cword = (K % 4 == 0 && (reinterpret_cast<uintptr_t>(C) & 3u) == 0) ? 1 : 0;
     p.ntiles = batch * (size_t)p.tiles * (size_t)p.k_tiles;
@@ -309,11 +309,21 @@ static int launch_prow(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, in
     if (rc != GF_OK) return rc;
     if (base > kPrBar) return GF_EARG;                        // layout needs the window to start at <= 0x400
     const size_t smem = kPrSmemEnd - base;
-    if (cudaFuncSetAttribute(encode_prow_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(encode_prow_kernel<F, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
         return GF_ECUDA;
-    encode_prow_kernel<F><<<(unsigned)grid, kPrThreads, smem, st>>>(p);
+    encode_prow_kernel<F, KC><<<(unsigned)grid, kPrThreads, smem, st>>>(p);
     return launch_status();
+}
+
+// product-row kernel with 64 (path 6), 32 (path 9) or 16 (path 10) coded packets per CTA
+template <int F>
+static int launch_prow_kc(int path, const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M,
+                          size_t batch, cudaStream_t st)
+{
+    if (path == 10) return launch_prow<F, 16>(A, C, B, N, K, M, batch, st);
+    if (path == 9) return launch_prow<F, 32>(A, C, B, N, K, M, batch, st);
+    return launch_prow<F, 64>(A, C, B, N, K, M, batch, st);
 }
 
 template <int F, int KT, int V>
@@ -421,7 +431,7 @@ static int encode_path_override()
 
 // 0 column (words), 1 column (bytes), 2 lane-k KG=1, 3 lane-k KG=2,
 // 4 fused KG=1, 5 fused KG=2, 6 product-row, 7 persistent lane-k (GF(2)/GF(4), K <= 32),
-// 8 streaming (K <= 4, word-aligned packets).  The fused kernel (lane-k + column warps on one
+// 8 streaming (K <= 4, word-aligned packets), 9 / 10 product-row with 32 / 16 coded packets per CTA.  The fused kernel (lane-k + column warps on one
 // tile) is correct but measured slower than lane-k alone (per-step barrier
 // coupling of the two roles): opt-in via GFRLNC_ENCODE_PATH=fused.
 static bool lanek2_default()
@@ -437,10 +447,13 @@ static int encode_path(int field, int N, int K, size_t M, const void *A, const v
     const int ov = encode_path_override();
     if (!aligned) return 1;
     if (K <= 4 && (ov == 6 || ov == 0)) return 8;                // streaming (16- or 4-byte chunks)
-    if (ov == 1 || (ov == 0 && K < 24)) return 0;
+    if (ov == 1 || (ov == 0 && K < 24 && !(field >= 16 && K > 8))) return 0;
     const int kg2 = K > 32 ? 1 : 0;      // (K > 64 uses 128 coded packets per CTA)
     if (ov == 3) return 4 + kg2;
-    if ((ov == 4 || (ov == 0 && field >= 16 && K > 32))) return 6;
+    // product rows for GF(16)/GF(256) from K = 9 on (measured: tools/exp_shapes.py),
+    // with 16, 32 or 64 coded packets per CTA so that few lanes idle
+    const int prow = K <= 16 ? 10 : K <= 32 ? 9 : 6;
+    if (ov == 4 || (ov == 0 && field >= 16 && K > 8)) return prow;
     if (field <= 4 && K <= 32 && (ov == 5 || (ov == 0 && lanek2_default()))) return 7;
     return 2 + kg2;
 }
@@ -455,12 +468,12 @@ static int encode_on_stream(int field, int fi, const uint8_t *A, const uint8_t *
             return field == 2 ? launch_lanek2<2>(A, C, B, N, K, M, batch, st)
                               : launch_lanek2<4>(A, C, B, N, K, M, batch, st);
         }
-        if (path >= 6) {
+        if (path == 6 || path == 9 || path == 10) {
             switch (field) {
-            case 256: return launch_prow<256>(A, C, B, N, K, M, batch, st);
-            case 16: return launch_prow<16>(A, C, B, N, K, M, batch, st);
-            case 4: return launch_prow<4>(A, C, B, N, K, M, batch, st);
-            case 2: return launch_prow<2>(A, C, B, N, K, M, batch, st);
+            case 256: return launch_prow_kc<256>(path, A, C, B, N, K, M, batch, st);
+            case 16: return launch_prow_kc<16>(path, A, C, B, N, K, M, batch, st);
+            case 4: return launch_prow_kc<4>(path, A, C, B, N, K, M, batch, st);
+            case 2: return launch_prow_kc<2>(path, A, C, B, N, K, M, batch, st);
             default: return GF_EFIELD;
             }
         }

@@ -81,7 +81,7 @@ def version() -> int:
 
 
 ENCODE_PATHS = {0: "column-words", 1: "column-bytes", 2: "lanek-32", 3: "lanek-64", 4: "fused-32",
-                5: "fused-64", 6: "prow", 7: "lanek2", 8: "stream"}
+                5: "fused-64", 6: "prow", 7: "lanek2", 8: "stream", 9: "prow-32", 10: "prow-16"}
 
 
 FORCE_PATHS = {"auto": 0, "column": 1, "lanek": 2, "fused": 3, "prow": 4, "lanek2": 5, "stream": 6}

@@ -197,7 +197,10 @@ def test_encode_path_query():
     assert gf.encode_path(256, 64, 64, 1500) == "prow"          # C3
     assert gf.encode_path(16, 64, 64, 1500) == "prow"
     assert gf.encode_path(256, 256, 256, 65536) == "prow"       # C4
-    assert gf.encode_path(256, 64, 32, 1500) == "lanek-32"
+    assert gf.encode_path(256, 64, 32, 1500) == "prow-32"
+    assert gf.encode_path(16, 32, 16, 1500) == "prow-16"
+    assert gf.encode_path(256, 16, 8, 1500) == "column-words"
+    assert gf.encode_path(4, 32, 32, 1500) == "lanek-32"
     assert gf.encode_path(4, 64, 64, 1500) == "lanek-64"
     assert gf.encode_path(2, 32, 32, 1 << 20) == "lanek-32"     # C5
     assert gf.encode_path(256, 16, 1, 1024) == "stream"         # NEXT-2 (paper: N = 16, K = 1)

@@ -27,7 +27,8 @@ else:
     cases = [(q, s) for q in (2, 4, 16, 256) for s in ((17, 33, 1500, 3), (64, 64, 1500, 2), (32, 32, 4100, 2),
                                                        (5, 24, 400, 3), (33, 96, 3000, 2), (7, 65, 1540, 2))]
     if want == "prow":     # one-step tiles (N <= 4), a single coded packet, many small tiles
-        cases += [(q, s) for q in (16, 256) for s in ((1, 64, 1500, 5), (3, 1, 1536, 9), (4, 70, 4, 400))]
+        cases += [(q, s) for q in (16, 256) for s in ((1, 64, 1500, 5), (3, 1, 1536, 9), (4, 70, 4, 400),
+                                                     (19, 12, 1500, 3), (16, 16, 16384, 2), (40, 9, 388, 7))]
 for q, (N, K, M, batch) in cases:
     gf.init(q)
     A = si.random_bytes(7 + N, 1, 0, batch * N * M).reshape(batch, N, M)
