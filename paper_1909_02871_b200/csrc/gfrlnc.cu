@@ -24,7 +24,7 @@
 namespace gfr {
 
 constexpr int kMaxDevices = 64;
-constexpr int kVersion = 134;   // 0.1.34: + streaming kernel (K <= 4), producer poll back-off
+constexpr int kVersion = 135;   // 0.1.35: + product-row with 16 / 32 coded packets per CTA, streaming on word-aligned packets
 
 __device__ uint32_t g_dev_tabs[4][256 * kTableWords];
 __device__ uint8_t g_dev_inv[4][256];

@@ -14,7 +14,8 @@ from paper_1909_02871_b200 import gf  # noqa: E402
 
 SHAPES = [(16, 8, 1500), (16, 12, 1500), (16, 16, 1500), (32, 16, 1500), (32, 32, 1500), (64, 32, 1500),
           (16, 16, 16384), (64, 64, 1500)]
-for q in (16, 256):
+FIELDS = [int(x) for x in sys.argv[1].split(',')] if len(sys.argv) > 1 else [16, 256]
+for q in FIELDS:
     gf.init(q)
     for (N, K, M) in SHAPES:
         G = max(1, int(4e9 // (N * M)))
