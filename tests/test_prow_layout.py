@@ -94,26 +94,48 @@ def test_gather_address_is_one_prmt():
             assert prmt(aw, col, 0x5504 | (j << 4)) == ((aw >> (8 * j)) & 0xFF) * 256 + col
 
 
-def test_quarter_warp_bank_slots_distinct_for_any_data():
-    """Lane (qw, jw, kc) at sub-step t reads row a (data) of the 256-B-row table
-    at column ((jw + t) & 3) * 64 + kc * 16: the 16-B bank slot (address / 16
-    mod 8) of the 8 lanes of a quarter-warp is distinct whatever the rows are."""
-    rng = np.random.default_rng(2)
-    for t in range(4):
-        for q8 in range(4):
-            for _ in range(200):
-                slots = set()
-                for ql in range(8):
-                    jw, kc = ql >> 2, ql & 3
-                    a = int(rng.integers(0, 256))
-                    addr = 0x1000 + a * 256 + ((jw + t) & 3) * 64 + kc * 16
-                    slots.add((addr // 16) % 8)
-                assert len(slots) == 8
+@pytest.mark.parametrize("KC", (64, 32, 16))
+def test_quarter_warp_bank_slots_distinct_for_any_data(KC):
+    """PrCfg<KC>: S = 256/KC sources per step, NKC = KC/16 chunks, lane (jw, kc)
+    = (ql / NKC, ql % NKC) of a quarter-warp reads row a (data) of the 256-B-row
+    table at column ((jw + t) mod S) * KC + kc * 16 at sub-step t: the 16-B bank
+    slot (address / 16 mod 8) of the 8 lanes is distinct whatever the rows are."""
+    S, NKC = 256 // KC, KC // 16
+    rng = np.random.default_rng(KC)
+    for t in range(S):
+        for _ in range(200):
+            slots = set()
+            for ql in range(8):
+                jw, kc = ql // NKC, ql % NKC
+                a = int(rng.integers(0, 256))
+                addr = 0x1000 + a * 256 + ((jw + t) % S) * KC + kc * 16
+                slots.add((addr // 16) % 8)
+            assert len(slots) == 8
 
 
-def test_sub_steps_cover_every_source_once():
-    for jw in range(2):
-        assert sorted((jw + t) & 3 for t in range(4)) == [0, 1, 2, 3]
+@pytest.mark.parametrize("KC", (64, 32, 16))
+def test_sub_steps_cover_every_source_once(KC):
+    S, NKC = 256 // KC, KC // 16
+    for jw in range(8 // NKC):
+        assert sorted((jw + t) % S for t in range(S)) == list(range(S))
+
+
+@pytest.mark.parametrize("KC", (64, 32, 16))
+def test_tile_geometry(KC):
+    """Every (word, coefficient chunk) of a 384-word tile x KC coded packets is
+    owned by exactly one (gatherer warp, lane, item): 12 warps, R items."""
+    NKC, WQ = KC // 16, 8 // (KC // 16)
+    WPW, GW, TW = 4 * WQ, 12, 384
+    R = TW // (GW * WPW)
+    owned = set()
+    for warp in range(GW):
+        for lane in range(32):
+            qw, ql = lane >> 3, lane & 7
+            jw, kc = ql // NKC, ql % NKC
+            wbase = warp * WPW + qw * WQ + jw
+            for r in range(R):
+                owned.add((wbase + GW * WPW * r, kc))
+    assert owned == {(w, c) for w in range(TW) for c in range(NKC)}
 
 
 def test_writeback_transpose():
