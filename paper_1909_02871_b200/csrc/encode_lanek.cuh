@@ -48,14 +48,17 @@ constexpr int kLkBuildWarps = 4;
 constexpr int kLkSteps = 4;               // cp.async ring depth in steps
 constexpr int kLkNQ = 3;                  // Q buffers between builders and gatherers
 
-template <int KG> struct LkGeom {
-    static constexpr int WT = KG == 1 ? 32 : 48;          // words per gatherer lane
+// WIDE (GF(2) with KG = 1): 64 words per gatherer lane, two CTAs per SM
+// (C5 GF(2): 1649 vs 1610 GB/s with 32 words and three CTAs; GF(4) is the
+// other way round: 1047 vs 1093)
+template <int KG, bool WIDE = false> struct LkGeom {
+    static constexpr int WT = KG == 1 ? (WIDE ? 64 : 32) : 48;   // words per gatherer lane
     static constexpr int WG = KG == 4 ? 4 : kLkWG;        // word groups
     static constexpr int TW = WT * WG;                    // words per tile
     static constexpr int QS = TW + 1;                     // Q row stride (odd)
     static constexpr int BWORDS = (TW + 32 * kLkBuildWarps - 1) / (32 * kLkBuildWarps);
     static constexpr int THREADS = 32 * (KG * WG + kLkBuildWarps);
-    static constexpr int MINB = KG == 1 ? 3 : 1;          // CTAs per SM targeted
+    static constexpr int MINB = KG == 1 ? (WIDE ? 2 : 3) : 1;   // CTAs per SM targeted
 };
 
 struct LanekParams {
@@ -143,10 +146,11 @@ __device__ __forceinline__ void build_word(uint32_t *q, const uint32_t (&a)[LkFi
 }
 
 template <int F, int KG>
-__global__ void __launch_bounds__(LkGeom<KG>::THREADS, LkGeom<KG>::MINB) encode_lanek_kernel(LanekParams p)
+__global__ void __launch_bounds__(LkGeom<KG, F == 2 && KG == 1>::THREADS, LkGeom<KG, F == 2 && KG == 1>::MINB)
+encode_lanek_kernel(LanekParams p)
 {
     using L = LkField<F>;
-    using G = LkGeom<KG>;
+    using G = LkGeom<KG, F == 2 && KG == 1>;
     constexpr int SG = L::kSG;
     constexpr int WT = G::WT, TW = G::TW, QS = G::QS;
     constexpr int KTL = 32 * KG;                               // coded packets per CTA
@@ -318,7 +322,7 @@ __global__ void __launch_bounds__(LkGeom<KG>::THREADS, LkGeom<KG>::MINB) encode_
 template <int F, int KG>
 __host__ __device__ constexpr size_t lk_smem_bytes(int N)
 {
-    using G = LkGeom<KG>;
+    using G = LkGeom<KG, F == 2 && KG == 1>;
     return (size_t)kLkNQ * LkField<F>::kRows * G::QS * 4 +
            (size_t)32 * KG * ((N + LkField<F>::kSG - 1) / LkField<F>::kSG);
 }

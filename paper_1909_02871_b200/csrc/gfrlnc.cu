@@ -215,7 +215,7 @@ template <int F, int KG>
 static int launch_lanek(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M,
                         size_t batch, cudaStream_t st)
 {
-    using G = LkGeom<KG>;
+    using G = LkGeom<KG, F == 2 && KG == 1>;
     LanekParams p{};
     p.A = A; p.C = C; p.B = B; p.M = M; p.Mw = (uint32_t)(M / 4); p.batch = batch;
     p.N = N; p.K = K; p.qmask = F - 1;
