@@ -320,8 +320,11 @@ def test_next2_full_size_sampled(gfm, q):
 
 
 @pytest.mark.parametrize("q", (4, 256))
-def test_encode_host_path(gfm, q):
-    batch, N, K, M = 37, 16, 8, 1500
+@pytest.mark.parametrize("shape", ((37, 16, 8, 1500), (29, 64, 64, 1500), (11, 32, 32, 4096)))
+def test_encode_host_path(gfm, q, shape):
+    """gf_encode_batch_host (pinned host buffers, chunked pipeline) through the
+    column, product-row and lane-k / product-row-32 kernels."""
+    batch, N, K, M = shape
     A = si.random_bytes(91, 1, 0, batch * N * M).reshape(batch, N, M)
     C = si.uniform_coeffs(q, 92, 2, 0, batch * N * K).reshape(batch, N, K)
     Ah = torch.from_numpy(A).pin_memory()
