@@ -24,7 +24,7 @@
 namespace gfr {
 
 constexpr int kMaxDevices = 64;
-constexpr int kVersion = 135;   // 0.1.35: + product-row with 16 / 32 coded packets per CTA, streaming on word-aligned packets
+constexpr int kVersion = 136;   // 0.1.36: + wide lane-k for GF(2)
 
 __device__ uint32_t g_dev_tabs[4][256 * kTableWords];
 __device__ uint8_t g_dev_inv[4][256];
