@@ -126,6 +126,92 @@ __global__ void __launch_bounds__(256) invert_kernel(InvertParams p)
     if (tid == 0 && p.rank) p.rank[g] = rank;
 }
 
+// ---- warp-per-matrix inversion for N <= 64 (the C3 decode shape) ----------
+// One warp owns one generation's augmented matrix [C | I] (N rows x RW words,
+// row stride RW + 1 so that the 32 rows a warp touches per word sit in 32
+// banks); no CTA-wide barrier at all -- the CTA version above pays five
+// __syncthreads per column.  Per column: pivot by two ballots (lane l holds
+// rows l and l + 32), row swap + scaling with one word per lane, then each
+// lane eliminates its own rows word by word with the split tables of its
+// row's factor (loaded once per column).  Eight matrices per CTA share the
+// field tables.
+constexpr int kInvWarps = 8;
+
+__global__ void __launch_bounds__(32 * kInvWarps) invert_warp_kernel(InvertParams p)
+{
+    extern __shared__ __align__(16) uint32_t smem[];
+    const int N = p.N;
+    const int RW = (2 * N + 3) / 4;                   // words per augmented row
+    const int RS = RW + 1;                            // row stride (odd: conflict-free column access)
+    uint32_t *stab = smem;                            // [256][8]
+    uint8_t *sinv = reinterpret_cast<uint8_t *>(stab + 256 * 8);
+    uint32_t *Mall = stab + 256 * 8 + 64;             // [warps][N][RS]
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    for (int e = tid; e < 256 * 8; e += blockDim.x) {
+        const int c = e >> 3, j = e & 7;
+        stab[e] = j < 5 ? __ldg(p.tabs + (size_t)c * 16u + j) : 0u;
+    }
+    for (int e = tid; e < 256; e += blockDim.x) sinv[e] = __ldg(p.inv + e);
+    const size_t g = (size_t)blockIdx.x * kInvWarps + warp;
+    const bool live = g < p.batch;
+    uint32_t *Mx = Mall + (size_t)warp * N * RS;
+    uint8_t *Mb = reinterpret_cast<uint8_t *>(Mx);
+    if (live) {
+        const uint8_t *Cg = p.C + g * (size_t)N * N;
+        for (int e = lane; e < N * RW * 4; e += 32) {
+            const int r = e / (RW * 4), c = e - r * RW * 4;
+            uint8_t v = 0;
+            if (c < N) v = Cg[(size_t)r * N + c] & (uint8_t)p.qmask;
+            else if (c < 2 * N) v = (c - N == r) ? 1 : 0;
+            Mb[(size_t)r * RS * 4 + c] = v;
+        }
+    }
+    __syncthreads();                                  // tables ready
+    if (!live) return;
+    __syncwarp();
+
+    const int ra = lane, rb = lane + 32;              // this lane's rows
+    int rank = 0;
+    for (int col = 0; col < N; col++) {
+        const int cw = col >> 2;                      // word of the column
+        // pivot: first row >= rank with a nonzero entry in this column
+        const bool ha = ra < N && ra >= rank && Mb[(size_t)ra * RS * 4 + col] != 0;
+        const bool hb = rb < N && rb >= rank && Mb[(size_t)rb * RS * 4 + col] != 0;
+        const uint32_t ba = __ballot_sync(0xffffffffu, ha), bb = __ballot_sync(0xffffffffu, hb);
+        if ((ba | bb) == 0u) continue;                // rank deficient column
+        const int piv = ba ? __ffs(ba) - 1 : 32 + __ffs(bb) - 1;
+        // swap the pivot row into place and scale it by the pivot's inverse
+        const uint32_t pv = Mb[(size_t)piv * RS * 4 + col];
+        __syncwarp();
+        if (lane >= cw && lane < RW) {
+            const uint32_t a = Mx[(size_t)piv * RS + lane], b = Mx[(size_t)rank * RS + lane];
+            Mx[(size_t)piv * RS + lane] = b;
+            Mx[(size_t)rank * RS + lane] = mul_word(tab_of(stab, sinv[pv]), a);
+        }
+        __syncwarp();
+        // eliminate: each lane its rows, word by word, with its row factor's tables
+        const uint32_t *prow = Mx + (size_t)rank * RS;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int r = h ? rb : ra;
+            if (r >= N || r == rank) continue;
+            const uint32_t f = Mb[(size_t)r * RS * 4 + col];
+            if (f == 0) continue;
+            const PrmtTab T = tab_of(stab, f);
+            uint32_t *row = Mx + (size_t)r * RS;
+            for (int w = cw; w < RW; w++) row[w] ^= mul_word(T, prow[w]);
+        }
+        __syncwarp();
+        rank++;
+    }
+    uint8_t *Dg = p.D + g * (size_t)N * N;
+    for (int e = lane; e < N * N; e += 32) {
+        const int r = e / N, c = e - r * N;
+        Dg[e] = Mb[(size_t)r * RS * 4 + N + c];
+    }
+    if (lane == 0 && p.rank) p.rank[g] = rank;
+}
+
 }  // namespace gfr
 
 namespace gfr {

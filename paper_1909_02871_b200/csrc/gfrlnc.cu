@@ -767,6 +767,15 @@ int gf_invert_batch(int field, const uint8_t *C, uint8_t *D, int *rank, int N, s
     p.tabs = reinterpret_cast<const uint32_t *>(tabs) + (size_t)fi * 256 * kTableWords;
     p.inv = reinterpret_cast<const uint8_t *>(inv) + (size_t)fi * 256;
     const size_t rw = (2 * (size_t)N + 3) / 4;
+    if (N <= 64) {                                            // warp per matrix (no CTA barriers)
+        const size_t smem_w = (256 * 8 + 64) * 4 + (size_t)kInvWarps * N * (rw + 1) * 4;
+        if (cudaFuncSetAttribute(invert_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem_w) != cudaSuccess)
+            return GF_ECUDA;
+        invert_warp_kernel<<<(unsigned)((batch + kInvWarps - 1) / kInvWarps), 32 * kInvWarps, smem_w,
+                             tls_stream>>>(p);
+        return launch_status();
+    }
     const size_t smem = (size_t)N * rw * 4 + 256 * 8 * 4 + 256;
     if (cudaFuncSetAttribute(invert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
