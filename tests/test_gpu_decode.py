@@ -32,7 +32,7 @@ def mat_mul(q, X, Y):
 
 
 @pytest.mark.parametrize("q", FIELDS)
-@pytest.mark.parametrize("N", [1, 5, 16, 33, 64])
+@pytest.mark.parametrize("N", [1, 5, 16, 33, 64, 65, 130])
 def test_invert_batch(gfm, q, N):
     batch = 24
     C = si.uniform_coeffs(q, 100 + N, 2, 0, batch * N * N).reshape(batch, N, N)
