@@ -137,19 +137,27 @@ __global__ void __launch_bounds__(256) invert_kernel(InvertParams p)
 // field tables.
 constexpr int kInvWarps = 8;
 
+__device__ __forceinline__ PrmtTab tab5_of(const uint32_t *stab, uint32_t c)
+{
+    const uint32_t *t = stab + c * 5u;
+    PrmtTab T;
+    T.t0lo = t[0]; T.t0hi = t[1]; T.t1lo = t[2]; T.t1hi = t[3]; T.t2 = t[4];
+    return T;
+}
+
 __global__ void __launch_bounds__(32 * kInvWarps) invert_warp_kernel(InvertParams p)
 {
     extern __shared__ __align__(16) uint32_t smem[];
     const int N = p.N;
     const int RW = (2 * N + 3) / 4;                   // words per augmented row
     const int RS = RW + 1;                            // row stride (odd: conflict-free column access)
-    uint32_t *stab = smem;                            // [256][8]
-    uint8_t *sinv = reinterpret_cast<uint8_t *>(stab + 256 * 8);
-    uint32_t *Mall = stab + 256 * 8 + 64;             // [warps][N][RS]
+    uint32_t *stab = smem;                            // [256][5]: T0lo,T0hi,T1lo,T1hi,T2
+    uint8_t *sinv = reinterpret_cast<uint8_t *>(stab + 256 * 5);
+    uint32_t *Mall = stab + 256 * 5 + 64;             // [warps][N][RS]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    for (int e = tid; e < 256 * 8; e += blockDim.x) {
-        const int c = e >> 3, j = e & 7;
-        stab[e] = j < 5 ? __ldg(p.tabs + (size_t)c * 16u + j) : 0u;
+    for (int e = tid; e < 256 * 5; e += blockDim.x) {
+        const int c = e / 5, j = e - c * 5;
+        stab[e] = __ldg(p.tabs + (size_t)c * 16u + j);
     }
     for (int e = tid; e < 256; e += blockDim.x) sinv[e] = __ldg(p.inv + e);
     const size_t g = (size_t)blockIdx.x * kInvWarps + warp;
@@ -186,7 +194,7 @@ __global__ void __launch_bounds__(32 * kInvWarps) invert_warp_kernel(InvertParam
         if (lane >= cw && lane < RW) {
             const uint32_t a = Mx[(size_t)piv * RS + lane], b = Mx[(size_t)rank * RS + lane];
             Mx[(size_t)piv * RS + lane] = b;
-            Mx[(size_t)rank * RS + lane] = mul_word(tab_of(stab, sinv[pv]), a);
+            Mx[(size_t)rank * RS + lane] = mul_word(tab5_of(stab, sinv[pv]), a);
         }
         __syncwarp();
         // eliminate: each lane its rows, word by word, with its row factor's tables
@@ -197,9 +205,15 @@ __global__ void __launch_bounds__(32 * kInvWarps) invert_warp_kernel(InvertParam
             if (r >= N || r == rank) continue;
             const uint32_t f = Mb[(size_t)r * RS * 4 + col];
             if (f == 0) continue;
-            const PrmtTab T = tab_of(stab, f);
+            const PrmtTab T = tab5_of(stab, f);
             uint32_t *row = Mx + (size_t)r * RS;
-            for (int w = cw; w < RW; w++) row[w] ^= mul_word(T, prow[w]);
+            int w = cw;
+            for (; w + 1 < RW; w += 2) {                  // two words in flight
+                const uint32_t p0 = prow[w], p1 = prow[w + 1], q0 = row[w], q1 = row[w + 1];
+                row[w] = q0 ^ mul_word(T, p0);
+                row[w + 1] = q1 ^ mul_word(T, p1);
+            }
+            if (w < RW) row[w] ^= mul_word(T, prow[w]);
         }
         __syncwarp();
         rank++;
