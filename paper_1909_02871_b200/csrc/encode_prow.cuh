@@ -101,21 +101,6 @@ template <int F> __device__ __forceinline__ uint32_t pr_xtime(uint32_t a)
     else return a;
 }
 
-// P[2^b] for 4 coefficients c (one per byte, c < q): slot j = b / w of each
-// byte holds c * x^(b mod w) -- the packed product of c with the byte 1 << b.
-template <int F> __device__ __forceinline__ uint32_t pr_basis(uint32_t c, int b)
-{
-    constexpr int w = F == 256 ? 8 : F == 16 ? 4 : F == 4 ? 2 : 1;
-    const int j = b / w, e = b - j * w;
-    uint32_t v = c;
-#pragma unroll
-    for (int u = 0; u < w - 1; u++) {
-        const uint32_t nv = pr_xtime<F>(v);
-        v = u < e ? nv : v;
-    }
-    return v << (j * w);
-}
-
 __device__ __forceinline__ void sts128(uint32_t a, uint4 v)
 {
     asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" :: "r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
