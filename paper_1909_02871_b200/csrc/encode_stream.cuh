@@ -17,11 +17,15 @@
 //   GF(2):   acc ^= a & M0                                 1 LOP3
 //   GF(4):   the paper's imul (Alg. 2): 2 IMAD + 1 LOP3
 //            (a & 0x55..)*c ^ ((a>>1) & 0x55..)*(x c)
-//   GF(16):  imul on the four nibble bit planes: 4 IMAD + 2 LOP3
+//   GF(16):  imul on the four nibble bit planes: 4 IMAD + 3 IMAD.HI (FMA
+//            pipe) + 4 AND + 1 LOP3 (measured 2-4% faster than the PRMT form
+//            below with GF(16) tables, which the same kernel also supports)
 //   GF(256): three byte-permute split tables over bit groups {0-2}, {3-5},
-//            {6-7} (Alg. 1's shuffle): 3 PRMT + 3 AND +
-//            2 LOP3 on the ALU pipe, selector packing on the FMA pipe;
-//            results in PRMT byte order, un-permuted once per output word.
+//            {6-7} (Alg. 1's shuffle): 3 AND + 3 PRMT + 1
+//            LOP3 on the ALU pipe, 3 IMAD.HI (selector packing) on the FMA
+//            pipe; results in PRMT byte order, un-permuted once per output word.
+// Products of two sources are folded into an accumulator with one 3-input
+// XOR (LOP3): 7.5 ALU operations per source word for GF(256).
 // Grid-stride over (generation, chunk); packets of 512 B or more give
 // warp-uniform coefficients (broadcast table loads).
 #pragma once
@@ -33,6 +37,7 @@
 namespace gfr {
 
 constexpr int kStThreads = 256;
+
 
 struct StreamParams {
     const uint8_t *A;
@@ -53,16 +58,19 @@ __device__ __forceinline__ uint4 st_ld_stream(const uint4 *p)
     return v;
 }
 
-// acc ^= c * x for one 32-bit word, e = the coefficient's table entry
+// c * x for one 32-bit word, e = the coefficient's table entry.  kBatch =
+// source chunks loaded together (measured), even.
 template <int F> struct StreamOp;
 template <> struct StreamOp<2> {
     static constexpr bool kPermuted = false;
+    static constexpr int kBatch = 8;
     struct E { uint32_t m0; };
     __device__ __forceinline__ static E entry(const uint32_t *t) { return E{__ldg(t + 5)}; }
     __device__ __forceinline__ static uint32_t mul(uint32_t x, const E &e) { return x & e.m0; }
 };
 template <> struct StreamOp<4> {
     static constexpr bool kPermuted = false;
+    static constexpr int kBatch = 8;
     struct E { uint32_t p0, p1; };
     __device__ __forceinline__ static E entry(const uint32_t *t)
     {
@@ -74,8 +82,9 @@ template <> struct StreamOp<4> {
         return ((x & 0x55555555u) * e.p0) ^ ((mul_hi(x, 1u << 31) & 0x55555555u) * e.p1);
     }
 };
-template <> struct StreamOp<16> {
+struct StreamImul16 {      // GF(16) imul on the nibble bit planes
     static constexpr bool kPermuted = false;
+    static constexpr int kBatch = 4;
     struct E { uint32_t p0, p1, p2, p3; };
     __device__ __forceinline__ static E entry(const uint32_t *t)
     {
@@ -89,8 +98,9 @@ template <> struct StreamOp<16> {
         return (n0 * e.p0) ^ (n1 * e.p1) ^ (n2 * e.p2) ^ (n3 * e.p3);
     }
 };
-template <> struct StreamOp<256> {
+struct StreamPrmt {        // split-table PRMT lookups (GF(16), GF(256))
     static constexpr bool kPermuted = true;
+    static constexpr int kBatch = 4;
     struct E { PrmtTab T; };
     __device__ __forceinline__ static E entry(const uint32_t *t)
     {
@@ -99,9 +109,24 @@ template <> struct StreamOp<256> {
         e.T.t0lo = v.x; e.T.t0hi = v.y; e.T.t1lo = v.z; e.T.t1hi = v.w; e.T.t2 = __ldg(t + 4);
         return e;
     }
-    // three split-table PRMTs (bit groups {0-2}, {3-5}, {6-7}): 8 ALU + 5 FMA-pipe ops
     __device__ __forceinline__ static uint32_t mul(uint32_t x, const E &e) { return lookup_perm(e.T, make_sel(x)); }
 };
+template <> struct StreamOp<16> : StreamImul16 {};
+template <> struct StreamOp<256> : StreamPrmt {};      // (StreamPrmt also serves GF(16): tables.cpp)
+
+__device__ __forceinline__ uint32_t st_xor3(uint32_t a, uint32_t b, uint32_t c)
+{
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+// table entry of coefficient C[g][i][k] (0 past the last source: its chunk is 0 too)
+__device__ __forceinline__ const uint32_t *st_tab(const StreamParams &p, const uint8_t *Cg, int i, int k)
+{
+    const uint32_t c = i < p.N ? (__ldg(Cg + (size_t)i * p.K + k) & p.qmask) : 0u;
+    return p.tabs + (size_t)c * kTableWords;
+}
 
 // generic V-word chunks; used with V = 1 (4-byte chunks) for packets that are
 // only word aligned (e.g. C1's M = 1500)
@@ -122,11 +147,10 @@ template <int V> __device__ __forceinline__ void st_store(uint8_t *p, const uint
 
 // 16-byte chunks (packets 16-byte aligned): the measured fast form, kept as
 // written for uint4 (a generic word-array version of it measured 2-6% slower)
-template <int F, int KT>
+template <class Op, int KT>
 __global__ void __launch_bounds__(kStThreads) encode_stream_kernel(StreamParams p)
 {
-    using Op = StreamOp<F>;
-    constexpr int kStBatch = F <= 4 ? 8 : 4;                  // source chunks loaded together (measured)
+    constexpr int kStBatch = Op::kBatch;
     const size_t stride = (size_t)gridDim.x * kStThreads;
     for (size_t t = (size_t)blockIdx.x * kStThreads + threadIdx.x; t < p.total; t += stride) {
         const size_t g = t / p.M16, ch = t - g * p.M16;
@@ -141,17 +165,17 @@ __global__ void __launch_bounds__(kStThreads) encode_stream_kernel(StreamParams 
             for (int b = 0; b < kStBatch; b++)
                 a[b] = i0 + b < p.N ? st_ld_stream(Ag + (size_t)(i0 + b) * p.M16) : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-            for (int b = 0; b < kStBatch; b++) {
+            for (int b = 0; b < kStBatch; b += 2) {
                 if (i0 + b >= p.N) break;
 #pragma unroll
                 for (int k = 0; k < KT; k++) {
                     if (k < p.K) {
-                        const uint32_t c = __ldg(Cg + (size_t)(i0 + b) * p.K + k) & p.qmask;
-                        const typename Op::E e = Op::entry(p.tabs + (size_t)c * kTableWords);
-                        acc[k].x ^= Op::mul(a[b].x, e);
-                        acc[k].y ^= Op::mul(a[b].y, e);
-                        acc[k].z ^= Op::mul(a[b].z, e);
-                        acc[k].w ^= Op::mul(a[b].w, e);
+                        const typename Op::E e0 = Op::entry(st_tab(p, Cg, i0 + b, k));
+                        const typename Op::E e1 = Op::entry(st_tab(p, Cg, i0 + b + 1, k));
+                        acc[k].x = st_xor3(acc[k].x, Op::mul(a[b].x, e0), Op::mul(a[b + 1].x, e1));
+                        acc[k].y = st_xor3(acc[k].y, Op::mul(a[b].y, e0), Op::mul(a[b + 1].y, e1));
+                        acc[k].z = st_xor3(acc[k].z, Op::mul(a[b].z, e0), Op::mul(a[b + 1].z, e1));
+                        acc[k].w = st_xor3(acc[k].w, Op::mul(a[b].w, e0), Op::mul(a[b + 1].w, e1));
                     }
                 }
             }
@@ -168,11 +192,10 @@ __global__ void __launch_bounds__(kStThreads) encode_stream_kernel(StreamParams 
     }
 }
 
-template <int F, int KT, int V>
+template <class Op, int KT, int V>
 __global__ void __launch_bounds__(kStThreads) encode_stream_words_kernel(StreamParams p)
 {
-    using Op = StreamOp<F>;
-    constexpr int kStBatch = F <= 4 ? 8 : 4;                  // source chunks loaded together (measured)
+    constexpr int kStBatch = Op::kBatch;
     constexpr size_t kChunk = 4 * V;                           // bytes per chunk
     const size_t Mc = p.M16;                                   // chunks per packet
     const size_t M = Mc * kChunk;
@@ -196,15 +219,16 @@ __global__ void __launch_bounds__(kStThreads) encode_stream_words_kernel(StreamP
                     for (int v = 0; v < V; v++) a[b][v] = 0u;
             }
 #pragma unroll
-            for (int b = 0; b < kStBatch; b++) {
+            for (int b = 0; b < kStBatch; b += 2) {
                 if (i0 + b >= p.N) break;
 #pragma unroll
                 for (int k = 0; k < KT; k++) {
                     if (k < p.K) {
-                        const uint32_t c = __ldg(Cg + (size_t)(i0 + b) * p.K + k) & p.qmask;
-                        const typename Op::E e = Op::entry(p.tabs + (size_t)c * kTableWords);
+                        const typename Op::E e0 = Op::entry(st_tab(p, Cg, i0 + b, k));
+                        const typename Op::E e1 = Op::entry(st_tab(p, Cg, i0 + b + 1, k));
 #pragma unroll
-                        for (int v = 0; v < V; v++) acc[k][v] ^= Op::mul(a[b][v], e);
+                        for (int v = 0; v < V; v++)
+                            acc[k][v] = st_xor3(acc[k][v], Op::mul(a[b][v], e0), Op::mul(a[b + 1][v], e1));
                     }
                 }
             }

@@ -8,11 +8,11 @@
 // products of 4 bytes at once.  Selector nibble 3 must stay clear (it means
 // "replicate the sign bit"), which the masks 0x07 / 0x03 guarantee.
 //
-// Selector packing: t = (x >> s) & 0x07070707 holds the 4 indices in byte
-// positions; t | (t >> 12) moves them into the four low nibbles in the order
+// Selector packing: the indices of bit group g sit at 3-bit fields in byte
+// positions; the four low nibbles of the selector must hold them in the order
 // [b0, b2, b1, b3], so every lookup result is in that byte order.  Results
 // are XOR-accumulated in permuted order and un-permuted once at the end with
-// prmt(y, y, 0x3120).
+// prmt(y, y, 0x3120).  One AND and one IMAD.HI per group (make_sel).
 #pragma once
 #include <cstdint>
 
@@ -50,16 +50,27 @@ __device__ __forceinline__ uint32_t mul_hi(uint32_t a, uint32_t b)
     return d;
 }
 
+// Selector multipliers, read from the constant bank: ptxas strength-reduces a
+// multiply by a known power of two into SHF / LEA.HI on the ALU pipe (the pipe
+// the PRMTs and XORs need), but must issue IMAD.HI (FMA pipe) for a value it
+// cannot see.  Never written after load.
+__constant__ uint32_t c_selmul[3] = {1u << 20, (1u << 29) | (1u << 17), (1u << 26) | (1u << 14)};
+
 __device__ __forceinline__ Sel make_sel(uint32_t x)
 {
-    // t | (t >> 12) == t + (t >> 12) (disjoint bits) == mad.hi(t, 2^20, t)
-    const uint32_t t0 = x & 0x07070707u;
-    const uint32_t t1 = mul_hi(x, 1u << 29) & 0x07070707u;   // (x >> 3) & ..
-    const uint32_t t2 = mul_hi(x, 1u << 26) & 0x03030303u;   // (x >> 6) & ..
+    // t0 = x & 0x07..: fields at bits 8j; t0 + (t0 >> 12) = hi(t0 * 2^20) + t0
+    //   adds b2 -> nibble 1 and b3 -> nibble 3 (disjoint bits, so + is |).
+    // t1 = x & 0x38..: hi(t1 * (2^29 + 2^17)) = (t1 >> 3) + (t1 >> 15): every
+    //   bit of t1 is >= 3, so the low word of t1 * 2^29 is 0 and that of
+    //   t1 * 2^17 is < 2^31 -- no carry into the high word.
+    // t2 = x & 0xC0..: hi(t2 * (2^26 + 2^14)) = (t2 >> 6) + (t2 >> 18), same
+    //   argument (bits >= 6).
+    // Nibble bit 3 stays clear in all three (it would mean "replicate sign").
+    const uint32_t t0 = x & 0x07070707u, t1 = x & 0x38383838u, t2 = x & 0xC0C0C0C0u;
     Sel s;
-    s.s0 = mad_hi(t0, 1u << 20, t0);
-    s.s1 = mad_hi(t1, 1u << 20, t1);
-    s.s2 = mad_hi(t2, 1u << 20, t2);
+    s.s0 = mad_hi(t0, c_selmul[0], t0);
+    s.s1 = mul_hi(t1, c_selmul[1]);
+    s.s2 = mul_hi(t2, c_selmul[2]);
     return s;
 }
 

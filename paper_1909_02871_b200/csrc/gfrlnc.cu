@@ -24,7 +24,7 @@
 namespace gfr {
 
 constexpr int kMaxDevices = 64;
-constexpr int kVersion = 136;   // 0.1.36: + wide lane-k for GF(2)
+constexpr int kVersion = 137;   // 0.1.37: selectors on IMAD.HI, paired XOR in the stream kernel
 
 __device__ uint32_t g_dev_tabs[4][256 * kTableWords];
 __device__ uint8_t g_dev_inv[4][256];
@@ -326,7 +326,7 @@ static int launch_prow_kc(int path, const uint8_t *A, const uint8_t *C, uint8_t 
     return launch_prow<F, 64>(A, C, B, N, K, M, batch, st);
 }
 
-template <int F, int KT, int V>
+template <class Op, int KT, int V>
 static int launch_stream_t(const StreamParams &p, cudaStream_t st)
 {
     int dev;
@@ -334,23 +334,23 @@ static int launch_stream_t(const StreamParams &p, cudaStream_t st)
     const size_t sms = (size_t)(g_sm_count[dev] > 0 ? g_sm_count[dev] : 148);
     size_t grid = (p.total + kStThreads - 1) / kStThreads;
     if (grid > sms * 8) grid = sms * 8;                       // grid-stride: 8 CTAs of 256 per SM
-    if constexpr (V == 4) encode_stream_kernel<F, KT><<<(unsigned)grid, kStThreads, 0, st>>>(p);
-    else encode_stream_words_kernel<F, KT, V><<<(unsigned)grid, kStThreads, 0, st>>>(p);
+    if constexpr (V == 4) encode_stream_kernel<Op, KT><<<(unsigned)grid, kStThreads, 0, st>>>(p);
+    else encode_stream_words_kernel<Op, KT, V><<<(unsigned)grid, kStThreads, 0, st>>>(p);
     return launch_status();
 }
 
-template <int F, int V>
+template <class Op, int V>
 static int launch_stream_v(const StreamParams &p, cudaStream_t st)
 {
-    if (p.K == 1) return launch_stream_t<F, 1, V>(p, st);
-    if (p.K == 2) return launch_stream_t<F, 2, V>(p, st);
-    return launch_stream_t<F, 4, V>(p, st);
+    if (p.K == 1) return launch_stream_t<Op, 1, V>(p, st);
+    if (p.K == 2) return launch_stream_t<Op, 2, V>(p, st);
+    return launch_stream_t<Op, 4, V>(p, st);
 }
 
-template <int F>
+template <class Op>
 static int launch_stream_f(const StreamParams &p, bool wide, cudaStream_t st)
 {
-    return wide ? launch_stream_v<F, 4>(p, st) : launch_stream_v<F, 1>(p, st);
+    return wide ? launch_stream_v<Op, 4>(p, st) : launch_stream_v<Op, 1>(p, st);
 }
 
 static int launch_stream(int field, int fi, const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K,
@@ -366,10 +366,10 @@ static int launch_stream(int field, int fi, const uint8_t *A, const uint8_t *C, 
     p.A = A; p.C = C; p.B = B; p.M16 = wide ? M / 16 : M / 4; p.total = batch * p.M16; p.N = N; p.K = K;
     p.qmask = (uint32_t)field - 1u;
     switch (field) {
-    case 2: return launch_stream_f<2>(p, wide, st);
-    case 4: return launch_stream_f<4>(p, wide, st);
-    case 16: return launch_stream_f<16>(p, wide, st);
-    case 256: return launch_stream_f<256>(p, wide, st);
+    case 2: return launch_stream_f<StreamOp<2>>(p, wide, st);
+    case 4: return launch_stream_f<StreamOp<4>>(p, wide, st);
+    case 16: return launch_stream_f<StreamOp<16>>(p, wide, st);
+    case 256: return launch_stream_f<StreamOp<256>>(p, wide, st);
     default: return GF_EFIELD;
     }
 }

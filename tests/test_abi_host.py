@@ -112,6 +112,26 @@ def test_selectors_never_set_sign_mode():
                 assert not (s >> (4 * i)) & 0x8
 
 
+def test_kernel_selector_packing_equals_shift_form():
+    """gf_device.cuh make_sel: one AND + one IMAD.HI per group, multipliers
+    c_selmul = {2^20, 2^29 + 2^17, 2^26 + 2^14} (parsed from the header), equals
+    the shift-and-or selectors above in the 16 bits PRMT reads, for random and
+    extreme words (the no-carry argument of the header comment)."""
+    src = open(os.path.join(ROOT, "paper_1909_02871_b200", "csrc", "gf_device.cuh")).read()
+    m = re.search(r"c_selmul\[3\]\s*=\s*\{([^}]*)\}", src)
+    consts = [eval(e.replace("u", ""), {}) for e in m.group(1).split(",")]
+    assert consts == [1 << 20, (1 << 29) | (1 << 17), (1 << 26) | (1 << 14)]
+    rng = np.random.default_rng(5)
+    x = np.concatenate([rng.integers(0, 2 ** 32, size=1 << 18, dtype=np.uint64),
+                        np.array([0, 0xFFFFFFFF, 0x80808080, 0x7F7F7F7F, 0xC0C0C0C0, 0x38383838], dtype=np.uint64)])
+    t0, t1, t2 = x & 0x07070707, x & 0x38383838, x & 0xC0C0C0C0
+    got = [((t0 * consts[0]) >> 32) + t0, (t1 * consts[1]) >> 32, (t2 * consts[2]) >> 32]
+    want = [((x >> s) & mk) | (((x >> s) & mk) >> 12) for s, mk in ((0, 0x07070707), (3, 0x07070707), (6, 0x03030303))]
+    for g, w in zip(got, want):
+        assert np.array_equal(g & 0xFFFF, w & 0xFFFF)
+        assert not np.any(g & 0x8888)                     # never the sign-replicate mode
+
+
 def gf4_xtime(a):
     hi = (a >> 1) & 0x55555555
     return hi | (((a & 0x55555555) ^ hi) << 1)
