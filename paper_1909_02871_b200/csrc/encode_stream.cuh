@@ -59,10 +59,14 @@ __device__ __forceinline__ uint4 st_ld_stream(const uint4 *p)
 }
 
 // c * x for one 32-bit word, e = the coefficient's table entry.  kBatch =
-// source chunks loaded together (measured), even.
+// source chunks loaded together (measured), even; kPair = fold the products
+// of two sources into the accumulator with one 3-input XOR (PRMT lookups end
+// in an XOR anyway; for the masked / imul forms pairing only raised register
+// use: GF(2) 97% -> 93%, GF(4) 89% -> 86% of HBM on the same box).
 template <int F> struct StreamOp;
 template <> struct StreamOp<2> {
     static constexpr bool kPermuted = false;
+    static constexpr bool kPair = false;
     static constexpr int kBatch = 8;
     struct E { uint32_t m0; };
     __device__ __forceinline__ static E entry(const uint32_t *t) { return E{__ldg(t + 5)}; }
@@ -70,6 +74,7 @@ template <> struct StreamOp<2> {
 };
 template <> struct StreamOp<4> {
     static constexpr bool kPermuted = false;
+    static constexpr bool kPair = false;
     static constexpr int kBatch = 8;
     struct E { uint32_t p0, p1; };
     __device__ __forceinline__ static E entry(const uint32_t *t)
@@ -84,6 +89,7 @@ template <> struct StreamOp<4> {
 };
 struct StreamImul16 {      // GF(16) imul on the nibble bit planes
     static constexpr bool kPermuted = false;
+    static constexpr bool kPair = false;
     static constexpr int kBatch = 4;
     struct E { uint32_t p0, p1, p2, p3; };
     __device__ __forceinline__ static E entry(const uint32_t *t)
@@ -100,6 +106,7 @@ struct StreamImul16 {      // GF(16) imul on the nibble bit planes
 };
 struct StreamPrmt {        // split-table PRMT lookups (GF(16), GF(256))
     static constexpr bool kPermuted = true;
+    static constexpr bool kPair = true;
     static constexpr int kBatch = 4;
     struct E { PrmtTab T; };
     __device__ __forceinline__ static E entry(const uint32_t *t)
@@ -164,18 +171,35 @@ __global__ void __launch_bounds__(kStThreads) encode_stream_kernel(StreamParams 
 #pragma unroll
             for (int b = 0; b < kStBatch; b++)
                 a[b] = i0 + b < p.N ? st_ld_stream(Ag + (size_t)(i0 + b) * p.M16) : make_uint4(0u, 0u, 0u, 0u);
+            if constexpr (Op::kPair) {
 #pragma unroll
-            for (int b = 0; b < kStBatch; b += 2) {
-                if (i0 + b >= p.N) break;
+                for (int b = 0; b < kStBatch; b += 2) {
+                    if (i0 + b >= p.N) break;
 #pragma unroll
-                for (int k = 0; k < KT; k++) {
-                    if (k < p.K) {
-                        const typename Op::E e0 = Op::entry(st_tab(p, Cg, i0 + b, k));
-                        const typename Op::E e1 = Op::entry(st_tab(p, Cg, i0 + b + 1, k));
-                        acc[k].x = st_xor3(acc[k].x, Op::mul(a[b].x, e0), Op::mul(a[b + 1].x, e1));
-                        acc[k].y = st_xor3(acc[k].y, Op::mul(a[b].y, e0), Op::mul(a[b + 1].y, e1));
-                        acc[k].z = st_xor3(acc[k].z, Op::mul(a[b].z, e0), Op::mul(a[b + 1].z, e1));
-                        acc[k].w = st_xor3(acc[k].w, Op::mul(a[b].w, e0), Op::mul(a[b + 1].w, e1));
+                    for (int k = 0; k < KT; k++) {
+                        if (k < p.K) {
+                            const typename Op::E e0 = Op::entry(st_tab(p, Cg, i0 + b, k));
+                            const typename Op::E e1 = Op::entry(st_tab(p, Cg, i0 + b + 1, k));
+                            acc[k].x = st_xor3(acc[k].x, Op::mul(a[b].x, e0), Op::mul(a[b + 1].x, e1));
+                            acc[k].y = st_xor3(acc[k].y, Op::mul(a[b].y, e0), Op::mul(a[b + 1].y, e1));
+                            acc[k].z = st_xor3(acc[k].z, Op::mul(a[b].z, e0), Op::mul(a[b + 1].z, e1));
+                            acc[k].w = st_xor3(acc[k].w, Op::mul(a[b].w, e0), Op::mul(a[b + 1].w, e1));
+                        }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int b = 0; b < kStBatch; b++) {
+                    if (i0 + b >= p.N) break;
+#pragma unroll
+                    for (int k = 0; k < KT; k++) {
+                        if (k < p.K) {
+                            const typename Op::E e = Op::entry(st_tab(p, Cg, i0 + b, k));
+                            acc[k].x ^= Op::mul(a[b].x, e);
+                            acc[k].y ^= Op::mul(a[b].y, e);
+                            acc[k].z ^= Op::mul(a[b].z, e);
+                            acc[k].w ^= Op::mul(a[b].w, e);
+                        }
                     }
                 }
             }
@@ -219,16 +243,21 @@ __global__ void __launch_bounds__(kStThreads) encode_stream_words_kernel(StreamP
                     for (int v = 0; v < V; v++) a[b][v] = 0u;
             }
 #pragma unroll
-            for (int b = 0; b < kStBatch; b += 2) {
+            for (int b = 0; b < kStBatch; b += Op::kPair ? 2 : 1) {
                 if (i0 + b >= p.N) break;
 #pragma unroll
                 for (int k = 0; k < KT; k++) {
                     if (k < p.K) {
                         const typename Op::E e0 = Op::entry(st_tab(p, Cg, i0 + b, k));
-                        const typename Op::E e1 = Op::entry(st_tab(p, Cg, i0 + b + 1, k));
+                        if constexpr (Op::kPair) {
+                            const typename Op::E e1 = Op::entry(st_tab(p, Cg, i0 + b + 1, k));
 #pragma unroll
-                        for (int v = 0; v < V; v++)
-                            acc[k][v] = st_xor3(acc[k][v], Op::mul(a[b][v], e0), Op::mul(a[b + 1][v], e1));
+                            for (int v = 0; v < V; v++)
+                                acc[k][v] = st_xor3(acc[k][v], Op::mul(a[b][v], e0), Op::mul(a[b + 1][v], e1));
+                        } else {
+#pragma unroll
+                            for (int v = 0; v < V; v++) acc[k][v] ^= Op::mul(a[b][v], e0);
+                        }
                     }
                 }
             }
