@@ -219,7 +219,9 @@ __global__ void __launch_bounds__(kStThreads) encode_stream_kernel(StreamParams 
 template <class Op, int KT, int V>
 __global__ void __launch_bounds__(kStThreads) encode_stream_words_kernel(StreamParams p)
 {
-    constexpr int kStBatch = Op::kBatch;
+    // 4-byte chunks: all 16 sources of a chunk in flight at once (one memory
+    // latency per chunk instead of four: C1, one generation, is latency-bound)
+    constexpr int kStBatch = V == 1 ? 16 : Op::kBatch;
     constexpr size_t kChunk = 4 * V;                           // bytes per chunk
     const size_t Mc = p.M16;                                   // chunks per packet
     const size_t M = Mc * kChunk;
