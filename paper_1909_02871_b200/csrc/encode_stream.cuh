@@ -45,7 +45,8 @@ struct StreamParams {
     uint8_t *B;
     const uint32_t *tabs;   // table of tables of the field (16 words per coefficient)
     size_t M16;             // chunks per packet (16-byte chunks, or 4-byte ones for word-aligned packets)
-    size_t total;           // batch * chunks per packet
+    size_t total;           // batch * chunks per packet (strided kernel: batch * wblocks * 32 threads)
+    size_t wblocks;         // strided kernel: 128-word blocks per packet
     int N, K;
     uint32_t qmask;
 };
@@ -272,6 +273,72 @@ __global__ void __launch_bounds__(kStThreads) encode_stream_words_kernel(StreamP
 #pragma unroll
                 for (int v = 0; v < V; v++) r[v] = Op::kPermuted ? unperm(acc[k][v]) : acc[k][v];
                 st_store<V>(Bg + (size_t)k * M, r);
+            }
+        }
+    }
+}
+
+// Word-aligned packets that are not 16-byte aligned (e.g. 1500 B) in bulk: a
+// warp owns a block of 128 consecutive words of one packet and lane l the words
+// l, l + 32, l + 64, l + 96, so every 4-byte load instruction of the warp reads
+// 128 contiguous bytes (full sectors) and a thread keeps 4 words x kStBatch
+// sources in flight, as the 16-byte-chunk kernel does.
+template <class Op, int KT>
+__global__ void __launch_bounds__(kStThreads) encode_stream_strided_kernel(StreamParams p)
+{
+    constexpr int kStBatch = Op::kBatch;
+    constexpr int W = 4;
+    const size_t Mw = p.M16;                                   // words per packet
+    const size_t M = Mw * 4;
+    const size_t stride = (size_t)gridDim.x * kStThreads;     // a multiple of 32: t & 31 is the lane
+    for (size_t t = (size_t)blockIdx.x * kStThreads + threadIdx.x; t < p.total; t += stride) {
+        const size_t blk = t >> 5;
+        const size_t g = blk / p.wblocks;
+        const size_t w0 = (blk - g * p.wblocks) * 128 + (t & 31);
+        bool ok[W];
+#pragma unroll
+        for (int j = 0; j < W; j++) ok[j] = w0 + 32 * j < Mw;
+        const uint32_t *Ag = reinterpret_cast<const uint32_t *>(p.A + g * (size_t)p.N * M) + w0;
+        const uint8_t *Cg = p.C + g * (size_t)p.N * p.K;
+        uint32_t acc[KT][W];
+#pragma unroll
+        for (int k = 0; k < KT; k++)
+#pragma unroll
+            for (int j = 0; j < W; j++) acc[k][j] = 0u;
+        for (int i0 = 0; i0 < p.N; i0 += kStBatch) {
+            uint32_t a[kStBatch][W];
+#pragma unroll
+            for (int b = 0; b < kStBatch; b++)
+#pragma unroll
+                for (int j = 0; j < W; j++)
+                    a[b][j] = (i0 + b < p.N && ok[j]) ? __ldg(Ag + (size_t)(i0 + b) * Mw + 32 * j) : 0u;
+#pragma unroll
+            for (int b = 0; b < kStBatch; b += Op::kPair ? 2 : 1) {
+                if (i0 + b >= p.N) break;
+#pragma unroll
+                for (int k = 0; k < KT; k++) {
+                    if (k < p.K) {
+                        const typename Op::E e0 = Op::entry(st_tab(p, Cg, i0 + b, k));
+                        if constexpr (Op::kPair) {
+                            const typename Op::E e1 = Op::entry(st_tab(p, Cg, i0 + b + 1, k));
+#pragma unroll
+                            for (int j = 0; j < W; j++)
+                                acc[k][j] = st_xor3(acc[k][j], Op::mul(a[b][j], e0), Op::mul(a[b + 1][j], e1));
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < W; j++) acc[k][j] ^= Op::mul(a[b][j], e0);
+                        }
+                    }
+                }
+            }
+        }
+        uint32_t *Bg = reinterpret_cast<uint32_t *>(p.B + g * (size_t)p.K * M) + w0;
+#pragma unroll
+        for (int k = 0; k < KT; k++) {
+            if (k < p.K) {
+#pragma unroll
+                for (int j = 0; j < W; j++)
+                    if (ok[j]) Bg[(size_t)k * Mw + 32 * j] = Op::kPermuted ? unperm(acc[k][j]) : acc[k][j];
             }
         }
     }

@@ -326,7 +326,9 @@ static int launch_prow_kc(int path, const uint8_t *A, const uint8_t *C, uint8_t 
     return launch_prow<F, 64>(A, C, B, N, K, M, batch, st);
 }
 
-template <class Op, int KT, int V>
+// layout L: 0 = 16-byte chunks, 1 = 4-byte chunks (latency: few words),
+// 2 = strided 4-word blocks (bulk word-aligned packets)
+template <class Op, int KT, int L>
 static int launch_stream_t(const StreamParams &p, cudaStream_t st)
 {
     int dev;
@@ -334,23 +336,26 @@ static int launch_stream_t(const StreamParams &p, cudaStream_t st)
     const size_t sms = (size_t)(g_sm_count[dev] > 0 ? g_sm_count[dev] : 148);
     size_t grid = (p.total + kStThreads - 1) / kStThreads;
     if (grid > sms * 8) grid = sms * 8;                       // grid-stride: 8 CTAs of 256 per SM
-    if constexpr (V == 4) encode_stream_kernel<Op, KT><<<(unsigned)grid, kStThreads, 0, st>>>(p);
-    else encode_stream_words_kernel<Op, KT, V><<<(unsigned)grid, kStThreads, 0, st>>>(p);
+    if constexpr (L == 0) encode_stream_kernel<Op, KT><<<(unsigned)grid, kStThreads, 0, st>>>(p);
+    else if constexpr (L == 1) encode_stream_words_kernel<Op, KT, 1><<<(unsigned)grid, kStThreads, 0, st>>>(p);
+    else encode_stream_strided_kernel<Op, KT><<<(unsigned)grid, kStThreads, 0, st>>>(p);
     return launch_status();
 }
 
-template <class Op, int V>
+template <class Op, int L>
 static int launch_stream_v(const StreamParams &p, cudaStream_t st)
 {
-    if (p.K == 1) return launch_stream_t<Op, 1, V>(p, st);
-    if (p.K == 2) return launch_stream_t<Op, 2, V>(p, st);
-    return launch_stream_t<Op, 4, V>(p, st);
+    if (p.K == 1) return launch_stream_t<Op, 1, L>(p, st);
+    if (p.K == 2) return launch_stream_t<Op, 2, L>(p, st);
+    return launch_stream_t<Op, 4, L>(p, st);
 }
 
 template <class Op>
-static int launch_stream_f(const StreamParams &p, bool wide, cudaStream_t st)
+static int launch_stream_f(const StreamParams &p, int layout, cudaStream_t st)
 {
-    return wide ? launch_stream_v<Op, 4>(p, st) : launch_stream_v<Op, 1>(p, st);
+    if (layout == 0) return launch_stream_v<Op, 0>(p, st);
+    if (layout == 1) return launch_stream_v<Op, 1>(p, st);
+    return launch_stream_v<Op, 2>(p, st);
 }
 
 static int launch_stream(int field, int fi, const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K,
@@ -360,16 +365,23 @@ static int launch_stream(int field, int fi, const uint8_t *A, const uint8_t *C, 
     void *tabs = nullptr;
     if (symbol_address(0, &tabs) != GF_OK) return GF_ECUDA;
     p.tabs = reinterpret_cast<const uint32_t *>(tabs) + (size_t)fi * 256 * kTableWords;
-    // 16-byte chunks when packets are 16-byte aligned, else 4-byte chunks
+    // 16-byte chunks when packets are 16-byte aligned; else 4-byte words, one
+    // per thread while the job is small (C1: latency) and in strided 4-word
+    // blocks per thread in bulk
     const bool wide = M % 16 == 0 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0 &&
                       (reinterpret_cast<uintptr_t>(B) & 15u) == 0;
-    p.A = A; p.C = C; p.B = B; p.M16 = wide ? M / 16 : M / 4; p.total = batch * p.M16; p.N = N; p.K = K;
+    static const int strided_min = env_int("GFRLNC_STREAM_STRIDED_MIN_WORDS", 1 << 20);   // experiments
+    const int layout = wide ? 0 : batch * (M / 4) < (size_t)strided_min ? 1 : 2;
+    p.A = A; p.C = C; p.B = B; p.N = N; p.K = K;
+    p.M16 = wide ? M / 16 : M / 4;
+    p.wblocks = (M / 4 + 127) / 128;
+    p.total = layout == 2 ? batch * p.wblocks * 32 : batch * p.M16;
     p.qmask = (uint32_t)field - 1u;
     switch (field) {
-    case 2: return launch_stream_f<StreamOp<2>>(p, wide, st);
-    case 4: return launch_stream_f<StreamOp<4>>(p, wide, st);
-    case 16: return launch_stream_f<StreamOp<16>>(p, wide, st);
-    case 256: return launch_stream_f<StreamOp<256>>(p, wide, st);
+    case 2: return launch_stream_f<StreamOp<2>>(p, layout, st);
+    case 4: return launch_stream_f<StreamOp<4>>(p, layout, st);
+    case 16: return launch_stream_f<StreamOp<16>>(p, layout, st);
+    case 256: return launch_stream_f<StreamOp<256>>(p, layout, st);
     default: return GF_EFIELD;
     }
 }

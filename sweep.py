@@ -198,10 +198,11 @@ def main():
     if "NEXT2" in todo:
         # paper-shaped sweep (Fig. 2): random linear
         # combinations of N=16 packets, K=1 coded packet, packet sizes 128 B ..
-        # 64 KiB, all fields; enough generations per launch for ~2 GiB of source.
-        # Coded throughput in Gbit/s is the paper's unit (X13).
+        # 64 KiB, all fields, plus the 1500-byte packets of C1/C3 (word- but not
+        # 16-byte-aligned rows); enough generations per launch for ~2 GiB of
+        # source. Coded throughput in Gbit/s is the paper's unit (X13).
         for q in (2, 4, 16, 256):
-            for size in [128 << j for j in range(10)]:
+            for size in [128 << j for j in range(10)] + [1500]:
                 N, K = 16, 1
                 gens = max(1, (2 << 30) // (N * size))
                 A = torch.empty((gens, N, size), dtype=torch.uint8, device=dev)

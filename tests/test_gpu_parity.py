@@ -296,12 +296,14 @@ def test_c5_chunk_sampled(gfm, q):
 
 
 @pytest.mark.parametrize("q", (2, 256))
-def test_next2_full_size_sampled(gfm, q):
+@pytest.mark.parametrize("M", (1024, 1500))
+def test_next2_full_size_sampled(gfm, q, M):
     """The paper's own shape (N = 16 source packets, K = 1) at
-    the NEXT-2 sweep's launch size (2 GiB of source, 1 KiB packets) through the
-    streaming kernel: sampled generations recomputed by the oracle from
-    host-regenerated inputs (device fill by absolute index)."""
-    N, K, M = 16, 1, 1024
+    the NEXT-2 sweep's launch size (2 GiB of source; 1 KiB packets: 16-byte
+    chunks, 1500 B: the strided word kernel) through the streaming kernel:
+    sampled generations recomputed by the oracle from host-regenerated inputs
+    (device fill by absolute index)."""
+    N, K = 16, 1
     G = (2 << 30) // (N * M)
     seed = 190902871 + 2 + 1000 * q
     assert gfm.encode_path(q, N, K, M) == "stream"

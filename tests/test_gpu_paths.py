@@ -22,7 +22,8 @@ if want == "lanek2":       # persistent lane-k: GF(2)/GF(4), K <= 32
 elif want == "stream":    # few coded packets, 16-byte aligned packets (the paper's N = 16, K = 1)
     cases = [(q, s) for q in (2, 4, 16, 256) for s in ((16, 1, 1024, 50), (16, 1, 128, 300), (5, 2, 4096, 3),
                                                        (17, 3, 2064, 4), (64, 4, 16, 100), (1, 1, 16, 10),
-                                                       (16, 1, 1500, 7), (9, 3, 1028, 5), (3, 4, 4, 33))]
+                                                       (16, 1, 1500, 7), (9, 3, 1028, 5), (3, 4, 4, 33),
+                                                       (16, 1, 1500, 700), (7, 2, 516, 40), (16, 4, 2052, 9))]
 else:
     cases = [(q, s) for q in (2, 4, 16, 256) for s in ((17, 33, 1500, 3), (64, 64, 1500, 2), (32, 32, 4100, 2),
                                                        (5, 24, 400, 3), (33, 96, 3000, 2), (7, 65, 1540, 2))]
@@ -41,12 +42,15 @@ print("ok", want)
 ''' % ROOT
 
 
-@pytest.mark.parametrize("path", ["column", "lanek", "fused", "prow", "lanek2", "stream"])
+@pytest.mark.parametrize("path", ["column", "lanek", "fused", "prow", "lanek2", "stream", "stream-strided"])
 def test_forced_encode_path(path):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     env = dict(os.environ, GFRLNC_ENCODE_PATH=path)
+    if path == "stream-strided":   # word-aligned packets through the strided 4-word kernel at any size
+        path = "stream"
+        env.update(GFRLNC_ENCODE_PATH=path, GFRLNC_STREAM_STRIDED_MIN_WORDS="1")
     out = subprocess.run([sys.executable, "-c", SCRIPT, path], env=env, capture_output=True, text=True,
                          timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
