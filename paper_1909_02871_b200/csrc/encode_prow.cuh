@@ -395,6 +395,11 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
                 }
             }
         }
+        // table s is free once this warp's gathers are performed (release
+        // semantics of the arrive); tell the producers before the next step's
+        // source loads and a tile's write-back
+        __syncwarp();
+        if (lane == 0) mbar_arrive(kDone + (s & 3u) * 8u);
         load_a();                                              // step s + 1
         if (++st_g == p.NS) {
             st_g = 0;
@@ -425,8 +430,6 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
                 for (int j = 0; j < 4; j++) acc[r][j] = make_uint4(0u, 0u, 0u, 0u);
             }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(kDone + (s & 3u) * 8u);
     };
 
 #pragma unroll 1
