@@ -81,15 +81,17 @@ int main()
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const int iters = 4096;
     for (int cf = 1; cf >= 0; cf--) {
-        cudaMemset(d_cyc, 0, 8);
-        if (cf) gather_kernel<true><<<sms, 512, smem>>>(d_out, iters, d_cyc);
-        else gather_kernel<false><<<sms, 512, smem>>>(d_out, iters, d_cyc);
-        cudaError_t e = cudaDeviceSynchronize();
-        long long cyc = 0;
-        cudaMemcpy(&cyc, d_cyc, 8, cudaMemcpyDeviceToHost);
-        const double warp_lds = 16.0 * iters * 4;
-        printf("LDS.128 prmt-gather %-14s  err=%d  warp-LDS/clk/SM = %.3f  gathered B/clk/SM = %.1f\n",
-               cf ? "conflict-free" : "2-row-conflict", (int)e, warp_lds / cyc, warp_lds * 512 / cyc);
+        for (int threads = (cf ? 256 : 512); threads <= 512; threads += 128) {   // 8 / 12 / 16 gathering warps
+            cudaMemset(d_cyc, 0, 8);
+            if (cf) gather_kernel<true><<<sms, threads, smem>>>(d_out, iters, d_cyc);
+            else gather_kernel<false><<<sms, threads, smem>>>(d_out, iters, d_cyc);
+            cudaError_t e = cudaDeviceSynchronize();
+            long long cyc = 0;
+            cudaMemcpy(&cyc, d_cyc, 8, cudaMemcpyDeviceToHost);
+            const double warp_lds = threads / 32.0 * iters * 4;
+            printf("LDS.128 prmt-gather %-14s %2d warps  err=%d  warp-LDS/clk/SM = %.3f  gathered B/clk/SM = %.1f\n",
+                   cf ? "conflict-free" : "2-row-conflict", threads / 32, (int)e, warp_lds / cyc, warp_lds * 512 / cyc);
+        }
     }
     return 0;
 }
