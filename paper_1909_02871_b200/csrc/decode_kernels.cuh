@@ -133,8 +133,12 @@ __global__ void __launch_bounds__(256) invert_kernel(InvertParams p)
 // __syncthreads per column.  Per column: pivot by two ballots (lane l holds
 // rows l and l + 32), row swap + scaling with one word per lane, then each
 // lane eliminates its own rows word by word with the split tables of its
-// row's factor (loaded once per column).  Eight matrices per CTA share the
-// field tables.
+// row's factor (loaded once per column).  The PRMT selectors depend only on
+// the pivot row, so lane w computes those of pivot word w once per column
+// (from the byte-permuted word, so that the lookups come out in natural byte
+// order) and every row update reads them back with one broadcast LDS.128:
+// 3 PRMT + 2 LOP3 per row word instead of 12 ALU/FMA operations.  Eight
+// matrices per CTA share the field tables.
 constexpr int kInvWarps = 8;
 
 __device__ __forceinline__ PrmtTab tab5_of(const uint32_t *stab, uint32_t c)
@@ -153,7 +157,8 @@ __global__ void __launch_bounds__(32 * kInvWarps) invert_warp_kernel(InvertParam
     const int RS = RW + 1;                            // row stride (odd: conflict-free column access)
     uint32_t *stab = smem;                            // [256][5]: T0lo,T0hi,T1lo,T1hi,T2
     uint8_t *sinv = reinterpret_cast<uint8_t *>(stab + 256 * 5);
-    uint32_t *Mall = stab + 256 * 5 + 64;             // [warps][N][RS]
+    uint32_t *ssel_all = stab + 256 * 5 + 64;         // [warps][32 words][4]: pivot-row selectors
+    uint32_t *Mall = ssel_all + kInvWarps * 32 * 4;   // [warps][N][RS]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     for (int e = tid; e < 256 * 5; e += blockDim.x) {
         const int c = e / 5, j = e - c * 5;
@@ -163,6 +168,7 @@ __global__ void __launch_bounds__(32 * kInvWarps) invert_warp_kernel(InvertParam
     const size_t g = (size_t)blockIdx.x * kInvWarps + warp;
     const bool live = g < p.batch;
     uint32_t *Mx = Mall + (size_t)warp * N * RS;
+    uint32_t *ssel = ssel_all + warp * 32 * 4;
     uint8_t *Mb = reinterpret_cast<uint8_t *>(Mx);
     if (live) {
         const uint8_t *Cg = p.C + g * (size_t)N * N;
@@ -179,41 +185,40 @@ __global__ void __launch_bounds__(32 * kInvWarps) invert_warp_kernel(InvertParam
     __syncwarp();
 
     const int ra = lane, rb = lane + 32;              // this lane's rows
+    const bool has_a = ra < N, has_b = rb < N;        // has_b is warp-uniform false for N <= 32
+    uint32_t *rowa = Mx + (size_t)ra * RS, *rowb = Mx + (size_t)rb * RS;
     int rank = 0;
     for (int col = 0; col < N; col++) {
         const int cw = col >> 2;                      // word of the column
         // pivot: first row >= rank with a nonzero entry in this column
-        const bool ha = ra < N && ra >= rank && Mb[(size_t)ra * RS * 4 + col] != 0;
-        const bool hb = rb < N && rb >= rank && Mb[(size_t)rb * RS * 4 + col] != 0;
+        const bool ha = has_a && ra >= rank && Mb[(size_t)ra * RS * 4 + col] != 0;
+        const bool hb = has_b && rb >= rank && Mb[(size_t)rb * RS * 4 + col] != 0;
         const uint32_t ba = __ballot_sync(0xffffffffu, ha), bb = __ballot_sync(0xffffffffu, hb);
         if ((ba | bb) == 0u) continue;                // rank deficient column
         const int piv = ba ? __ffs(ba) - 1 : 32 + __ffs(bb) - 1;
-        // swap the pivot row into place and scale it by the pivot's inverse
+        // swap the pivot row into place and scale it by the pivot's inverse;
+        // lane w keeps the selectors of the scaled pivot word w
         const uint32_t pv = Mb[(size_t)piv * RS * 4 + col];
         __syncwarp();
         if (lane >= cw && lane < RW) {
             const uint32_t a = Mx[(size_t)piv * RS + lane], b = Mx[(size_t)rank * RS + lane];
+            const uint32_t sa = mul_word(tab5_of(stab, sinv[pv]), a);
             Mx[(size_t)piv * RS + lane] = b;
-            Mx[(size_t)rank * RS + lane] = mul_word(tab5_of(stab, sinv[pv]), a);
+            Mx[(size_t)rank * RS + lane] = sa;
+            const Sel sl = make_sel(prmt(sa, sa, 0x3120u));   // permuted input: natural-order products
+            *reinterpret_cast<uint4 *>(ssel + lane * 4) = make_uint4(sl.s0, sl.s1, sl.s2, 0u);
         }
         __syncwarp();
-        // eliminate: each lane its rows, word by word, with its row factor's tables
-        const uint32_t *prow = Mx + (size_t)rank * RS;
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const int r = h ? rb : ra;
-            if (r >= N || r == rank) continue;
-            const uint32_t f = Mb[(size_t)r * RS * 4 + col];
-            if (f == 0) continue;
-            const PrmtTab T = tab5_of(stab, f);
-            uint32_t *row = Mx + (size_t)r * RS;
-            int w = cw;
-            for (; w + 1 < RW; w += 2) {                  // two words in flight
-                const uint32_t p0 = prow[w], p1 = prow[w + 1], q0 = row[w], q1 = row[w + 1];
-                row[w] = q0 ^ mul_word(T, p0);
-                row[w + 1] = q1 ^ mul_word(T, p1);
-            }
-            if (w < RW) row[w] ^= mul_word(T, prow[w]);
+        // eliminate: each lane its rows (factor 0 for the pivot row: no change)
+        const uint32_t fa = (has_a && ra != rank) ? Mb[(size_t)ra * RS * 4 + col] : 0u;
+        const uint32_t fb = (has_b && rb != rank) ? Mb[(size_t)rb * RS * 4 + col] : 0u;
+        __syncwarp();                                 // factors read before any row update
+        const PrmtTab Ta = tab5_of(stab, fa), Tb = tab5_of(stab, fb);
+        for (int w = cw; w < RW; w++) {
+            const uint4 sv = *reinterpret_cast<const uint4 *>(ssel + w * 4);   // broadcast
+            const Sel sl{sv.x, sv.y, sv.z};
+            if (has_a) rowa[w] ^= lookup_perm(Ta, sl);
+            if (has_b) rowb[w] ^= lookup_perm(Tb, sl);
         }
         __syncwarp();
         rank++;

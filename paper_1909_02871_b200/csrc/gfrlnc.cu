@@ -780,7 +780,7 @@ int gf_invert_batch(int field, const uint8_t *C, uint8_t *D, int *rank, int N, s
     p.inv = reinterpret_cast<const uint8_t *>(inv) + (size_t)fi * 256;
     const size_t rw = (2 * (size_t)N + 3) / 4;
     if (N <= 64) {                                            // warp per matrix (no CTA barriers)
-        const size_t smem_w = (256 * 5 + 64) * 4 + (size_t)kInvWarps * N * (rw + 1) * 4;
+        const size_t smem_w = (256 * 5 + 64 + kInvWarps * 32 * 4) * 4 + (size_t)kInvWarps * N * (rw + 1) * 4;
         if (cudaFuncSetAttribute(invert_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem_w) != cudaSuccess)
             return GF_ECUDA;
