@@ -55,7 +55,15 @@ template <int KG, bool WIDE = false> struct LkGeom {
     static constexpr int WT = KG == 1 ? (WIDE ? 64 : 32) : 48;   // words per gatherer lane
     static constexpr int WG = KG == 4 ? 4 : kLkWG;        // word groups
     static constexpr int TW = WT * WG;                    // words per tile
-    static constexpr int QS = TW + 1;                     // Q row stride (odd)
+    // V2 (KG = 1: C5): 64-bit gathers. Q row stride even with QS / 2 odd, so
+    // that rows are 8-byte aligned and the 16 possible rows of a half-warp's
+    // LDS.64 sit in 16 distinct 8-byte bank slots (half the LSU instructions of
+    // LDS.32 for the same wavefronts; ncu: the LSU instruction pipe was 74% busy
+    // against 68% for the wavefronts).  C5 GF(2) +1.1%, GF(4) +3.3%; with
+    // KG = 2 it measured 3% slower, so KG > 1 keeps 32-bit gathers, odd stride.
+    static constexpr bool V2 = KG == 1;
+    static constexpr int QS = V2 ? TW + 2 : TW + 1;
+    static_assert(V2 ? (QS / 2) % 2 == 1 : QS % 2 == 1, "Q row stride");
     static constexpr int BWORDS = (TW + 32 * kLkBuildWarps - 1) / (32 * kLkBuildWarps);
     static constexpr int THREADS = 32 * (KG * WG + kLkBuildWarps);
     static constexpr int MINB = KG == 1 ? (WIDE ? 2 : 3) : 1;   // CTAs per SM targeted
@@ -256,15 +264,28 @@ encode_lanek_kernel(LanekParams p)
         const int b = s % kLkNQ;
         nbar_sync(BAR_FULL + b, NT);
         const uint32_t *q = Q + b * kQWords + wg * WT;
-        if (F == 256) {
-            const uint32_t *lo = q + (r & 15u) * QS;
+        if constexpr (!G::V2) {
+            const uint32_t *lo = q + (F == 256 ? (r & 15u) : r) * QS;
             const uint32_t *hi = q + (16u + (r >> 4)) * QS;
 #pragma unroll
-            for (int w = 0; w < WT; w++) acc[w] ^= lo[w] ^ hi[w];
-        } else {
-            const uint32_t *lo = q + r * QS;
+            for (int w = 0; w < WT; w++) acc[w] ^= F == 256 ? lo[w] ^ hi[w] : lo[w];
+        } else if (F == 256) {
+            const uint2 *lo = reinterpret_cast<const uint2 *>(q + (r & 15u) * QS);
+            const uint2 *hi = reinterpret_cast<const uint2 *>(q + (16u + (r >> 4)) * QS);
 #pragma unroll
-            for (int w = 0; w < WT; w++) acc[w] ^= lo[w];
+            for (int v = 0; v < WT / 2; v++) {
+                const uint2 x = lo[v], y = hi[v];
+                acc[2 * v] ^= x.x ^ y.x;
+                acc[2 * v + 1] ^= x.y ^ y.y;
+            }
+        } else {
+            const uint2 *lo = reinterpret_cast<const uint2 *>(q + r * QS);
+#pragma unroll
+            for (int v = 0; v < WT / 2; v++) {
+                const uint2 x = lo[v];
+                acc[2 * v] ^= x.x;
+                acc[2 * v + 1] ^= x.y;
+            }
         }
         nbar_arrive(BAR_EMPTY + b, NT);
     }
@@ -292,7 +313,7 @@ encode_lanek_kernel(LanekParams p)
     // ---- epilogue: transpose through shared memory so that each warp writes
     // contiguous runs of one coded packet (the Q buffers are free once every
     // gatherer passed its last step: named barrier over the gatherers only)
-    constexpr int OS = TW + 1;
+    constexpr int OS = G::V2 ? TW + 2 : TW + 1;                 // V2: even, OS / 2 odd (64-bit stores conflict-free)
     // rows of coded packets staged per pass: the largest of KTL, KTL/2, ... (>= 32)
     // that fits in the Q buffers
     constexpr int kFit = (kLkNQ * kQWords) / OS;
@@ -306,8 +327,14 @@ encode_lanek_kernel(LanekParams p)
         nbar_sync(BAR_EPI, 32 * GW);
         if (kl / kRowsPerPass == h) {
             const int r = kl - h * kRowsPerPass;
+            if constexpr (G::V2) {
+                uint2 *o2 = reinterpret_cast<uint2 *>(ot + r * OS + wg * WT);
 #pragma unroll
-            for (int w = 0; w < WT; w++) ot[r * OS + wg * WT + w] = acc[w];
+                for (int v = 0; v < WT / 2; v++) o2[v] = make_uint2(acc[2 * v], acc[2 * v + 1]);
+            } else {
+#pragma unroll
+                for (int w = 0; w < WT; w++) ot[r * OS + wg * WT + w] = acc[w];
+            }
         }
         nbar_sync(BAR_EPI, 32 * GW);
         const int kbase = k0 + h * kRowsPerPass;
