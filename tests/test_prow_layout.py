@@ -159,3 +159,24 @@ def test_smem_layout_fits():
     assert end - 0x400 <= 227 * 1024
     assert 0x400 + 8 * 8 <= 0x1000
     assert 0x1000 + 3 * 0x10000 <= 0x31000
+
+
+@pytest.mark.parametrize("TW", (512, 256))
+def test_lanek_v2_gathers_conflict_free(TW):
+    """encode_lanek.cuh LkGeom V2 (32 coded packets per CTA): Q row stride
+    QS = TW + 2 (even, QS / 2 odd).  A half-warp's LDS.64 reads row r_k at word
+    offset wg*WT + 2v: 16 lanes, rows from 16 values, land in 16 distinct 8-byte
+    bank slots unless they read the same row (broadcast), for any rows; and
+    rows are 8-byte aligned."""
+    QS = TW + 2
+    assert QS % 2 == 0 and (QS // 2) % 2 == 1
+    rng = np.random.default_rng(TW)
+    WT = TW // 8
+    for wg in range(8):
+        for v in range(0, WT // 2, 7):
+            for _ in range(50):
+                rows = rng.integers(0, 16, size=16)
+                addr = {int(r): (int(r) * QS + wg * WT + 2 * v) * 4 for r in rows}   # distinct rows only
+                assert all(a % 8 == 0 for a in addr.values())
+                slots = [(a // 8) % 16 for a in addr.values()]
+                assert len(set(slots)) == len(slots)
