@@ -45,8 +45,8 @@ struct StreamParams {
     uint8_t *B;
     const uint32_t *tabs;   // table of tables of the field (16 words per coefficient)
     size_t M16;             // chunks per packet (16-byte chunks, or 4-byte ones for word-aligned packets)
-    size_t total;           // batch * chunks per packet (strided kernel: batch * wblocks * 32 threads)
-    size_t wblocks;         // strided kernel: 128-word blocks per packet
+    size_t total;           // batch * chunks per packet (strided / wide2 kernels: batch * wblocks * 32 threads)
+    size_t wblocks;         // strided kernel: 128-word blocks per packet; wide2: 64-chunk blocks
     int N, K;
     uint32_t qmask;
 };
@@ -339,6 +339,81 @@ __global__ void __launch_bounds__(kStThreads) encode_stream_strided_kernel(Strea
 #pragma unroll
                 for (int j = 0; j < W; j++)
                     if (ok[j]) Bg[(size_t)k * Mw + 32 * j] = Op::kPermuted ? unperm(acc[k][j]) : acc[k][j];
+            }
+        }
+    }
+}
+
+// 16-byte chunks, two per thread (chunks l and l + 32 of a warp's 64-chunk
+// block of one packet): every per-source cost (coefficient byte, table entry,
+// addresses) is paid once per 32 source bytes instead of 16.
+template <class Op, int KT>
+__global__ void __launch_bounds__(kStThreads) encode_stream_wide2_kernel(StreamParams p)
+{
+    constexpr int kStBatch = Op::kBatch;
+    constexpr int W = 2;
+    const size_t M16 = p.M16;
+    const size_t stride = (size_t)gridDim.x * kStThreads;     // a multiple of 32: t & 31 is the lane
+    for (size_t t = (size_t)blockIdx.x * kStThreads + threadIdx.x; t < p.total; t += stride) {
+        const size_t blk = t >> 5;
+        const size_t g = blk / p.wblocks;
+        const size_t c0 = (blk - g * p.wblocks) * 64 + (t & 31);
+        bool ok[W];
+#pragma unroll
+        for (int j = 0; j < W; j++) ok[j] = c0 + 32 * j < M16;
+        const uint4 *Ag = reinterpret_cast<const uint4 *>(p.A + g * (size_t)p.N * (M16 * 16)) + c0;
+        const uint8_t *Cg = p.C + g * (size_t)p.N * p.K;
+        uint4 acc[KT][W];
+#pragma unroll
+        for (int k = 0; k < KT; k++)
+#pragma unroll
+            for (int j = 0; j < W; j++) acc[k][j] = make_uint4(0u, 0u, 0u, 0u);
+        for (int i0 = 0; i0 < p.N; i0 += kStBatch) {
+            uint4 a[kStBatch][W];
+#pragma unroll
+            for (int b = 0; b < kStBatch; b++)
+#pragma unroll
+                for (int j = 0; j < W; j++)
+                    a[b][j] = (i0 + b < p.N && ok[j]) ? st_ld_stream(Ag + (size_t)(i0 + b) * M16 + 32 * j)
+                                                      : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+            for (int b = 0; b < kStBatch; b += Op::kPair ? 2 : 1) {
+                if (i0 + b >= p.N) break;
+#pragma unroll
+                for (int k = 0; k < KT; k++) {
+                    if (k < p.K) {
+                        const typename Op::E e0 = Op::entry(st_tab(p, Cg, i0 + b, k));
+                        if constexpr (Op::kPair) {
+                            const typename Op::E e1 = Op::entry(st_tab(p, Cg, i0 + b + 1, k));
+#pragma unroll
+                            for (int j = 0; j < W; j++) {
+                                acc[k][j].x = st_xor3(acc[k][j].x, Op::mul(a[b][j].x, e0), Op::mul(a[b + 1][j].x, e1));
+                                acc[k][j].y = st_xor3(acc[k][j].y, Op::mul(a[b][j].y, e0), Op::mul(a[b + 1][j].y, e1));
+                                acc[k][j].z = st_xor3(acc[k][j].z, Op::mul(a[b][j].z, e0), Op::mul(a[b + 1][j].z, e1));
+                                acc[k][j].w = st_xor3(acc[k][j].w, Op::mul(a[b][j].w, e0), Op::mul(a[b + 1][j].w, e1));
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < W; j++) {
+                                acc[k][j].x ^= Op::mul(a[b][j].x, e0); acc[k][j].y ^= Op::mul(a[b][j].y, e0);
+                                acc[k][j].z ^= Op::mul(a[b][j].z, e0); acc[k][j].w ^= Op::mul(a[b][j].w, e0);
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        uint4 *Bg = reinterpret_cast<uint4 *>(p.B + g * (size_t)p.K * (M16 * 16)) + c0;
+#pragma unroll
+        for (int k = 0; k < KT; k++) {
+            if (k < p.K) {
+#pragma unroll
+                for (int j = 0; j < W; j++) {
+                    if (!ok[j]) continue;
+                    uint4 r = acc[k][j];
+                    if (Op::kPermuted) r = make_uint4(unperm(r.x), unperm(r.y), unperm(r.z), unperm(r.w));
+                    Bg[(size_t)k * M16 + 32 * j] = r;
+                }
             }
         }
     }

@@ -327,7 +327,8 @@ static int launch_prow_kc(int path, const uint8_t *A, const uint8_t *C, uint8_t 
 }
 
 // layout L: 0 = 16-byte chunks, 1 = 4-byte chunks (latency: few words),
-// 2 = strided 4-word blocks (bulk word-aligned packets)
+// 2 = strided 4-word blocks (bulk word-aligned packets), 3 = two 16-byte
+// chunks per thread (16-byte-aligned packets of >= 1 KiB)
 template <class Op, int KT, int L>
 static int launch_stream_t(const StreamParams &p, cudaStream_t st)
 {
@@ -337,6 +338,7 @@ static int launch_stream_t(const StreamParams &p, cudaStream_t st)
     size_t grid = (p.total + kStThreads - 1) / kStThreads;
     if (grid > sms * 8) grid = sms * 8;                       // grid-stride: 8 CTAs of 256 per SM
     if constexpr (L == 0) encode_stream_kernel<Op, KT><<<(unsigned)grid, kStThreads, 0, st>>>(p);
+    else if constexpr (L == 3) encode_stream_wide2_kernel<Op, KT><<<(unsigned)grid, kStThreads, 0, st>>>(p);
     else if constexpr (L == 1) encode_stream_words_kernel<Op, KT, 1><<<(unsigned)grid, kStThreads, 0, st>>>(p);
     else encode_stream_strided_kernel<Op, KT><<<(unsigned)grid, kStThreads, 0, st>>>(p);
     return launch_status();
@@ -355,7 +357,8 @@ static int launch_stream_f(const StreamParams &p, int layout, cudaStream_t st)
 {
     if (layout == 0) return launch_stream_v<Op, 0>(p, st);
     if (layout == 1) return launch_stream_v<Op, 1>(p, st);
-    return launch_stream_v<Op, 2>(p, st);
+    if (layout == 2) return launch_stream_v<Op, 2>(p, st);
+    return launch_stream_v<Op, 3>(p, st);
 }
 
 static int launch_stream(int field, int fi, const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K,
@@ -370,12 +373,16 @@ static int launch_stream(int field, int fi, const uint8_t *A, const uint8_t *C, 
     // blocks per thread in bulk
     const bool wide = M % 16 == 0 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0 &&
                       (reinterpret_cast<uintptr_t>(B) & 15u) == 0;
+    // 16-byte-aligned packets of >= 1 KiB: two chunks per thread (per-source
+    // costs halved: NEXT-2 GF(16)/GF(256) +7%, GF(4) +4%); smaller packets
+    // would leave most lanes of a 64-chunk block idle
     static const int strided_min = env_int("GFRLNC_STREAM_STRIDED_MIN_WORDS", 1 << 20);   // experiments
-    const int layout = wide ? 0 : batch * (M / 4) < (size_t)strided_min ? 1 : 2;
+    static const int wide2_min = env_int("GFRLNC_STREAM_WIDE2_MIN_CHUNKS", 64);           // experiments
+    const int layout = wide ? (M / 16 >= (size_t)wide2_min ? 3 : 0) : batch * (M / 4) < (size_t)strided_min ? 1 : 2;
     p.A = A; p.C = C; p.B = B; p.N = N; p.K = K;
     p.M16 = wide ? M / 16 : M / 4;
-    p.wblocks = (M / 4 + 127) / 128;
-    p.total = layout == 2 ? batch * p.wblocks * 32 : batch * p.M16;
+    p.wblocks = layout == 3 ? (p.M16 + 63) / 64 : (M / 4 + 127) / 128;
+    p.total = layout >= 2 ? batch * p.wblocks * 32 : batch * p.M16;
     p.qmask = (uint32_t)field - 1u;
     switch (field) {
     case 2: return launch_stream_f<StreamOp<2>>(p, layout, st);

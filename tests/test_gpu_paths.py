@@ -42,7 +42,8 @@ print("ok", want)
 ''' % ROOT
 
 
-@pytest.mark.parametrize("path", ["column", "lanek", "fused", "prow", "lanek2", "stream", "stream-strided"])
+@pytest.mark.parametrize("path", ["column", "lanek", "fused", "prow", "lanek2", "stream", "stream-strided",
+                                  "stream-wide2"])
 def test_forced_encode_path(path):
     import torch
     if not torch.cuda.is_available():
@@ -51,6 +52,9 @@ def test_forced_encode_path(path):
     if path == "stream-strided":   # word-aligned packets through the strided 4-word kernel at any size
         path = "stream"
         env.update(GFRLNC_ENCODE_PATH=path, GFRLNC_STREAM_STRIDED_MIN_WORDS="1")
+    if path == "stream-wide2":     # 16-byte-aligned packets through the two-chunk kernel at any size
+        path = "stream"
+        env.update(GFRLNC_ENCODE_PATH=path, GFRLNC_STREAM_WIDE2_MIN_CHUNKS="1")
     out = subprocess.run([sys.executable, "-c", SCRIPT, path], env=env, capture_output=True, text=True,
                          timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
