@@ -466,13 +466,18 @@ static int encode_path(int field, int N, int K, size_t M, const void *A, const v
     const int ov = encode_path_override();
     if (!aligned) return 1;
     if (K <= 4 && (ov == 6 || ov == 0)) return 8;                // streaming (16- or 4-byte chunks)
-    if (ov == 1 || (ov == 0 && K < 24 && !(field >= 16 && K > 8))) return 0;
+    // GF(4), 9 <= K < 24: product rows beat the column kernel when the 384-word
+    // tiles cover the packet well (>= 85%) and either K > 16 (where the column
+    // kernel halves) or packets are >= 4 KiB (profiles/r01_gf4_prow_routing.txt)
+    const size_t mw = M / 4, tiles = (mw + 383) / 384;
+    const bool gf4_prow = field == 4 && K > 8 && K < 24 && mw * 100 >= tiles * 384 * 85 && (K > 16 || M >= 4096);
+    if (ov == 1 || (ov == 0 && K < 24 && !(field >= 16 && K > 8) && !gf4_prow)) return 0;
     const int kg2 = K > 32 ? 1 : 0;      // (K > 64 uses 128 coded packets per CTA)
     if (ov == 3) return 4 + kg2;
     // product rows for GF(16)/GF(256) from K = 9 on (measured: tools/exp_shapes.py),
     // with 16, 32 or 64 coded packets per CTA so that few lanes idle
     const int prow = K <= 16 ? 10 : K <= 32 ? 9 : 6;
-    if (ov == 4 || (ov == 0 && field >= 16 && K > 8)) return prow;
+    if (ov == 4 || (ov == 0 && ((field >= 16 && K > 8) || gf4_prow))) return prow;
     if (field <= 4 && K <= 32 && (ov == 5 || (ov == 0 && lanek2_default()))) return 7;
     return 2 + kg2;
 }

@@ -221,6 +221,12 @@ def test_encode_path_query():
     assert gf.encode_path(16, 32, 16, 1500) == "prow-16"
     assert gf.encode_path(256, 16, 8, 1500) == "column-words"
     assert gf.encode_path(4, 32, 32, 1500) == "lanek-32"
+    # GF(4), 9 <= K < 24: product rows when tiles cover >= 85% and (K > 16 or M >= 4 KiB)
+    assert gf.encode_path(4, 32, 20, 1500) == "prow-32"
+    assert gf.encode_path(4, 32, 20, 2048) == "column-words"      # 2 tiles for 512 words: 67%
+    assert gf.encode_path(4, 32, 12, 4096) == "prow-16"
+    assert gf.encode_path(4, 32, 12, 1500) == "column-words"
+    assert gf.encode_path(2, 32, 20, 4096) == "column-words"
     assert gf.encode_path(4, 64, 64, 1500) == "lanek-64"
     assert gf.encode_path(2, 32, 32, 1 << 20) == "lanek-32"     # C5
     assert gf.encode_path(256, 16, 1, 1024) == "stream"         # NEXT-2 (paper: N = 16, K = 1)

@@ -169,7 +169,8 @@ def test_c1_full(gfm):
     (1, 1, 1, 1), (1, 1, 4, 1), (3, 2, 5, 2), (16, 1, 1500, 3), (17, 33, 1500, 3),
     (64, 64, 1500, 4), (5, 7, 4096, 2), (2, 3, 130, 9), (32, 32, 4100, 2), (40, 17, 999, 2),
     (8, 5, 12, 17), (5, 24, 400, 3), (3, 40, 64, 5), (7, 65, 1540, 2), (1, 32, 8, 1),
-    (33, 96, 3000, 2), (300, 260, 68, 2), (5, 520, 36, 2), (257, 3, 1500, 2)])
+    (33, 96, 3000, 2), (300, 260, 68, 2), (5, 520, 36, 2), (257, 3, 1500, 2), (9, 20, 1500, 3),
+    (11, 12, 4096, 2)])
 def test_encode_parity_shapes(gfm, q, N, K, M, batch):
     A = si.random_bytes(51 + N, si.STREAM_A, 0, batch * N * M).reshape(batch, N, M)
     C = si.uniform_coeffs(q, 52 + K, si.STREAM_C, 0, batch * N * K).reshape(batch, N, K)
