@@ -1,5 +1,6 @@
 """Host-side logic of bench.py: roofline accounting and JSON contract pieces."""
 import bench
+import seeded_inputs as si
 
 
 def test_roofline_lanek_is_smem_bound():
@@ -18,3 +19,30 @@ def test_roofline_column_is_alu_bound_and_hbm_takes_over():
     assert r["bound"] in ("alu", "hbm")
     r, _ = bench.dominant_roofline(2, 32, 1, 1 << 20, 64, "column-words", 0.01, peaks)
     assert r["bound"] == "hbm"          # K = 1: the stream dominates
+
+
+def test_cpu_baseline_every_small_config():
+    """The bench's cpu_baseline leg (the oracle on a bounded sample) runs for
+    the one-generation C1 as well as C3 (regression: C1 has batch = 1)."""
+    for name in ("C1", "C3"):
+        cfg = si.ENCODE_CONFIGS[name]
+        out = bench.cpu_baseline(cfg, 256, seconds_target=0.02)
+        assert out["kind"] == "oracle" and out["value"] > 0 and out["cores"] >= 1
+        assert f"of {cfg.batch} generations of {name}" in out["sample"]
+
+
+def test_reference_arm_c1_line(capsys):
+    """bench.py --impl reference prints one JSON line with the oracle's numbers
+    (C1: one generation per step)."""
+    import json
+    import sys
+    old = sys.argv
+    sys.argv = ["bench.py", "--impl", "reference", "--config", "C1", "--steps", "2", "--warmup", "1"]
+    try:
+        args = bench.parse()
+    finally:
+        sys.argv = old
+    bench.run_reference(args)
+    line = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] == 0
+    assert line["cpu_baseline"]["kind"] == "oracle"
