@@ -46,7 +46,7 @@ struct StreamParams {
     const uint32_t *tabs;   // table of tables of the field (16 words per coefficient)
     size_t M16;             // chunks per packet (16-byte chunks, or 4-byte ones for word-aligned packets)
     size_t total;           // batch * chunks per packet (strided / wide2 kernels: batch * wblocks * 32 threads)
-    size_t wblocks;         // strided kernel: 128-word blocks per packet; wide2: 64-chunk blocks
+    size_t wblocks;         // strided kernel: (32 W)-word blocks per packet; wide2: 64-chunk blocks
     int N, K;
     uint32_t qmask;
 };
@@ -279,22 +279,23 @@ __global__ void __launch_bounds__(kStThreads) encode_stream_words_kernel(StreamP
 }
 
 // Word-aligned packets that are not 16-byte aligned (e.g. 1500 B) in bulk: a
-// warp owns a block of 128 consecutive words of one packet and lane l the words
-// l, l + 32, l + 64, l + 96, so every 4-byte load instruction of the warp reads
-// 128 contiguous bytes (full sectors) and a thread keeps 4 words x kStBatch
-// sources in flight, as the 16-byte-chunk kernel does.
-template <class Op, int KT>
+// warp owns a block of 32 W consecutive words of one packet and lane l the
+// words l, l + 32, ..., l + 32 (W - 1), so every 4-byte load instruction of the
+// warp reads 128 contiguous bytes (full sectors); W (4, 8 or 12) is chosen per
+// launch so that the blocks cover the packet well (1500 B = 375 words: one
+// 384-word block, W = 12), and every per-source cost (coefficient byte, table
+// entry, addresses) is paid once per W words.
+template <class Op, int KT, int W>
 __global__ void __launch_bounds__(kStThreads) encode_stream_strided_kernel(StreamParams p)
 {
     constexpr int kStBatch = Op::kBatch;
-    constexpr int W = 4;
     const size_t Mw = p.M16;                                   // words per packet
     const size_t M = Mw * 4;
     const size_t stride = (size_t)gridDim.x * kStThreads;     // a multiple of 32: t & 31 is the lane
     for (size_t t = (size_t)blockIdx.x * kStThreads + threadIdx.x; t < p.total; t += stride) {
         const size_t blk = t >> 5;
         const size_t g = blk / p.wblocks;
-        const size_t w0 = (blk - g * p.wblocks) * 128 + (t & 31);
+        const size_t w0 = (blk - g * p.wblocks) * (32 * W) + (t & 31);
         bool ok[W];
 #pragma unroll
         for (int j = 0; j < W; j++) ok[j] = w0 + 32 * j < Mw;

@@ -327,8 +327,8 @@ static int launch_prow_kc(int path, const uint8_t *A, const uint8_t *C, uint8_t 
 }
 
 // layout L: 0 = 16-byte chunks, 1 = 4-byte chunks (latency: few words),
-// 2 = strided 4-word blocks (bulk word-aligned packets), 3 = two 16-byte
-// chunks per thread (16-byte-aligned packets of >= 1 KiB)
+// 2 / 4 / 5 = strided 4- / 8- / 12-word blocks per thread (bulk word-aligned
+// packets), 3 = two 16-byte chunks per thread (16-byte-aligned packets >= 1 KiB)
 template <class Op, int KT, int L>
 static int launch_stream_t(const StreamParams &p, cudaStream_t st)
 {
@@ -340,7 +340,9 @@ static int launch_stream_t(const StreamParams &p, cudaStream_t st)
     if constexpr (L == 0) encode_stream_kernel<Op, KT><<<(unsigned)grid, kStThreads, 0, st>>>(p);
     else if constexpr (L == 3) encode_stream_wide2_kernel<Op, KT><<<(unsigned)grid, kStThreads, 0, st>>>(p);
     else if constexpr (L == 1) encode_stream_words_kernel<Op, KT, 1><<<(unsigned)grid, kStThreads, 0, st>>>(p);
-    else encode_stream_strided_kernel<Op, KT><<<(unsigned)grid, kStThreads, 0, st>>>(p);
+    else if constexpr (L == 2) encode_stream_strided_kernel<Op, KT, 4><<<(unsigned)grid, kStThreads, 0, st>>>(p);
+    else if constexpr (L == 4) encode_stream_strided_kernel<Op, KT, 8><<<(unsigned)grid, kStThreads, 0, st>>>(p);
+    else encode_stream_strided_kernel<Op, KT, 12><<<(unsigned)grid, kStThreads, 0, st>>>(p);
     return launch_status();
 }
 
@@ -358,6 +360,8 @@ static int launch_stream_f(const StreamParams &p, int layout, cudaStream_t st)
     if (layout == 0) return launch_stream_v<Op, 0>(p, st);
     if (layout == 1) return launch_stream_v<Op, 1>(p, st);
     if (layout == 2) return launch_stream_v<Op, 2>(p, st);
+    if (layout == 4) return launch_stream_v<Op, 4>(p, st);
+    if (layout == 5) return launch_stream_v<Op, 5>(p, st);
     return launch_stream_v<Op, 3>(p, st);
 }
 
@@ -378,10 +382,27 @@ static int launch_stream(int field, int fi, const uint8_t *A, const uint8_t *C, 
     // would leave most lanes of a 64-chunk block idle
     static const int strided_min = env_int("GFRLNC_STREAM_STRIDED_MIN_WORDS", 1 << 20);   // experiments
     static const int wide2_min = env_int("GFRLNC_STREAM_WIDE2_MIN_CHUNKS", 64);           // experiments
-    const int layout = wide ? (M / 16 >= (size_t)wide2_min ? 3 : 0) : batch * (M / 4) < (size_t)strided_min ? 1 : 2;
+    static const int strided_wmax_env = env_int("GFRLNC_STREAM_STRIDED_W", 0);             // experiments: force W
+    int layout = wide ? (M / 16 >= (size_t)wide2_min ? 3 : 0) : batch * (M / 4) < (size_t)strided_min ? 1 : 2;
+    // strided: the widest of 12 / 8 / 4 words per thread whose (32 W)-word
+    // blocks cover >= 90% of the packet (layouts 5 / 4 / 2); GF(2) / GF(4)
+    // stay at 4 (their 8-source batches at W = 12 need 180 registers: 1500 B,
+    // N = 16: GF(2) 5.79 -> 4.81 TB/s, while GF(16) 3.74 -> 4.07, GF(256)
+    // 3.61 -> 4.03; profiles/r01_stream_strided_w_v34.txt)
+    const int strided_wmax = field >= 16 ? 12 : 4;
+    int sw = 4;
+    if (layout == 2) {
+        const size_t mw = M / 4;
+        for (int w = 12; w >= 8; w -= 4) {
+            const size_t blk = 32u * (size_t)w, nb = (mw + blk - 1) / blk;
+            if (w <= strided_wmax && mw * 10 >= nb * blk * 9) { sw = w; break; }
+        }
+        if (strided_wmax_env == 4 || strided_wmax_env == 8 || strided_wmax_env == 12) sw = strided_wmax_env;   // forced
+        layout = sw == 12 ? 5 : sw == 8 ? 4 : 2;
+    }
     p.A = A; p.C = C; p.B = B; p.N = N; p.K = K;
     p.M16 = wide ? M / 16 : M / 4;
-    p.wblocks = layout == 3 ? (p.M16 + 63) / 64 : (M / 4 + 127) / 128;
+    p.wblocks = layout == 3 ? (p.M16 + 63) / 64 : (M / 4 + 32u * sw - 1) / (32u * sw);
     p.total = layout >= 2 ? batch * p.wblocks * 32 : batch * p.M16;
     p.qmask = (uint32_t)field - 1u;
     switch (field) {

@@ -43,15 +43,16 @@ print("ok", want)
 
 
 @pytest.mark.parametrize("path", ["column", "lanek", "fused", "prow", "lanek2", "stream", "stream-strided",
-                                  "stream-wide2"])
+                                  "stream-strided8", "stream-strided12", "stream-wide2"])
 def test_forced_encode_path(path):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     env = dict(os.environ, GFRLNC_ENCODE_PATH=path)
-    if path == "stream-strided":   # word-aligned packets through the strided 4-word kernel at any size
+    if path.startswith("stream-strided"):   # word-aligned packets through the strided kernel at any size
+        wmax = path[len("stream-strided"):] or "4"
         path = "stream"
-        env.update(GFRLNC_ENCODE_PATH=path, GFRLNC_STREAM_STRIDED_MIN_WORDS="1")
+        env.update(GFRLNC_ENCODE_PATH=path, GFRLNC_STREAM_STRIDED_MIN_WORDS="1", GFRLNC_STREAM_STRIDED_W=wmax)
     if path == "stream-wide2":     # 16-byte-aligned packets through the two-chunk kernel at any size
         path = "stream"
         env.update(GFRLNC_ENCODE_PATH=path, GFRLNC_STREAM_WIDE2_MIN_CHUNKS="1")
