@@ -345,20 +345,19 @@ __global__ void __launch_bounds__(kStThreads) encode_stream_strided_kernel(Strea
     }
 }
 
-// 16-byte chunks, two per thread (chunks l and l + 32 of a warp's 64-chunk
-// block of one packet): every per-source cost (coefficient byte, table entry,
-// addresses) is paid once per 32 source bytes instead of 16.
-template <class Op, int KT>
+// 16-byte chunks, W (2 or 4) per thread (chunks l, l + 32, ... of a warp's
+// (32 W)-chunk block of one packet): every per-source cost (coefficient byte,
+// table entry, addresses) is paid once per 16 W source bytes instead of 16.
+template <class Op, int KT, int W>
 __global__ void __launch_bounds__(kStThreads) encode_stream_wide2_kernel(StreamParams p)
 {
     constexpr int kStBatch = Op::kBatch;
-    constexpr int W = 2;
     const size_t M16 = p.M16;
     const size_t stride = (size_t)gridDim.x * kStThreads;     // a multiple of 32: t & 31 is the lane
     for (size_t t = (size_t)blockIdx.x * kStThreads + threadIdx.x; t < p.total; t += stride) {
         const size_t blk = t >> 5;
         const size_t g = blk / p.wblocks;
-        const size_t c0 = (blk - g * p.wblocks) * 64 + (t & 31);
+        const size_t c0 = (blk - g * p.wblocks) * (32 * W) + (t & 31);
         bool ok[W];
 #pragma unroll
         for (int j = 0; j < W; j++) ok[j] = c0 + 32 * j < M16;

@@ -338,7 +338,8 @@ static int launch_stream_t(const StreamParams &p, cudaStream_t st)
     size_t grid = (p.total + kStThreads - 1) / kStThreads;
     if (grid > sms * 8) grid = sms * 8;                       // grid-stride: 8 CTAs of 256 per SM
     if constexpr (L == 0) encode_stream_kernel<Op, KT><<<(unsigned)grid, kStThreads, 0, st>>>(p);
-    else if constexpr (L == 3) encode_stream_wide2_kernel<Op, KT><<<(unsigned)grid, kStThreads, 0, st>>>(p);
+    else if constexpr (L == 3) encode_stream_wide2_kernel<Op, KT, 2><<<(unsigned)grid, kStThreads, 0, st>>>(p);
+    else if constexpr (L == 6) encode_stream_wide2_kernel<Op, KT, 4><<<(unsigned)grid, kStThreads, 0, st>>>(p);
     else if constexpr (L == 1) encode_stream_words_kernel<Op, KT, 1><<<(unsigned)grid, kStThreads, 0, st>>>(p);
     else if constexpr (L == 2) encode_stream_strided_kernel<Op, KT, 4><<<(unsigned)grid, kStThreads, 0, st>>>(p);
     else if constexpr (L == 4) encode_stream_strided_kernel<Op, KT, 8><<<(unsigned)grid, kStThreads, 0, st>>>(p);
@@ -362,6 +363,7 @@ static int launch_stream_f(const StreamParams &p, int layout, cudaStream_t st)
     if (layout == 2) return launch_stream_v<Op, 2>(p, st);
     if (layout == 4) return launch_stream_v<Op, 4>(p, st);
     if (layout == 5) return launch_stream_v<Op, 5>(p, st);
+    if (layout == 6) return launch_stream_v<Op, 6>(p, st);
     return launch_stream_v<Op, 3>(p, st);
 }
 
@@ -400,9 +402,18 @@ static int launch_stream(int field, int fi, const uint8_t *A, const uint8_t *C, 
         if (strided_wmax_env == 4 || strided_wmax_env == 8 || strided_wmax_env == 12) sw = strided_wmax_env;   // forced
         layout = sw == 12 ? 5 : sw == 8 ? 4 : 2;
     }
+    // 16-byte chunks, GF(16)/GF(256): 4 per thread (128-chunk blocks) when they
+    // cover >= 90% of the packet (NEXT-2 GF(256) 4.53 -> 4.70 TB/s, GF(16) 4.78
+    // -> 4.85; GF(4) loses 14% at 200 registers; profiles/r01_stream_wide4_v36.txt).
+    // GFRLNC_STREAM_WIDE4 = 0 / 1 turns it off / forces it (tests).
+    static const int wide4 = env_int("GFRLNC_STREAM_WIDE4", -1);
+    if (layout == 3 && wide4 != 0) {
+        const size_t m16 = M / 16, nb = (m16 + 127) / 128;
+        if (wide4 == 1 || (field >= 16 && m16 * 10 >= nb * 128 * 9)) layout = 6;
+    }
     p.A = A; p.C = C; p.B = B; p.N = N; p.K = K;
     p.M16 = wide ? M / 16 : M / 4;
-    p.wblocks = layout == 3 ? (p.M16 + 63) / 64 : (M / 4 + 32u * sw - 1) / (32u * sw);
+    p.wblocks = layout == 6 ? (p.M16 + 127) / 128 : layout == 3 ? (p.M16 + 63) / 64 : (M / 4 + 32u * sw - 1) / (32u * sw);
     p.total = layout >= 2 ? batch * p.wblocks * 32 : batch * p.M16;
     p.qmask = (uint32_t)field - 1u;
     switch (field) {

@@ -43,7 +43,7 @@ print("ok", want)
 
 
 @pytest.mark.parametrize("path", ["column", "lanek", "fused", "prow", "lanek2", "stream", "stream-strided",
-                                  "stream-strided8", "stream-strided12", "stream-wide2"])
+                                  "stream-strided8", "stream-strided12", "stream-wide2", "stream-wide4"])
 def test_forced_encode_path(path):
     import torch
     if not torch.cuda.is_available():
@@ -53,9 +53,10 @@ def test_forced_encode_path(path):
         wmax = path[len("stream-strided"):] or "4"
         path = "stream"
         env.update(GFRLNC_ENCODE_PATH=path, GFRLNC_STREAM_STRIDED_MIN_WORDS="1", GFRLNC_STREAM_STRIDED_W=wmax)
-    if path == "stream-wide2":     # 16-byte-aligned packets through the two-chunk kernel at any size
+    if path in ("stream-wide2", "stream-wide4"):   # 16-byte-aligned packets, 2 / 4 chunks per thread, any size
+        w4 = "1" if path == "stream-wide4" else "0"
         path = "stream"
-        env.update(GFRLNC_ENCODE_PATH=path, GFRLNC_STREAM_WIDE2_MIN_CHUNKS="1")
+        env.update(GFRLNC_ENCODE_PATH=path, GFRLNC_STREAM_WIDE2_MIN_CHUNKS="1", GFRLNC_STREAM_WIDE4=w4)
     out = subprocess.run([sys.executable, "-c", SCRIPT, path], env=env, capture_output=True, text=True,
                          timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
