@@ -205,8 +205,17 @@ static int launch_encode_field(int field, EncodeParams p, cudaStream_t st)
     switch (field) {
     case 256: return launch_encode_kt<256, 4, 16, BW>(p, st);
     case 16: return launch_encode_kt<16, 4, 16, BW>(p, st);
-    case 4: return launch_encode_kt<4, 2, 32, BW>(p, st);
-    case 2: return launch_encode_kt<2, 2, 32, BW>(p, st);
+    // GF(2) / GF(4): 4 words per lane (the table entries of each shared-memory
+    // load reused over twice the words) for K <= 8 (GF(2) also K <= 16 on long
+    // packets): N = 16, 1500 B, K = 8: GF(2) 2.32 -> 2.87 TB/s, GF(4) 1.57 ->
+    // 1.80; GF(2) K = 16 at 16 KiB 1.62 -> 1.85 (at 1500 B it loses 7%);
+    // profiles/r01_column_w4_v38.txt
+    case 4:
+        if (p.K <= 8) return launch_encode_kt<4, 4, 16, BW>(p, st);
+        return launch_encode_kt<4, 2, 32, BW>(p, st);
+    case 2:
+        if (p.K <= 8 || (p.K <= 16 && p.Mw >= 1024)) return launch_encode_kt<2, 4, 16, BW>(p, st);
+        return launch_encode_kt<2, 2, 32, BW>(p, st);
     default: return GF_EFIELD;
     }
 }
