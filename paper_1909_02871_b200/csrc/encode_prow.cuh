@@ -362,6 +362,7 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
         }
     };
     seta();
+    uint32_t gmask = vmask;                                    // words of the gather tile that exist
     load_a();                                                  // step 0
 
     uint4 acc[R][4];
@@ -381,6 +382,7 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
         for (int t = 0; t < kPrS; t++) col[t] = (uint32_t)(((jw + t) & (kPrS - 1)) * KC + kc * 16);
 #pragma unroll
         for (int r = 0; r < R; r++) {
+            if (!(gmask >> r & 1u)) continue;                  // past the packet end: no gathers (partial tiles)
 #pragma unroll
             for (int j = 0; j < 4; j++) {
                 const uint32_t sel = 0x5504u | (j << 4);
@@ -429,6 +431,11 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
 #pragma unroll
                 for (int j = 0; j < 4; j++) acc[r][j] = make_uint4(0u, 0u, 0u, 0u);
             }
+            const PrTile Tn = tile_of(j_g);                     // the next gather tile's words
+            gmask = 0;
+#pragma unroll
+            for (int r = 0; r < R; r++)
+                if (j_g < ntj && Tn.w0 + wbase + kRW * r < p.Mw) gmask |= 1u << r;
         }
     };
 
