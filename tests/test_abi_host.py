@@ -240,3 +240,20 @@ def test_encode_path_query():
     assert gf.encode_path(256, 64, 64, 1500, a_align=1) == "column-bytes"
     with pytest.raises(gf.GFError):
         gf.encode_path(3, 1, 1, 4)
+
+
+@pytest.mark.parametrize("q", (4, 16, 256))
+def test_corrupted_table_is_caught(q):
+    """SURVEY 4 negative test: one flipped bit in one coefficient's
+    split table makes the table-identity check (the emulated 3-PRMT lookup
+    against the oracle's products) fail."""
+    tabs = [list(t) for t in gf.host_tables(q)]
+    MB = oracle.mulbyte_table(q)
+    c = q - 1
+    tabs[c][1] ^= 1 << 9                        # T0[5] (byte 1 of word 1), bit 1
+    bad = 0
+    for v in range(256):
+        x = v * 0x01010101
+        y = lookup_word(tabs[c], x)
+        bad += y != int(MB[c, v]) * 0x01010101
+    assert bad > 0

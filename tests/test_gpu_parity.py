@@ -339,3 +339,18 @@ def test_encode_host_path(gfm, q, shape):
     L = gfm.lib()
     assert L.gf_encode_batch_host(q, Ah.data_ptr(), Ch.data_ptr(), Bh.data_ptr(), N, K, M, batch,
                                   ws.data_ptr(), 100) == gfm.GF_EARG
+
+
+@pytest.mark.parametrize("q", FIELDS)
+def test_encode_linear_in_coefficients_and_deterministic(gfm, q):
+    """SPEC invariants on the GPU, for the shapes of
+    every default kernel (streaming, column, product-row / lane-k): encode is
+    linear in C (encode(A, C1 + C2) = encode(A, C1) + encode(A, C2), + = XOR in
+    F_q) and repeated launches are bitwise identical."""
+    for (N, K, M, batch) in ((16, 1, 1024, 40), (16, 8, 1500, 5), (64, 64, 1500, 3), (32, 32, 4096, 2)):
+        A = si.random_bytes(91 + N, si.STREAM_A, 0, batch * N * M).reshape(batch, N, M)
+        C1 = si.uniform_coeffs(q, 92 + K, si.STREAM_C, 0, batch * N * K).reshape(batch, N, K)
+        C2 = si.uniform_coeffs(q, 93 + K, si.STREAM_C, 0, batch * N * K).reshape(batch, N, K)
+        B1, B2 = run_encode(gfm, q, A, C1), run_encode(gfm, q, A, C2)
+        assert np.array_equal(run_encode(gfm, q, A, C1 ^ C2), B1 ^ B2), (q, N, K, M)
+        assert np.array_equal(run_encode(gfm, q, A, C1), B1), (q, N, K, M)
