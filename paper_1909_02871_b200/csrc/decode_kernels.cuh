@@ -137,9 +137,9 @@ __global__ void __launch_bounds__(256) invert_kernel(InvertParams p)
 // the pivot row, so lane w computes those of pivot word w once per column
 // (from the byte-permuted word, so that the lookups come out in natural byte
 // order) and every row update reads them back with one broadcast LDS.128:
-// 3 PRMT + 2 LOP3 per row word instead of 12 ALU/FMA operations.  Eight
+// 3 PRMT + 2 LOP3 per row word instead of 12 ALU/FMA operations.  Twelve
 // matrices per CTA share the field tables.
-constexpr int kInvWarps = 8;
+constexpr int kInvWarps = 12;            // 12 x 8.4 KB matrices: two CTAs (24 warps) per SM (8: 1.21 ms, 12: 1.16 ms for 16384 64x64 inversions)
 
 __device__ __forceinline__ PrmtTab tab5_of(const uint32_t *stab, uint32_t c)
 {
