@@ -156,6 +156,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extra-fields", action="store_true")
+    ap.add_argument("--e2e-chunk-bytes", type=float, default=0.2e9,
+                    help="host bytes per pipeline chunk of the e2e (host-buffer) path")
     ap.add_argument("--chunk-gens", type=int, default=0,
                     help="generations per launch for configs that do not fit one GPU")
     return ap.parse_args()
@@ -499,7 +501,7 @@ def run_e2e(gf, torch, dist, cfg, q, sh, device, ws, args):
         Ah[j:j + n].copy_(tmpA[:n])
         Ch[j:j + n].copy_(tmpC[:n])
     del tmpA, tmpC
-    chunk = max(1, min(G, int(0.2e9 // per_gen_host)))
+    chunk = max(1, min(G, int(args.e2e_chunk_bytes // per_gen_host)))
     ws_t = torch.empty(gf.host_workspace_bytes(N, K, Ms, chunk), dtype=torch.uint8, device=device)
     torch.cuda.synchronize()
     gf.encode_batch_host(q, Ah, Ch, Bh, ws_t)
