@@ -165,10 +165,13 @@ int gf_host_tables(int field, uint32_t *out, size_t cap_words);
  * kernel on bytes (unaligned or M % 4 != 0), 2 = lane-k kernel with 32 coded
  * packets per CTA, 3 = lane-k kernel with 64, 4 / 5 = fused lane-k + column
  * kernel with 32 / 64, 6 = product-row kernel (GF(16)/GF(256), K > 32: C3,
- * C4; 9 / 10 = the same with 32 / 16 coded packets per CTA, K <= 32 / 16, also
- * GF(4) with 9 <= K < 24 on well-tiled packets), 7 = persistent lane-k (opt-in, GF(2)/GF(4), K <= 32), 8 = streaming
- * kernel (K <= 4: C1 and the paper's N = 16, K = 1 shape) (DESIGN.md
- * section 6), or GF_EFIELD / GF_EARG. */
+ * C4; 9 / 10 = the same with 32 / 16 coded packets per CTA, K <= 32 / 16,
+ * also GF(4) with 9 <= K < 24 on well-tiled packets), 7 = persistent lane-k
+ * (opt-in, GF(2)/GF(4), K <= 32), 8 = streaming kernel (K <= 4: C1 and the
+ * paper's N = 16, K = 1 shape; its chunk layout -- 16-byte chunks one, two
+ * or four per thread, or 4-byte words one or 4 / 12 strided per thread --
+ * follows from M, the alignment and the job size), or
+ * GF_EFIELD / GF_EARG. */
 int gf_encode_path(int field, int N, int K, size_t M, size_t a_align, size_t b_align);
 
 /* Harness-only (experiments, forced-path tests): force the encode kernel of
