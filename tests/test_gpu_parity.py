@@ -354,3 +354,21 @@ def test_encode_linear_in_coefficients_and_deterministic(gfm, q):
         B1, B2 = run_encode(gfm, q, A, C1), run_encode(gfm, q, A, C2)
         assert np.array_equal(run_encode(gfm, q, A, C1 ^ C2), B1 ^ B2), (q, N, K, M)
         assert np.array_equal(run_encode(gfm, q, A, C1), B1), (q, N, K, M)
+
+
+@pytest.mark.parametrize("q", FIELDS)
+def test_encode_empty_batch_and_packets(gfm, q):
+    """Degenerate sizes (batch == 0 or M == 0 returns GF_OK and
+    launches nothing): empty outputs, no error; and a canary-guarded B is left
+    untouched for batch == 0."""
+    for batch, N, K, M in ((0, 4, 3, 64), (2, 4, 3, 0), (0, 1, 1, 0)):
+        A = torch.zeros((batch, N, M), dtype=torch.uint8, device="cuda")
+        C = torch.ones((batch, N, K), dtype=torch.uint8, device="cuda")
+        B = gfm.encode_batch(q, A, C)
+        assert tuple(B.shape) == (batch, K, M)
+    L = gfm.lib()
+    canary = torch.full((16,), 0xA5, dtype=torch.uint8, device="cuda")
+    A = torch.zeros(16, dtype=torch.uint8, device="cuda")
+    rc = L.gf_encode_batch(q, A.data_ptr(), A.data_ptr(), canary.data_ptr(), 2, 2, 4, 0)
+    torch.cuda.synchronize()
+    assert rc == gfm.GF_OK and (canary.cpu().numpy() == 0xA5).all()
