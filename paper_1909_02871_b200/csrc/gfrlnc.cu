@@ -415,11 +415,17 @@ static int launch_stream(int field, int fi, const uint8_t *A, const uint8_t *C, 
     // cover >= 90% of the packet (NEXT-2 GF(256) 4.53 -> 4.70 TB/s, GF(16) 4.78
     // -> 4.85; GF(4) loses 14% at 200 registers; profiles/r01_stream_wide4_v36.txt).
     // GFRLNC_STREAM_WIDE4 = 0 / 1 turns it off / forces it (tests).
+    // With several coded packets the accumulators multiply: four chunks only for
+    // K = 1 (GF(256) K = 2 too), and GF(16) with K >= 3 back to one chunk per
+    // thread (N = 16, 4 KiB: GF(16) K = 2 2.22 -> 2.73 TB/s, K = 4 1.19 -> 1.37;
+    // GF(256) K = 4 1.21 -> 1.40; profiles/r01_stream_k2to4_v47.txt).
     static const int wide4 = env_int("GFRLNC_STREAM_WIDE4", -1);
     if (layout == 3 && wide4 != 0) {
         const size_t m16 = M / 16, nb = (m16 + 127) / 128;
-        if (wide4 == 1 || (field >= 16 && m16 * 10 >= nb * 128 * 9)) layout = 6;
+        const bool few_k = K == 1 || (field == 256 && K == 2);
+        if (wide4 == 1 || (field >= 16 && few_k && m16 * 10 >= nb * 128 * 9)) layout = 6;
     }
+    if (layout == 3 && wide4 != 1 && field == 16 && K >= 3) layout = 0;
     p.A = A; p.C = C; p.B = B; p.N = N; p.K = K;
     p.M16 = wide ? M / 16 : M / 4;
     p.wblocks = layout == 6 ? (p.M16 + 127) / 128 : layout == 3 ? (p.M16 + 63) / 64 : (M / 4 + 32u * sw - 1) / (32u * sw);
