@@ -35,17 +35,18 @@
 //     wait BUILT(s), gather step s from table s % 3, prefetch the source words
 //     of step s+1 straight from global memory, write the tile back when s ends
 //     it (4x4 byte transpose, 4-byte stores), arrive DONE(s);
-//   * 4 producer warps (56 registers): wait DONE(s-2) (table buffer free),
-//     basis rows P[2^b] = C * x^b of step s+1 (packed xtime chain, coefficient
-//     words prefetched a step ahead), named barrier among the producers, then
-//     thread (chunk c16, h) writes rows 32 h .. 32 h + 31 in Gray-code order,
-//     one 16-B XOR per row (P[a] = XOR_{b in a} P[2^b], GF(2)-linearity of the
-//     product); arrive BUILT(s+1).
+//   * 4 producer warps (56 registers): wait DONE(s-3) (table buffer free);
+//     thread (chunk c16, h) derives its chunk's basis rows P[2^b] = C * x^b
+//     from the chunk's 16 coefficient bytes (packed xtime chain in registers,
+//     coefficients prefetched a step ahead) and writes rows 32 h .. 32 h + 31
+//     in Gray-code order, one 16-B XOR per row (P[a] = XOR_{b in a} P[2^b],
+//     GF(2)-linearity of the product); arrive BUILT(s).  (Computing the basis
+//     once per chunk into shared memory and reading it back cost 4% of the
+//     wavefronts and a producer barrier: C3 396.8 -> 409.7 GB/s without.)
 // Three table buffers at compile-time shared addresses (the gatherer loop is
 // unrolled three times so the table base is the LDS immediate), mbarrier
 // rings of four objects; producers may run two steps ahead.
-// Build + basis traffic per step: 64 KiB + 4 KiB against 4 x 4 x 384 x 64 B
-// of gathers (17%).
+// Build traffic per step: 64 KiB against 4 x 4 x 384 x 64 B of gathers (17%).
 #pragma once
 #include <cstdint>
 
@@ -73,9 +74,7 @@ template <int KC> struct PrCfg {
 };
 constexpr uint32_t kPrBar = 0x0400u;          // mbarriers: BUILT[4], DONE[4] at the dynamic window base
 constexpr uint32_t kPrTab0 = 0x1000u;         // tables u = 0, 1, 2 at kPrTab0 + u * 0x10000
-constexpr uint32_t kPrBasis = 0x31000u;       // basis rows: 2 buffers x 8 x 256 B
-constexpr int kPrBasisBytes = 8 * 256;
-constexpr uint32_t kPrSmemEnd = kPrBasis + 2 * kPrBasisBytes;
+constexpr uint32_t kPrSmemEnd = kPrTab0 + 3 * 0x10000u;
 
 struct ProwParams {
     const uint8_t *A;
@@ -222,30 +221,37 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
         // ======================= producers: basis rows + tables
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" :: "n"(kPrPRegs));
         const int pt = tid - kPrGW * 32;                       // 0 .. 127
-        // basis geometry: coefficient word (chunk cc16 = source cc16 / NKC, coefficient
-        // chunk cc16 % NKC; word cwq), bits b0, b0+2, b0+4, b0+6
-        const int cwq = pt & 3, cc16 = (pt >> 2) & 15, b0 = pt >> 6;
-        // coefficient cursor: &C[g][S st + cc16 / NKC][k0 + 16 (cc16 % NKC) + 4 cwq]
+        // thread (chunk c16, row group h3): table rows 32 h3 .. 32 h3 + 31 of the
+        // 16-byte chunk c16 = (source c16 / NKC, coefficient chunk c16 % NKC).
+        // Each thread derives its chunk's 8 basis rows P[2^b] = C * x^b itself
+        // from the 16 raw coefficient bytes (packed xtime chain in registers):
+        // no shared-memory basis buffer, no producer barrier.
+        const int c16 = pt & 15, h3 = pt >> 4;
+        const int csrc = c16 / NKC, ckc = c16 % NKC;
+        const bool c16ok = p.K % 16 == 0 && (reinterpret_cast<uintptr_t>(p.C) & 15u) == 0;
+        // coefficient cursor: &C[g][S st + csrc][k0 + 16 ckc]
         uint32_t cj = 0;
         int cst = 0;
         const uint8_t *cptr = nullptr;
+        int ck = 0;
         bool kok = false;
         auto setc = [&]() {
             const PrTile T = tile_of(cj);
-            const int k = T.k0 + 16 * (cc16 % NKC) + 4 * cwq;
-            cptr = p.C + (T.g * (size_t)p.N + (size_t)(cc16 / NKC)) * p.K + k;
-            kok = cj < ntj && k < p.K;
+            ck = T.k0 + 16 * ckc;
+            cptr = p.C + (T.g * (size_t)p.N + (size_t)csrc) * p.K + ck;
+            kok = cj < ntj && ck < p.K;
         };
-        auto load_c = [&]() -> uint32_t {                      // raw word of the cursor's step
-            uint32_t c = 0;
-            if (kok && kPrS * cst + (cc16 / NKC) < p.N) {
-                if (p.cword) {
-                    c = __ldg(reinterpret_cast<const uint32_t *>(cptr));
+        auto load_c = [&]() -> uint4 {                         // 16 raw coefficient bytes of the cursor's step
+            uint4 c = make_uint4(0u, 0u, 0u, 0u);
+            if (kok && kPrS * cst + csrc < p.N) {
+                if (c16ok) {
+                    c = __ldg(reinterpret_cast<const uint4 *>(cptr));
                 } else {
-                    const int k = (int)((size_t)(cptr - p.C) % (size_t)p.K);   // K % 4 != 0: rare
+                    uint32_t wv[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-                    for (int e = 0; e < 4; e++)
-                        if (k + e < p.K) c |= (uint32_t)__ldg(cptr + e) << (8 * e);
+                    for (int e = 0; e < 16; e++)
+                        if (ck + e < p.K) wv[e >> 2] |= (uint32_t)__ldg(cptr + e) << (8 * (e & 3));
+                    c = make_uint4(wv[0], wv[1], wv[2], wv[3]);
                 }
             }
             if (++cst == p.NS) {
@@ -257,36 +263,29 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
             }
             return c;
         };
-        auto basis = [&](uint32_t craw, uint32_t buf) {
+        auto build = [&](const uint4 craw, uint32_t tab) {
             constexpr int w = F == 256 ? 8 : F == 16 ? 4 : F == 4 ? 2 : 1;
-            uint32_t xt[w];
-            xt[0] = craw & p.qmask4;
+            uint32_t bvw[5][4], vw[4];
 #pragma unroll
-            for (int e = 1; e < w; e++) xt[e] = pr_xtime<F>(xt[e - 1]);
-            const uint32_t dst = kPrBasis + buf * kPrBasisBytes + cc16 * 16 + cwq * 4;
+            for (int q = 0; q < 4; q++) {
+                // basis bit b of coefficient word q: slot b / w holds c * x^(b mod w)
+                uint32_t xt[w];
+                xt[0] = u4c(craw, q) & p.qmask4;
 #pragma unroll
-            for (int v = 0; v < 4; v++) {
-                // bit b = b0 + 2v: slot b / w, power b % w (b0 is warp-uniform)
-                const int be = 2 * v, bo = 2 * v + 1;
-                const uint32_t ve = xt[be % w] << ((be / w) * w), vo = xt[bo % w] << ((bo / w) * w);
-                asm volatile("st.shared.u32 [%0], %1;" :: "r"(dst + (b0 + 2 * v) * 256), "r"(b0 ? vo : ve)
-                             : "memory");
+                for (int e = 1; e < w; e++) xt[e] = pr_xtime<F>(xt[e - 1]);
+                uint32_t vq = 0u;
+#pragma unroll
+                for (int bb = 0; bb < 8; bb++) {
+                    const uint32_t rb = xt[bb % w] << ((bb / w) * w);
+                    if (bb < 5) bvw[bb][q] = rb;
+                    else vq ^= rb & (0u - ((uint32_t)(h3 >> (bb - 5)) & 1u));   // rows 5..7 selected by h3
+                }
+                vw[q] = vq;
             }
-        };
-        // table of step x: thread (chunk c16, h) -> rows 32 h + Gray(0..31)
-        const int c16 = pt & 15, h3 = pt >> 4;
-        auto build = [&](uint32_t bbuf, uint32_t tab) {
-            const uint32_t bsrc = kPrBasis + bbuf * kPrBasisBytes + c16 * 16;
-            uint4 v = make_uint4(0u, 0u, 0u, 0u);
-#pragma unroll
-            for (int j = 0; j < 3; j++) {
-                const uint4 b = lds128(bsrc + (5 + j) * 256);
-                const uint32_t m = 0u - ((uint32_t)(h3 >> j) & 1u);
-                v.x ^= b.x & m; v.y ^= b.y & m; v.z ^= b.z & m; v.w ^= b.w & m;
-            }
+            uint4 v = make_uint4(vw[0], vw[1], vw[2], vw[3]);
             uint4 bv[5];
 #pragma unroll
-            for (int j = 0; j < 5; j++) bv[j] = lds128(bsrc + j * 256);
+            for (int j = 0; j < 5; j++) bv[j] = make_uint4(bvw[j][0], bvw[j][1], bvw[j][2], bvw[j][3]);
             const uint32_t tb = tab + (uint32_t)h3 * 32u * 256u + (uint32_t)c16 * 16u;
             sts128(tb, v);
 #pragma unroll
@@ -298,20 +297,13 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
         };
 
         setc();
-        basis(load_c(), 0);                                     // step 0
-        uint32_t creg = load_c();                               // step 1
-        nbar_sync_n(1, kPrPW * 32);
-        build(0, kPrTab0);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(kBuilt);                     // BUILT(0)
+        uint4 creg = load_c();                                  // step 0
 #pragma unroll 1
-        for (uint32_t x = 1; x < total; x++) {                  // table of step x
+        for (uint32_t x = 0; x < total; x++) {                  // table of step x
             mbar_wait_sleepy(kDone + ((x - 3) & 3u) * 8u, ((x + 1) >> 2) & 1u);   // DONE(x-3): buffer free
-            const uint32_t c = creg;
+            const uint4 c = creg;
             creg = load_c();                                    // step x + 1
-            basis(c, x & 1u);
-            nbar_sync_n(1, kPrPW * 32);
-            build(x & 1u, kPrTab0 + (x % 3u) * 0x10000u);
+            build(c, kPrTab0 + (x % 3u) * 0x10000u);
             __syncwarp();
             if (lane == 0) mbar_arrive(kBuilt + (x & 3u) * 8u);
         }
