@@ -40,7 +40,8 @@
 //     from the chunk's 16 coefficient bytes (packed xtime chain in registers,
 //     coefficients prefetched a step ahead) and writes rows 32 h .. 32 h + 31
 //     in Gray-code order, one 16-B XOR per row (P[a] = XOR_{b in a} P[2^b],
-//     GF(2)-linearity of the product); arrive BUILT(s).  (Computing the basis
+//     GF(2)-linearity of the product); arrive BUILT(s); one of them issues
+//     an L2 bulk prefetch of the source rows of step s + 2.  (Computing the basis
 //     once per chunk into shared memory and reading it back cost 4% of the
 //     wavefronts and a producer barrier: C3 396.8 -> 409.7 GB/s without.)
 // Three table buffers at compile-time shared addresses (the gatherer loop is
@@ -296,10 +297,33 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
             }
         };
 
+        // L2 prefetch of the gatherers' source rows: one bulk prefetch per
+        // source row segment of step x + PD (the producers run up to three steps
+        // ahead of the gatherers, whose per-lane loads then hit L2, not HBM)
+        constexpr uint32_t PD = 2;
+        auto prefetch_step = [&](uint32_t x) {
+            const uint32_t j = x / (uint32_t)p.NS, st = x - j * (uint32_t)p.NS;
+            if (j >= ntj) return;
+            const PrTile T = tile_of(j);
+            const uint32_t nw = min((uint32_t)kPrTW, p.Mw - T.w0);
+            const uint8_t *row0 = p.A + T.g * (size_t)p.N * p.M + 4 * (size_t)T.w0;
+#pragma unroll
+            for (int t = 0; t < kPrS; t++) {
+                const int i = kPrS * (int)st + t;
+                if (i >= p.N) break;
+                const uintptr_t a = reinterpret_cast<uintptr_t>(row0 + (size_t)i * p.M);
+                const uintptr_t a0 = a & ~(uintptr_t)15, a1 = (a + 4 * (uintptr_t)nw + 15) & ~(uintptr_t)15;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
+            }
+        };
+        if (pt == 0)
+            for (uint32_t x = 1; x < PD; x++) prefetch_step(x);
+
         setc();
         uint4 creg = load_c();                                  // step 0
 #pragma unroll 1
         for (uint32_t x = 0; x < total; x++) {                  // table of step x
+            if (pt == 0) prefetch_step(x + PD);
             mbar_wait_sleepy(kDone + ((x - 3) & 3u) * 8u, ((x + 1) >> 2) & 1u);   // DONE(x-3): buffer free
             const uint4 c = creg;
             creg = load_c();                                    // step x + 1
