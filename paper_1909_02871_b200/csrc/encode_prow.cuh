@@ -30,12 +30,12 @@
 // Warp specialisation.  Persistent CTAs (one per SM) of 16 warps walk a
 // flattened sequence of steps over their tiles (generation x 64 coded packets
 // x 384 words):
-//   * 12 gatherer warps (152 registers each, setmaxnreg): lane = (word,
+//   * 12 gatherer warps (144 registers each, setmaxnreg): lane = (word,
 //     16-coefficient chunk), 4 words per lane, 64 accumulator registers;
 //     wait BUILT(s), gather step s from table s % 3, prefetch the source words
 //     of step s+1 straight from global memory, write the tile back when s ends
 //     it (4x4 byte transpose, 4-byte stores), arrive DONE(s);
-//   * 4 producer warps (56 registers): wait DONE(s-3) (table buffer free);
+//   * 4 producer warps (80 registers): wait DONE(s-3) (table buffer free);
 //     thread (chunk c16, h) derives its chunk's basis rows P[2^b] = C * x^b
 //     from the chunk's 16 coefficient bytes (packed xtime chain in registers,
 //     coefficients prefetched a step ahead) and writes rows 32 h .. 32 h + 31
@@ -58,7 +58,7 @@ namespace gfr {
 constexpr int kPrThreads = 512;
 constexpr int kPrGW = 12;                     // gatherer warps (warps 0..11)
 constexpr int kPrPW = 4;                      // producer warps (warps 12..15, one warpgroup)
-constexpr int kPrGRegs = 152, kPrPRegs = 56;  // setmaxnreg budgets: 12*32*152 + 4*32*56 = 65536
+constexpr int kPrGRegs = 144, kPrPRegs = 80;  // setmaxnreg budgets: 12*32*144 + 4*32*80 = 65536 (80: no producer spill)
 constexpr int kPrTW = 384;                    // words per tile
 // Coded packets per CTA (KC = 64, or 32 for K <= 32): a table row (one source
 // byte value) is 256 B = S sources x KC products, so a step covers S = 256 / KC
@@ -307,6 +307,11 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
             const PrTile T = tile_of(j);
             const uint32_t nw = min((uint32_t)kPrTW, p.Mw - T.w0);
             const uint8_t *row0 = p.A + T.g * (size_t)p.N * p.M + 4 * (size_t)T.w0;
+            if (st == 0) {                                      // a new tile: its coefficient block too
+                const uintptr_t c = reinterpret_cast<uintptr_t>(p.C + T.g * (size_t)p.N * p.K);
+                const uintptr_t c0 = c & ~(uintptr_t)15, c1 = (c + (uintptr_t)p.N * p.K + 15) & ~(uintptr_t)15;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(c0), "r"((uint32_t)(c1 - c0)) : "memory");
+            }
 #pragma unroll
             for (int t = 0; t < kPrS; t++) {
                 const int i = kPrS * (int)st + t;
