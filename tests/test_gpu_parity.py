@@ -372,3 +372,25 @@ def test_encode_empty_batch_and_packets(gfm, q):
     rc = L.gf_encode_batch(q, A.data_ptr(), A.data_ptr(), canary.data_ptr(), 2, 2, 4, 0)
     torch.cuda.synchronize()
     assert rc == gfm.GF_OK and (canary.cpu().numpy() == 0xA5).all()
+
+
+@pytest.mark.parametrize("q", FIELDS)
+def test_encode_guard_bytes_every_layout(gfm, q):
+    """Out-of-bounds write check standing in for compute-sanitizer (closed on
+    this pool): B is a view inside a buffer of 0xEE guard bytes (4 KiB before
+    and after); every default kernel / layout on ragged shapes (partial
+    product-row tiles, 2- and 4-chunk streaming blocks, strided word blocks,
+    lane-k tiles) must leave the guards untouched and match the oracle."""
+    shapes = [(64, 64, 1500, 3), (16, 16, 2052, 4), (16, 1, 2064, 5), (16, 1, 65552, 2),
+              (16, 2, 1500, 3), (32, 32, 4100, 2), (9, 20, 1500, 3), (16, 8, 1508, 3)]
+    for (N, K, M, batch) in shapes:
+        A = si.random_bytes(101 + N, si.STREAM_A, 0, batch * N * M).reshape(batch, N, M)
+        C = si.uniform_coeffs(q, 102 + K, si.STREAM_C, 0, batch * N * K).reshape(batch, N, K)
+        guard = 4096
+        nb = batch * K * M
+        buf = torch.full((nb + 2 * guard,), 0xEE, dtype=torch.uint8, device="cuda")
+        Bv = buf[guard:guard + nb].view(batch, K, M)
+        gfm.encode_batch(q, dev(A), dev(C), Bv)
+        got = buf.cpu().numpy()
+        assert (got[:guard] == 0xEE).all() and (got[guard + nb:] == 0xEE).all(), (q, N, K, M)
+        assert np.array_equal(got[guard:guard + nb].reshape(batch, K, M), oracle.encode_batch(q, A, C)), (q, N, K, M)
