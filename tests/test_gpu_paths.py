@@ -36,7 +36,13 @@ for q, (N, K, M, batch) in cases:
     C = si.uniform_coeffs(q, 8 + K, 2, 0, batch * N * K).reshape(batch, N, K)
     path = gf.encode_path(q, N, K, M)
     assert path.startswith(want), (path, want)
-    got = gf.encode_batch(q, torch.from_numpy(A).cuda(), torch.from_numpy(C).cuda()).cpu().numpy()
+    # B inside 0xEE guard bytes: no kernel may write outside its output
+    nb = batch * K * M
+    buf = torch.full((nb + 8192,), 0xEE, dtype=torch.uint8, device="cuda")
+    gf.encode_batch(q, torch.from_numpy(A).cuda(), torch.from_numpy(C).cuda(), buf[4096:4096 + nb].view(batch, K, M))
+    allb = buf.cpu().numpy()
+    assert (allb[:4096] == 0xEE).all() and (allb[4096 + nb:] == 0xEE).all(), ("guard", q, N, K, M, path)
+    got = allb[4096:4096 + nb].reshape(batch, K, M)
     assert np.array_equal(got, oracle.encode_batch(q, A, C)), (q, N, K, M, path)
 print("ok", want)
 ''' % ROOT
