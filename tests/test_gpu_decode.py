@@ -87,3 +87,35 @@ def test_decode_errors(gfm):
     assert L.gf_invert_batch(256, p, p + 32, None, 300, 1) == gfm.GF_EARG
     assert L.gf_invert_batch(256, p, p + 8, None, 4, 1) == gfm.GF_EOVERLAP
     assert L.gf_decode_batch(256, p, p + 16, p + 32, None, 4, 4, 1, p + 48, 8) == gfm.GF_EARG
+
+
+@pytest.mark.parametrize("q", (2, 256))
+@pytest.mark.parametrize("N", (5, 33, 64, 65))
+def test_invert_and_decode_guard_bytes(gfm, q, N):
+    """Out-of-bounds write check (compute-sanitizer is closed on this pool):
+    D, rank and the decoded A sit inside 0xEE / -7 guard regions that the warp-
+    and CTA-per-matrix inversions and the decode must leave untouched."""
+    batch, M = 13, 1500
+    C = si.uniform_coeffs(q, 201 + N, si.STREAM_C, 0, batch * N * N).reshape(batch, N, N)
+    Cd = torch.from_numpy(C).cuda()
+    L = gfm.lib()
+    g = 4096
+    dbuf = torch.full((batch * N * N + 2 * g,), 0xEE, dtype=torch.uint8, device="cuda")
+    rbuf = torch.full((batch + 64,), -7, dtype=torch.int32, device="cuda")
+    rc = L.gf_invert_batch(q, Cd.data_ptr(), dbuf.data_ptr() + g, rbuf.data_ptr() + 4 * 32, N, batch)
+    torch.cuda.synchronize()
+    assert rc == gfm.GF_OK
+    d = dbuf.cpu().numpy()
+    r = rbuf.cpu().numpy()
+    assert (d[:g] == 0xEE).all() and (d[g + batch * N * N:] == 0xEE).all()
+    assert (r[:32] == -7).all() and (r[32 + batch:] == -7).all()
+    assert (r[32:32 + batch] == [oracle.rank(q, C[i]) for i in range(batch)]).all()
+    B = si.random_bytes(202 + N, si.STREAM_A, 0, batch * N * M).reshape(batch, N, M)
+    abuf = torch.full((batch * N * M + 2 * g,), 0xEE, dtype=torch.uint8, device="cuda")
+    ws = torch.empty(batch * N * N, dtype=torch.uint8, device="cuda")
+    rc = L.gf_decode_batch(q, torch.from_numpy(B).cuda().data_ptr(), Cd.data_ptr(), abuf.data_ptr() + g,
+                           rbuf.data_ptr() + 4 * 32, N, M, batch, ws.data_ptr(), ws.numel())
+    torch.cuda.synchronize()
+    assert rc == gfm.GF_OK
+    a = abuf.cpu().numpy()
+    assert (a[:g] == 0xEE).all() and (a[g + batch * N * M:] == 0xEE).all()
