@@ -1,19 +1,29 @@
 #!/usr/bin/env python
-"""bench.py -- RLNC encode throughput on B200 (source GB/s), driver contract.
+"""bench.py -- RLNC encode throughput on B200 (source GB/s per field), driver contract.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--field 256]
     python bench.py --impl reference ...        (the CPU oracle, rank 0 only)
 
-A step is one gf_encode_batch launch over the whole workload batch (the full
-hot path: per-coefficient tables, trivial-coefficient handling and the
-N x K x M multiply-add of Eq. 2).  Default workload: C3 =
-BASELINE.json configs[2] over GF(256) (N=64, M=1500, K=64, 65536 generations),
-the largest RLNC-encode config that fits one GPU unchunked; the same run also
-times GF(16) (C3's other field) under "per_field".
+A step is one gf_encode_batch launch over this rank's share of the workload
+(the whole hot path: per-coefficient tables, the N x K x M multiply-add of
+Eq. 2, output written).  Headline workload: C3 =
+BASELINE.json configs[2] over GF(256) (N=64, M=1500, K=64, 65536
+generations); "per_field" adds GF(16) on the same C3 job and GF(2) / GF(4)
+on the whole C5 job (configs[4]: N=K=32, 1 MiB packets, 4096 generations,
+launched in chunks of generations because it does not fit one GPU).
 
-Multi-GPU (torchrun, one process per GPU): every rank encodes its own 65536
-generations (generation-sharded, no collective on the data path), so
-"scaling" is "weak"; value = all ranks' source bytes / max-over-ranks time.
+Multi-GPU: `--gpus N` without torchrun re-launches itself under
+torch.distributed.run with N ranks (one process per GPU); under torchrun the
+world size must equal --gpus.  The BASELINE job is SPLIT across ranks
+(SURVEY.md 8(e)): C3 / C5 by generation (65536 / N, 4096 / N), C4 by packet
+byte range; no collective on the data path, NCCL only for the barrier, the
+max-over-ranks time and the parity gate.  "scaling" is "strong".
+
+Verification gate: after the timed loop every rank
+checks its timed output on the device (gf_verify_batch, Freivalds projections
+over sampled generations); rank 0's cpu_baseline leg also compares the
+oracle's result on its sample with the GPU's bytes.  Any mismatch prints
+"parity": "FAIL" and exits 2.
 
 The oracle is used only by the cpu_baseline leg and by --impl reference.
 """
@@ -22,6 +32,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -34,10 +45,16 @@ import seeded_inputs as si  # noqa: E402
 
 METRIC = "source GB/s per field for RLNC encode at 1/2/4/8 B200; % of HBM roofline"
 ALU_LANES_PER_SM_CLK = 64     # B300_MICROARCH.md: alu pipe rt_SMSP = 2 -> 16 lanes/clk/SMSP x 4
+ISSUE_LANES_PER_SM_CLK = 128  # 4 SMSPs x 1 warp-instruction / clk x 32 lanes
 N_SM = 148
-# algorithmic ALU ops per byte-madd of the inner loop:
+SMEM_BYTES_PER_SM_CLK = 128   # shared-memory pipe (tools/ubench_smem.cu, profiles/r01_ubench_smem.txt)
+# algorithmic ALU ops per byte-madd of the column kernel's inner loop:
 # GF(256)/GF(16) 3 PRMT + 2 LOP3 per 4 byte-madds; GF(4) 2 LOP3; GF(2) 1 LOP3
 OPS_PER_BYTE_MADD = {256: 5 / 4, 16: 5 / 4, 4: 2 / 4, 2: 1 / 4}
+# GF(2) split engine (encode_gf2.cuh): per (source word, coded packet) 21 LOP3 +
+# 22 IMAD per 32 terms -> issue slots per byte-madd (a 4-byte word = 4 byte-madds)
+GF2_SPLIT_ISSUE_PER_BYTE_MADD = 43 / 32 / 4
+LANEK = {2: (4, 1, 15), 4: (2, 1, 15), 16: (1, 1, 15), 256: (1, 2, 30)}   # SG, gathers/unit, build rows
 
 
 def load_peaks():
@@ -100,9 +117,13 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- oracle baseline
 
-def cpu_baseline(cfg, q, seconds_target=12.0):
-    """The oracle (scalar C, plain loops), as it stands, on a bounded sample
-    of the same workload, on this host's cores."""
+def cpu_baseline(cfg, q, seconds_target=12.0, gpu_B=None):
+    """The oracle (scalar C, plain loops), as it stands, on a bounded sample of
+    the same workload (the first generations of the job), on this host's cores.
+    gpu_B(g0, g1) -> host uint8 [g1-g0, K, M]: when given, the oracle's bytes
+    are also compared with the GPU's for the sample (the bench's parity gate)."""
+    import numpy as np
+
     import oracle
     cores = len(os.sched_getaffinity(0))
     per_gen = cfg.N * cfg.K * cfg.M
@@ -117,13 +138,20 @@ def cpu_baseline(cfg, q, seconds_target=12.0):
     gens = max(1, min(gens, cfg.batch))
     A, C = si.encode_inputs(cfg, q, 0, gens)
     t0 = time.perf_counter()
-    oracle.encode_batch(q, A, C, threads=cores)
+    Bo = oracle.encode_batch(q, A, C, threads=cores)
     dt = time.perf_counter() - t0
     src = gens * cfg.N * cfg.M
-    return {"value": round(src / dt / 1e9, 4), "unit": "GB/s", "cores": cores, "kind": "oracle",
-            "sample": f"{gens} of {cfg.batch} generations of {cfg.name} GF({q}), threads={cores}; "
-                      f"1-thread rate {g_cal * cfg.N * cfg.M / t1 / 1e9:.4f} GB/s",
-            "seconds": round(dt, 2)}
+    out = {"value": round(src / dt / 1e9, 4), "unit": "GB/s", "cores": cores, "kind": "oracle",
+           "sample": f"{gens} of {cfg.batch} generations of {cfg.name} GF({q}), threads={cores}; "
+                     f"1-thread rate {g_cal * cfg.N * cfg.M / t1 / 1e9:.4f} GB/s",
+           "seconds": round(dt, 2), "cpu_model": cpu_model()}
+    if gpu_B is not None:
+        bad = 0
+        for g0 in range(0, gens, 1024):                # chunked: no second full-size copy
+            g1 = min(gens, g0 + 1024)
+            bad += int(np.count_nonzero(gpu_B(g0, g1) != Bo[g0:g1]))
+        out["parity_vs_gpu"] = {"generations": gens, "mismatched_bytes": bad}
+    return out
 
 
 def cpu_model():
@@ -145,7 +173,7 @@ def dist_env():
     return ws, rank, local
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -159,13 +187,36 @@ def parse():
     ap.add_argument("--e2e-chunk-bytes", type=float, default=0.2e9,
                     help="host bytes per pipeline chunk of the e2e (host-buffer) path")
     ap.add_argument("--chunk-gens", type=int, default=0,
-                    help="generations per launch for configs that do not fit one GPU")
-    return ap.parse_args()
+                    help="generations per launch for jobs that do not fit one GPU")
+    ap.add_argument("--verify-gens", type=int, default=256,
+                    help="generations per launch checked on the device after the timed loop")
+    return ap.parse_args(argv)
 
 
-def workload_name(cfg, q, batch_per_rank):
+def relaunch_under_torchrun(args) -> int:
+    """--gpus N > 1 without a torchrun environment: start N ranks (one process
+    per GPU) through torch.distributed.run on this node and return its code."""
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def workload_name(cfg, q, gens, ws, by_bytes):
+    split = (f"byte-range sharded over {ws} GPU(s)" if by_bytes else
+             f"{cfg.batch} generations split over {ws} GPU(s), {gens} per GPU")
     return (f"{cfg.name} RLNC encode GF({q}): N={cfg.N} source packets x M={cfg.M} B, "
-            f"K={cfg.K} coded, {batch_per_rank} generations per GPU")
+            f"K={cfg.K} coded, {split}")
+
+
+def rank_shard(shard, cfg, ws, rank):
+    """This rank's part of the BASELINE job: by generation for
+    C1 / C3 / C5, by packet byte range for C4 (cfg.shard)."""
+    by_bytes = cfg.shard == "bytes"
+    return shard.plan(cfg.batch, cfg.M, ws, rank, by="bytes" if by_bytes else "generation"), by_bytes
 
 
 # ---------------------------------------------------------------- reference arm
@@ -200,10 +251,10 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * tot / args.steps, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "scaling": "strong", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic (seeded splitmix64 byte stream, seeded_inputs)",
-        "config": {"workload": workload_name(cfg, q, cfg.batch), "N": cfg.N, "K": cfg.K, "M": cfg.M,
-                   "batch": cfg.batch, "field": q},
+        "config": {"workload": workload_name(cfg, q, cfg.batch, 1, cfg.shard == "bytes"), "N": cfg.N,
+                   "K": cfg.K, "M": cfg.M, "batch": cfg.batch, "field": q},
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": "oracle",
                          "sample": f"{gens} generations per step of {cfg.name} GF({q}) "
                                    f"(scalar C oracle, {cores} threads, {cpu_model()})"},
@@ -214,6 +265,105 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+# ---------------------------------------------------------------- one workload on this rank
+
+class Job:
+    """This rank's share of one BASELINE workload over one field, resident in
+    HBM in chunks of generations (one chunk when it fits)."""
+
+    def __init__(self, gf, torch, cfg, q, sh, device, chunk_gens=0, mem_frac=0.8):
+        self.gf, self.torch, self.cfg, self.q, self.sh, self.device = gf, torch, cfg, q, sh, device
+        G, Ms, N, K = sh.generations, sh.columns, cfg.N, cfg.K
+        self.G, self.Ms = G, Ms
+        free, _ = torch.cuda.mem_get_info(device)
+        per_gen = (N + K) * Ms + N * K
+        chunk = min(G, chunk_gens or G)
+        if per_gen * chunk > mem_frac * free:
+            chunk = max(1, int(mem_frac * free // per_gen))
+        self.chunk = chunk
+        self.nchunks = -(-G // chunk) if G else 0
+        self.A = torch.empty((chunk, N, Ms), dtype=torch.uint8, device=device)
+        self.C = torch.empty((chunk, N, K), dtype=torch.uint8, device=device)
+        self.B = torch.empty((chunk, K, Ms), dtype=torch.uint8, device=device)
+        self.filled = -1
+
+    def fill(self, j):
+        """Inputs of chunk j, generated on the device by absolute index."""
+        cfg, q, sh = self.cfg, self.q, self.sh
+        seed = si.field_seed(cfg, q)
+        g = sh.g0 + j * self.chunk
+        n = min(self.chunk, self.G - j * self.chunk)
+        self.gf.fill_random2d(self.A[:n].view(n * cfg.N, self.Ms), seed, si.STREAM_A,
+                              g * cfg.N * cfg.M + sh.m0, cfg.M)
+        self.gf.fill_random(self.C[:n], seed, si.STREAM_C, g * cfg.N * cfg.K, mask=q - 1)
+        self.filled = j
+        return n
+
+    def encode(self, n):
+        self.gf.encode_batch(self.q, self.A[:n], self.C[:n], self.B[:n])
+
+    def verify(self, n, max_gens):
+        """Freivalds check of the chunk's B on the device (gf_verify_batch) for
+        up to max_gens generations spread over the chunk; returns the number of
+        mismatching bytes."""
+        torch, gf, q = self.torch, self.gf, self.q
+        step = max(1, n // max(1, max_gens))
+        idx = torch.arange(0, n, step, device=self.device)[:max_gens]
+        t = gf.freivalds_trials(q)
+        A, C, B = self.A[idx].contiguous(), self.C[idx].contiguous(), self.B[idx].contiguous()
+        R = torch.empty((idx.numel(), self.cfg.K, t), dtype=torch.uint8, device=self.device)
+        gf.fill_random(R, si.field_seed(self.cfg, q), si.STREAM_FREIVALDS, 0, mask=q - 1)
+        mism = gf.verify_batch(q, A, C, B, R)
+        return int(mism.sum().item()), int(idx.numel())
+
+    def free(self):
+        del self.A, self.C, self.B
+
+
+def time_job(job, steps, warmup, ws, dist, sampler=None):
+    """Device-resident throughput.  One chunk: CUDA-event span over all steps.
+    Several chunks (C5 does not fit one GPU): each chunk's inputs are generated
+    before its launch and only the encode launches are timed (the sum of their
+    event durations).  Returns (ms, per-launch ms list, launches, clocks)."""
+    torch = job.torch
+    stream = torch.cuda.current_stream(job.device)
+    n0 = job.fill(0)
+    torch.cuda.synchronize()
+    for _ in range(warmup):
+        job.encode(n0)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    nl = steps * job.nchunks
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nl)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    launches = 0
+    t_start.record(stream)
+    for s in range(steps):
+        for j in range(job.nchunks):
+            n = job.fill(j) if job.nchunks > 1 else n0
+            e0, e1 = ev[s * job.nchunks + j]
+            e0.record(stream)
+            job.encode(n)
+            e1.record(stream)
+            launches += 1
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop() if sampler else None
+    kern_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = t_start.elapsed_time(t_end) if job.nchunks == 1 else sum(kern_ms)
+    if ws > 1:
+        t = torch.tensor([total_ms], device=job.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    return total_ms, kern_ms, launches, clocks
+
+
 # ---------------------------------------------------------------- our arm
 
 def main():
@@ -221,12 +371,18 @@ def main():
     if args.impl == "reference":
         run_reference(args)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
+    ws, rank, local = dist_env()
+    if ws != args.gpus:
+        print(json.dumps({"error": f"WORLD_SIZE={ws} but --gpus {args.gpus}"}), flush=True)
+        sys.exit(1)
+
     import torch
     import torch.distributed as dist
 
     from paper_1909_02871_b200 import gf, shard
 
-    ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if ws > 1:
@@ -234,128 +390,100 @@ def main():
 
     cfg = si.ENCODE_CONFIGS[args.config]
     q = args.field or cfg.fields[-1]
-    fields = [q] + ([f for f in cfg.fields if f != q] if not args.no_extra_fields else [])
-    for f in fields:
+    for f in (2, 4, 16, 256):
         gf.init(f)
     peaks = load_peaks()
+    sh, by_bytes = rank_shard(shard, cfg, ws, rank)
+    N, K, M = cfg.N, cfg.K, cfg.M
+    parity = {}
 
-    # ---- this rank's shard: weak scaling by generation (C1, C3, C5) or
-    # strong scaling by packet byte range (C4), SURVEY.md 8(e)
-    by_bytes = cfg.shard == "bytes"
-    sh = shard.plan(cfg.batch, cfg.M, ws, rank, by="bytes" if by_bytes else "generation",
-                    weak=not by_bytes)
-    G, Ms, N, K, M = sh.generations, sh.columns, cfg.N, cfg.K, cfg.M
-    free, _ = torch.cuda.mem_get_info(device)
-    per_gen = (N + K) * Ms + N * K
-    chunk = min(G, args.chunk_gens or G)
-    if per_gen * chunk > 0.8 * free:
-        chunk = max(1, int(0.8 * free // per_gen))
-    nchunks = -(-G // chunk)
-    stream = torch.cuda.current_stream(device)
-
-    A = torch.empty((chunk, N, Ms), dtype=torch.uint8, device=device)
-    Cm = torch.empty((chunk, N, K), dtype=torch.uint8, device=device)
-    B = torch.empty((chunk, K, Ms), dtype=torch.uint8, device=device)
-
-    def fill(f, j):
-        """Inputs of chunk j, generated on device by absolute index."""
-        seed = si.field_seed(cfg, f)
-        g = sh.g0 + j * chunk
-        n = min(chunk, G - j * chunk)
-        gf.fill_random2d(A[:n].view(n * N, Ms), seed, si.STREAM_A, g * N * M + sh.m0, M)
-        gf.fill_random(Cm[:n], seed, si.STREAM_C, g * N * K, mask=f - 1)
-        return n
-
-    def time_field(f, steps, warmup, sampler=None):
-        """Device-resident throughput: inputs in HBM before the timed region.
-        One chunk: CUDA-event span over all steps.  Several chunks (C5 does not
-        fit): inputs of each chunk are regenerated between launches and only
-        the encode launches are timed (sum of their event durations)."""
-        n0 = fill(f, 0)
-        torch.cuda.synchronize()
-        for _ in range(warmup):
-            gf.encode_batch(f, A[:n0], Cm[:n0], B[:n0])
-        torch.cuda.synchronize()
-        if ws > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        if sampler:
-            sampler.start()
-            time.sleep(0.3)
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(steps * nchunks)]
-        t_start = torch.cuda.Event(enable_timing=True)
-        t_end = torch.cuda.Event(enable_timing=True)
-        launches = 0
-        t_start.record(stream)
-        for s in range(steps):
-            for j in range(nchunks):
-                n = fill(f, j) if nchunks > 1 else n0
-                e0, e1 = ev[s * nchunks + j]
-                e0.record(stream)
-                gf.encode_batch(f, A[:n], Cm[:n], B[:n])
-                e1.record(stream)
-                launches += 1
-        t_end.record(stream)
-        torch.cuda.synchronize()
-        clocks = sampler.stop() if sampler else None
-        kern_ms = [a.elapsed_time(b) for a, b in ev]
-        total_ms = t_start.elapsed_time(t_end) if nchunks == 1 else sum(kern_ms)
-        if ws > 1:
-            t = torch.tensor([total_ms], device=device)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            total_ms = float(t.item())
-            dist.barrier()
-        return total_ms, kern_ms, launches, clocks
-
-    job_src_per_step = (cfg.batch * N * M) if by_bytes else ws * G * N * M
+    # ---- headline: the configured workload over field q
+    job = Job(gf, torch, cfg, q, sh, device, args.chunk_gens)
     sampler = ClockSampler(local)
-    total_ms, kern_ms, launches, clocks = time_field(q, args.steps, args.warmup, sampler)
-    value = job_src_per_step * args.steps / (total_ms / 1e3) / 1e9
+    total_ms, kern_ms, launches, clocks = time_job(job, args.steps, args.warmup, ws, dist, sampler)
+    job_src = cfg.batch * N * M                        # the whole job, all ranks
+    value = job_src * args.steps / (total_ms / 1e3) / 1e9
     ms_per_step = total_ms / args.steps
+    # gate: the last timed chunk's output, on the device
+    bad, nver = job.verify(min(job.chunk, job.G - (job.nchunks - 1) * job.chunk), args.verify_gens)
+    parity[f"GF({q})"] = {"device_freivalds_gens": nver, "mismatched_bytes": bad}
 
-    per_field = {str(q): round(value, 3)}
-    for f in fields[1:]:
-        st = max(3, args.steps // 2)
-        tms, _, _, _ = time_field(f, st, args.warmup)
-        per_field[str(f)] = round(job_src_per_step * st / (tms / 1e3) / 1e9, 3)
-
-    # ---- roofline of the dominant kernel: the encode launch (every launch of
-    # the timed region is one); algorithmic work per launch / mean duration
+    # roofline of the dominant kernel: the encode launch (every launch of the
+    # timed region is one); algorithmic work per launch / mean launch duration
     avg_kernel_s = statistics.mean(kern_ms) / 1e3
-    gens_per_launch = chunk
-    path = gf.encode_path(q, N, K, Ms)
-    roof, hbm = dominant_roofline(q, N, K, Ms, gens_per_launch, path, avg_kernel_s, peaks)
-    roof["traffic"] = lookup_traffic(q, cfg, gens_per_launch, Ms, path)
+    path = gf.encode_path(q, N, K, job.Ms)
+    roof, hbm = dominant_roofline(q, N, K, job.Ms, job.chunk, path, avg_kernel_s, peaks)
+    roof["traffic"] = lookup_traffic(q, cfg, job.chunk, job.Ms, path)
     roof["kernel_ms"] = round(statistics.mean(kern_ms), 4)
-    del A, Cm, B
+
+    # the oracle's sample compared with the GPU's bytes (rank 0, N = 1): the
+    # first generations of the job, still resident when the job is one chunk
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        gpu_B = None
+        if job.nchunks == 1 and job.Ms == M:
+            def gpu_B(g0, g1):
+                return job.B[g0:g1].cpu().numpy()
+        cpu = cpu_baseline(cfg, q, gpu_B=gpu_B)
+        if "parity_vs_gpu" in cpu:
+            parity[f"GF({q})"]["oracle_gens"] = cpu["parity_vs_gpu"]["generations"]
+            parity[f"GF({q})"]["oracle_mismatched_bytes"] = cpu["parity_vs_gpu"]["mismatched_bytes"]
+    job.free()
+    del job
     torch.cuda.empty_cache()
+
+    # ---- the other fields of the metric: GF(16) on C3, GF(2) / GF(4) on C5
+    per_field = {str(q): field_entry(value, cfg, q, path, ms_per_step, total_ms, kern_ms, job_src, args.steps,
+                                     peaks, sh, ws)}
+    if not args.no_extra_fields:
+        extra = [(si.C3, 16), (si.C3, 256), (si.C5, 2), (si.C5, 4)]
+        for xcfg, f in extra:
+            if str(f) in per_field:
+                continue
+            xsh, _ = rank_shard(shard, xcfg, ws, rank)
+            xjob = Job(gf, torch, xcfg, f, xsh, device, 512 if xcfg is si.C5 else 0, mem_frac=0.6)
+            st = max(2, args.steps // 3) if xjob.nchunks > 1 else max(3, args.steps // 2)
+            tms, kms, nl, _ = time_job(xjob, st, 1, ws, dist)
+            launches += nl
+            xsrc = xcfg.batch * xcfg.N * xcfg.M
+            xval = xsrc * st / (tms / 1e3) / 1e9
+            bad, nver = xjob.verify(min(xjob.chunk, xjob.G - (xjob.nchunks - 1) * xjob.chunk),
+                                    min(args.verify_gens, 64))
+            parity[f"GF({f})"] = {"device_freivalds_gens": nver, "mismatched_bytes": bad}
+            xpath = gf.encode_path(f, xcfg.N, xcfg.K, xjob.Ms)
+            per_field[str(f)] = field_entry(xval, xcfg, f, xpath, tms / st, tms, kms, xsrc, st, peaks, xsh, ws,
+                                            chunk=xjob.chunk, nchunks=xjob.nchunks)
+            xjob.free()
+            del xjob
+            torch.cuda.empty_cache()
 
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(gf, torch, dist, cfg, q, sh, device, ws, args)
 
-    cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu:
-        cpu = cpu_baseline(cfg, q)
-        cpu["cpu_model"] = cpu_model()
-
+    # ---- parity gate over all ranks
+    nbad = sum(v["mismatched_bytes"] + v.get("oracle_mismatched_bytes", 0) for v in parity.values())
+    if ws > 1:
+        t = torch.tensor([nbad], device=device, dtype=torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        nbad = int(t.item())
     if rank == 0:
         out = {
             "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
-            "higher_is_better": True, "scaling": "strong" if by_bytes else "weak",
+            "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (seeded splitmix64 byte stream: uniform payload bytes, "
                     "i.i.d. uniform coefficients over F_q; generated on device)",
-            "config": {"workload": workload_name(cfg, q, G), "field": q, "N": N, "K": K, "M": M,
-                       "gens_per_gpu": G, "bytes_per_packet_per_gpu": Ms,
-                       "global_batch": cfg.batch if by_bytes else ws * G,
-                       "gens_per_launch": gens_per_launch, "launches_per_step": nchunks,
+            "config": {"workload": workload_name(cfg, q, sh.generations, ws, by_bytes), "field": q,
+                       "N": N, "K": K, "M": M, "batch": cfg.batch, "gens_per_gpu": sh.generations,
+                       "bytes_per_packet_per_gpu": sh.columns, "global_batch": cfg.batch,
+                       "launches_per_step": -(-sh.generations // max(1, roof.get("gens_per_launch", 1))),
                        "parallelism": (f"byte-range sharded x{ws}" if by_bytes else
-                                       f"generation-sharded x{ws}") + ", no collective",
-                       "l2": (f"inputs {G * N * Ms / 1e9:.2f} GB per GPU >> 126 MB L2 (no flush)"
-                              if G * N * Ms > 2 * 126e6 else "L2-resident working set")},
+                                       f"generation-split x{ws}") + ", no collective on the data path",
+                       "l2": (f"inputs {sh.generations * N * sh.columns / 1e9:.2f} GB per GPU >> 126 MB L2 "
+                              "(no flush)" if sh.generations * N * sh.columns > 2 * 126e6
+                              else "L2-resident working set")},
             "per_field": per_field,
             "roofline": roof,
             "hbm": hbm,
@@ -364,63 +492,83 @@ def main():
             "clocks": clocks,
             "gpu_launches": launches,
             "kernel_ms_per_launch": round(statistics.mean(kern_ms), 4),
+            "parity": "ok" if nbad == 0 else "FAIL",
+            "parity_detail": parity,
         }
         print(json.dumps(out), flush=True)
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
+    if nbad:
+        sys.exit(2)
 
 
-SMEM_BYTES_PER_SM_CLK = 128   # shared-memory crossbar (B300_MICROARCH.md; tools/ubench_smem.cu)
-LANEK = {2: (4, 1, 15), 4: (2, 1, 15), 16: (1, 1, 15), 256: (1, 2, 30)}   # SG, gathers/unit, build rows
+def field_entry(value, cfg, q, path, ms_per_step, total_ms, kern_ms, job_src, steps, peaks, sh, ws,
+                chunk=None, nchunks=1):
+    """One field of the metric: source GB/s of the whole job and its fraction
+    of the HBM roofline (read A, write B, read C at the measured copy peak, all
+    GPUs)."""
+    hbm_bytes = cfg.batch * ((cfg.N + cfg.K) * cfg.M + cfg.N * cfg.K)
+    hbm_gbs = hbm_bytes * steps / (total_ms / 1e3) / 1e9
+    e = {"value": round(value, 3), "unit": "GB/s", "workload": cfg.name, "N": cfg.N, "K": cfg.K, "M": cfg.M,
+         "batch": cfg.batch, "kernel": path, "ms_per_step": round(ms_per_step, 4),
+         "hbm_frac": round(hbm_gbs / (peaks["hbm_gbs"] * ws), 4)}
+    if nchunks > 1:
+        e["launches_per_step"] = nchunks
+        e["gens_per_launch"] = chunk
+        e["timing"] = "sum of encode-launch event durations (inputs of each chunk generated between launches)"
+    return e
 
 
 def dominant_roofline(q, N, K, Ms, gens, path, kernel_s, peaks):
-    """Roofline of the encode launch.
+    """Roofline of the encode launch, on the METHOD'S
+    algorithmic work only (no kernel-internal table builds in `achieved`).
 
-    The product-row kernel is bound by the shared-memory pipe: algorithmic
-    smem bytes = one gathered byte per byte-madd + the product tables written
-    (256 x 64 B per source, coded-packet tile and 384-word tile).
-    lane-k kernels are bound by the shared-memory pipe: algorithmic smem bytes
-    = gathers (4 B per gathered word, G per (step, k, word)) + table build
-    (R rows x 4 B per (step, word), once per CTA k-tile); peak = 148 SMs x
-    128 B/clk x max SM clock.  Column kernels are bound by the ALU pipe:
-    byte-madds x ops per byte-madd of the method; peak = 148 x 64 lanes/clk x
-    clock.  Both carry the HBM view (read A, write B, read C)."""
+    product-row (prow*): bound by the shared-memory pipe; algorithmic smem
+    bytes = one gathered product byte per byte-madd; peak 148 SMs x 128 B/clk
+    x max SM clock.  The kernel's own table stores (256 x 64 B per source,
+    coded-packet tile and word tile) are reported beside it.
+    lane-k: smem gathers (4 B per gathered word) + table build rows.
+    gf2-split: HBM-bound design; its issue-slot use (43 per 32 terms) is
+    reported beside.  column: ALU ops of the method per byte-madd.  Every entry
+    carries the HBM view (read A, write B, read C)."""
     clk = peaks["sm_max_mhz"] * 1e6
     bm = N * K * Ms * gens
     hbm_bytes = ((N + K) * Ms + N * K) * gens
     hbm_ach = hbm_bytes / kernel_s / 1e9
     hbm = {"achieved": round(hbm_ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
            "frac": round(hbm_ach / peaks["hbm_gbs"], 4), "peak_source": peaks["source"]}
-    if path == "prow":
-        # product-row kernel: every byte-madd is one gathered product byte;
-        # tables: 256 rows x 64 B per (source, 64-coded-packet tile, word tile)
-        tw = 384
-        m_tiles = -(-(Ms // 4) // tw)
-        k_tiles = -(-K // 64)
-        n_pad = -(-N // 4) * 4
-        smem_bytes = bm + gens * n_pad * k_tiles * m_tiles * 256 * 64
-        peak = N_SM * SMEM_BYTES_PER_SM_CLK * clk
-        ach = smem_bytes / kernel_s
-        roof = {"bound": "smem", "achieved": round(ach / 1e12, 3), "peak": round(peak / 1e12, 3),
-                "unit": "TB/s", "frac": round(ach / peak, 4),
-                "peak_source": f"{N_SM} SMs x {SMEM_BYTES_PER_SM_CLK} B/clk shared-memory pipe x "
-                               f"{peaks['sm_max_mhz']:.0f} MHz (DESIGN.md 'roofline')",
-                "smem_bytes_per_launch": smem_bytes}
+    smem_peak = N_SM * SMEM_BYTES_PER_SM_CLK * clk
+    smem_src = (f"{N_SM} SMs x {SMEM_BYTES_PER_SM_CLK} B/clk shared-memory pipe x "
+                f"{peaks['sm_max_mhz']:.0f} MHz (max SM clock; DESIGN.md 6)")
+    if path.startswith("prow"):
+        kc = {"prow": 64, "prow-32": 32, "prow-16": 16}[path]
+        m_tiles = -(-(Ms // 4) // 384)
+        k_tiles = -(-K // kc)
+        s = 256 // kc                                   # sources per step (a table row is 256 B)
+        n_pad = -(-N // s) * s
+        builds = gens * n_pad * k_tiles * m_tiles * 256 * kc
+        ach = bm / kernel_s
+        roof = {"bound": "smem", "achieved": round(ach / 1e12, 3), "peak": round(smem_peak / 1e12, 3),
+                "unit": "TB/s", "frac": round(ach / smem_peak, 4), "peak_source": smem_src,
+                "algorithmic": "1 gathered product byte per byte-madd",
+                "table_build_bytes_per_launch": builds,
+                "smem_frac_incl_table_builds": round((bm + builds) / kernel_s / smem_peak, 4)}
     elif path.startswith("lanek"):
         SG, G, R = LANEK[q]
         ktl = 64 if path == "lanek-64" else 32
         steps = -(-N // SG)
         k_tiles = -(-K // ktl)
         smem_bytes = gens * steps * (Ms // 4) * 4 * (K * G + R * k_tiles)
-        peak = N_SM * SMEM_BYTES_PER_SM_CLK * clk
         ach = smem_bytes / kernel_s
-        roof = {"bound": "smem", "achieved": round(ach / 1e12, 3), "peak": round(peak / 1e12, 3),
-                "unit": "TB/s", "frac": round(ach / peak, 4),
-                "peak_source": f"{N_SM} SMs x {SMEM_BYTES_PER_SM_CLK} B/clk shared-memory pipe x "
-                               f"{peaks['sm_max_mhz']:.0f} MHz (DESIGN.md 'roofline')",
+        roof = {"bound": "smem", "achieved": round(ach / 1e12, 3), "peak": round(smem_peak / 1e12, 3),
+                "unit": "TB/s", "frac": round(ach / smem_peak, 4), "peak_source": smem_src,
                 "smem_bytes_per_launch": smem_bytes}
+    elif path == "gf2-split":
+        issue_peak = N_SM * ISSUE_LANES_PER_SM_CLK * clk
+        roof = dict(hbm, bound="hbm")
+        roof["issue_frac"] = round(bm * GF2_SPLIT_ISSUE_PER_BYTE_MADD / kernel_s / issue_peak, 4)
+        roof["issue_peak_source"] = f"{N_SM} SMs x 4 SMSPs x 32 lanes x {peaks['sm_max_mhz']:.0f} MHz"
     else:
         ops = bm * OPS_PER_BYTE_MADD[q]
         peak = N_SM * ALU_LANES_PER_SM_CLK * clk
@@ -428,11 +576,12 @@ def dominant_roofline(q, N, K, Ms, gens, path, kernel_s, peaks):
         roof = {"bound": "alu", "achieved": round(ach / 1e12, 3), "peak": round(peak / 1e12, 3),
                 "unit": "Tops/s", "frac": round(ach / peak, 4),
                 "peak_source": f"{N_SM} SMs x {ALU_LANES_PER_SM_CLK} ALU-pipe lanes/clk x "
-                               f"{peaks['sm_max_mhz']:.0f} MHz (DESIGN.md 'roofline')",
+                               f"{peaks['sm_max_mhz']:.0f} MHz (DESIGN.md 6)",
                 "ops_per_byte_madd": OPS_PER_BYTE_MADD[q]}
     if hbm["frac"] > roof["frac"]:
-        roof = dict(hbm, bound="hbm")
+        roof = dict(roof, **{k: v for k, v in hbm.items()}, bound="hbm")
     roof["kernel"] = f"encode {path} GF({q})"
+    roof["gens_per_launch"] = gens
     roof["byte_madds_per_launch"] = bm
     roof["hbm_bytes_per_launch"] = hbm_bytes
     return roof, hbm
@@ -440,7 +589,7 @@ def dominant_roofline(q, N, K, Ms, gens, path, kernel_s, peaks):
 
 KERNEL_SOURCES = {"prow": "encode_prow.cuh", "prow-32": "encode_prow.cuh", "prow-16": "encode_prow.cuh",
                   "lanek-32": "encode_lanek.cuh", "lanek-64": "encode_lanek.cuh", "stream": "encode_stream.cuh",
-                  "column-words": "encode_kernels.cuh"}
+                  "column-words": "encode_kernels.cuh", "gf2-split": "encode_gf2.cuh"}
 
 
 def kernel_sha(path):

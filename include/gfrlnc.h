@@ -23,8 +23,11 @@
  *           throws across the ABI.  A size of zero returns GF_OK and launches
  *           nothing.  GF_ECUDA reports a launch / runtime failure
  *           (cudaGetLastError after the launch).
- *   hot path  no allocation, no host synchronisation, no host<->device copy
- *           inside gf_maddrc / gf_mulrc / gf_encode_batch.
+ *   hot path  no allocation, no host synchronisation, no host<->device copy,
+ *           no lock and no kernel-attribute call inside gf_maddrc / gf_mulrc /
+ *           gf_encode_batch (and gf_invert_batch / gf_decode_batch /
+ *           gf_verify_batch): gf_init prepares everything once per (device,
+ *           field), so these calls may be captured into a CUDA graph.
  */
 #ifndef GFRLNC_H
 #define GFRLNC_H
@@ -48,9 +51,12 @@ enum {
 
 /* Build the per-coefficient split multiplication tables of F_q on the host
  * and upload them to the CURRENT device (Alg. 1 tables tl/th,
- * re-cut for the GPU into three byte-permute tables).
- * Idempotent and thread-safe; call once per (device, field) before any other
- * call for that field.  Returns GF_OK, GF_EFIELD or GF_ECUDA. */
+ * re-cut for the GPU into three byte-permute tables), and
+ * prepare the field's kernels on that device (dynamic shared-memory opt-ins,
+ * the product-row kernel's shared-window probe).  Allocates and synchronises
+ * (not a hot-path call).  Idempotent and thread-safe; call once per (device,
+ * field) before any other call for that field.  Returns GF_OK, GF_EFIELD or
+ * GF_ECUDA. */
 int gf_init(int field);
 
 /* Region multiply-add  dst[j] := dst[j] + coeff * src[j]  for j < bytes:
@@ -162,25 +168,36 @@ int gf_host_tables(int field, uint32_t *out, size_t cap_words);
 /* Host-only introspection (harness / roofline accounting): which encode kernel
  * gf_encode_batch launches for these arguments, given the byte offsets of A
  * and B modulo 16.  Returns 0 = column kernel on 32-bit words, 1 = column
- * kernel on bytes (unaligned or M % 4 != 0), 2 = lane-k kernel with 32 coded
- * packets per CTA, 3 = lane-k kernel with 64, 4 / 5 = fused lane-k + column
- * kernel with 32 / 64, 6 = product-row kernel (GF(16)/GF(256), K > 32: C3,
- * C4; 9 / 10 = the same with 32 / 16 coded packets per CTA, K <= 32 / 16,
- * also GF(4) with 9 <= K < 24 on well-tiled packets), 7 = persistent lane-k
- * (opt-in, GF(2)/GF(4), K <= 32), 8 = streaming kernel (K <= 4: C1 and the
- * paper's N = 16, K = 1 shape; its chunk layout -- 16-byte chunks one, two
- * or four per thread, or 4-byte words one or 4 / 12 strided per thread --
- * follows from M, the alignment and the job size), or
- * GF_EFIELD / GF_EARG. */
+ * kernel on bytes (unaligned or M % 4 != 0), 2 / 3 = lane-k kernel with 32 /
+ * 64 (128 when K > 64) coded packets per CTA (GF(4), K >= 24, and GF(2) where
+ * the split engine does not apply), 6 / 9 / 10 = product-row kernel with 64 /
+ * 32 / 16 coded packets per CTA (GF(16)/GF(256), K > 8: C3, C4; GF(4) with
+ * 9 <= K < 24 on well-tiled packets), 8 = streaming kernel (K <= 4: C1 and
+ * the paper's N = 16, K = 1 shape; its chunk layout -- 16-byte chunks one,
+ * two or four per thread, or 4-byte words one or 4 / 8 / 12 strided per
+ * thread -- follows from M, the alignment and the job size), 11 = GF(2) split
+ * engine (GF(2), K >= 24, N <= 32, M % 16 == 0, 16-byte aligned A and B: C5)
+ * (DESIGN.md section 6), or GF_EFIELD / GF_EARG. */
 int gf_encode_path(int field, int N, int K, size_t M, size_t a_align, size_t b_align);
 
-/* Harness-only (experiments, forced-path tests): force the encode kernel of
- * the calling thread's gf_encode_batch calls.  0 = automatic (default), 1 =
- * column kernel, 2 = lane-k, 3 = fused lane-k + column, 4 = product-row,
- * 5 = persistent lane-k (GF(2)/GF(4) with K <= 32), 6 = streaming (K <= 4);
- * shapes a forced kernel cannot take fall back to lane-k.
- * Thread-local; returns GF_OK or GF_EARG.  Takes precedence over the
- * GFRLNC_ENCODE_PATH environment variable. */
+/* Harness-only (forced-path tests and experiments): force the encode kernel of
+ * the calling thread's gf_encode_batch calls.  Thread-local; nothing is read
+ * from the environment.  Shapes a forced kernel cannot take fall back to the
+ * lane-k kernel (GF_PATH_GF2: to the automatic choice).  Returns GF_OK or
+ * GF_EARG. */
+enum {
+    GF_PATH_AUTO = 0,
+    GF_PATH_COLUMN = 1,
+    GF_PATH_LANEK = 2,
+    GF_PATH_PROW = 4,
+    GF_PATH_STREAM = 6,              /* streaming kernel, automatic layout      */
+    GF_PATH_GF2 = 7,                 /* GF(2) split engine                      */
+    GF_PATH_STREAM_STRIDED4 = 8,     /* streaming, strided 4-word blocks at any job size */
+    GF_PATH_STREAM_STRIDED8 = 9,     /* ... 8-word blocks                       */
+    GF_PATH_STREAM_STRIDED12 = 10,   /* ... 12-word blocks                      */
+    GF_PATH_STREAM_WIDE2 = 11,       /* streaming, two 16-byte chunks per thread at any packet size */
+    GF_PATH_STREAM_WIDE4 = 12        /* streaming, four 16-byte chunks per thread                   */
+};
 int gf_set_encode_path(int path);
 
 /* Library version (major * 10000 + minor * 100 + patch). */

@@ -94,6 +94,9 @@ __global__ void __launch_bounds__(256) invert_kernel(InvertParams p)
         // swap pivot row into place and scale it by the inverse of the pivot
         const uint32_t pv = Mb[(size_t)piv * RW * 4 + col];
         const PrmtTab Ts = tab_of(stab, sinv[pv]);
+        // every thread has read the pivot before any thread rewrites its word
+        // in the swap below (warps > 0 would otherwise race with warp 0)
+        __syncthreads();
         for (int w = w0 + tid; w < RW; w += nt) {
             const uint32_t a = Mx[(size_t)piv * RW + w];
             const uint32_t b = Mx[(size_t)rank * RW + w];

@@ -1,0 +1,128 @@
+// encode_gf2.cuh -- batched RLNC encode over GF(2) with the source words of a
+// 512-byte column span held in registers and the multiply-add of every
+// (source i, coded packet k) split between the two integer pipes.
+//
+//   B[g][k][m] = XOR_{i < N} C[g][i][k] * A[g][i][m]          (Eq. 2)
+//
+// Over GF(2) a coefficient is one bit, so c * a is either a or 0 for a whole
+// 32-bit word of 32 field elements ("GF(2): XOR").  Two
+// data-independent ways to apply it, on two different pipes:
+//   * masked XOR on the ALU pipe: acc ^= a & m with m = 0 or ~0 (one LOP3 per
+//     term -- the paper's bit-plane masking, Alg. 2's `and` step);
+//   * the paper's imul (Alg. 2) on the FMA pipe: a * c with
+//     c = 0 or 1 is one IMAD; two such products are folded into the
+//     accumulator by one 3-input LOP3 (acc ^ p0 ^ p1).
+// Sources i with i % 3 == 2 take the masked form, the others the imul form in
+// pairs, so per (word, coded packet) the 32 terms cost 21 ALU + 22 FMA
+// instructions: both pipes ~2/3 busy per term and 1.34 issue slots per term
+// (all-masked would be 1 issue slot but 1 ALU op per term, ALU-bound at 71% of
+// the HBM roofline; tools/exp_c5_branch.cu has both and the branch variants).
+//
+// Layout: a block (4 warps) owns one generation; its coefficient words
+// cw[k][i] (c or mask, per the form of source i) are built once into shared
+// memory and read back per coded packet with broadcast LDS.128.  Lane l of a
+// warp owns words w0 + 4l .. w0 + 4l + 3 of every packet of a 128-word span
+// (16-byte loads / stores, 512 contiguous bytes per warp per packet); all NS
+// source words of the span stay in registers (4 NS registers) while the warp
+// walks k = 0 .. K-1 and stores each coded packet's span once.  HBM traffic is
+// the algorithmic N*M + K*M (+ N*K) per generation.
+//
+// Requirements (checked by the router): 1 <= N <= NS, M % 16 == 0, A and B
+// 16-byte aligned.  Sources i >= N read as zero with zero coefficients.
+#pragma once
+#include <cstdint>
+
+namespace gfr {
+
+constexpr int kG2Threads = 128;            // 4 warps, one generation per block
+constexpr int kG2SpanWords = 128;          // 32 lanes x 4 words
+
+struct Gf2Params {
+    const uint8_t *A;      // [batch][N][M]
+    const uint8_t *C;      // [batch][N][K]
+    uint8_t *B;            // [batch][K][M]
+    uint32_t Mw;           // 32-bit words per packet (M / 4, M % 16 == 0)
+    uint32_t spans;        // 128-word spans per packet
+    uint32_t blocks_per_gen;
+    int spw;               // spans per warp
+    int N, K;
+};
+
+__device__ __forceinline__ uint4 g2_ld(const uint8_t *p)
+{
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ void g2_st(uint8_t *p, uint32_t a, uint32_t b, uint32_t c, uint32_t d)
+{
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" :: "l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
+template <int NS>
+__global__ void __launch_bounds__(kG2Threads) encode_gf2_kernel(Gf2Params p)
+{
+    extern __shared__ __align__(16) uint32_t cw[];              // [K][NS]
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const size_t g = blockIdx.x / p.blocks_per_gen;
+    const uint32_t bi = blockIdx.x - (uint32_t)(g * p.blocks_per_gen);
+    const int N = p.N, K = p.K;
+    {
+        const uint8_t *Cg = p.C + g * (size_t)N * K;
+        for (int t = threadIdx.x; t < K * NS; t += kG2Threads) {
+            const int k = t / NS, i = t - k * NS;
+            const uint32_t c = i < N ? (__ldg(Cg + (size_t)i * K + k) & 1u) : 0u;
+            cw[t] = (i % 3 == 2) ? 0u - c : c;              // mask for the ALU form, 0/1 for imul
+        }
+    }
+    __syncthreads();
+    const size_t M = (size_t)p.Mw * 4;
+    const uint32_t sp0 = (bi * 4 + wid) * (uint32_t)p.spw;
+#pragma unroll 1
+    for (int s = 0; s < p.spw; s++) {
+        const uint32_t sp = sp0 + s;
+        if (sp >= p.spans) break;
+        const uint32_t w0 = sp * kG2SpanWords + 4 * lane;
+        const bool valid = w0 < p.Mw;
+        const uint8_t *Ag = p.A + g * (size_t)N * M + 4 * (size_t)w0;
+        uint32_t a[NS][4];
+#pragma unroll
+        for (int i = 0; i < NS; i++) {
+            if (valid && i < N) {
+                const uint4 v = g2_ld(Ag + (size_t)i * M);
+                a[i][0] = v.x; a[i][1] = v.y; a[i][2] = v.z; a[i][3] = v.w;
+            } else {
+                a[i][0] = a[i][1] = a[i][2] = a[i][3] = 0u;
+            }
+        }
+        uint8_t *Bp = p.B + g * (size_t)K * M + 4 * (size_t)w0;
+#pragma unroll 1
+        for (int k = 0; k < K; k++, Bp += M) {
+            uint32_t c[NS];
+#pragma unroll
+            for (int q = 0; q < NS / 4; q++) {
+                const uint4 v = reinterpret_cast<const uint4 *>(cw + k * NS)[q];
+                c[4 * q] = v.x; c[4 * q + 1] = v.y; c[4 * q + 2] = v.z; c[4 * q + 3] = v.w;
+            }
+            uint32_t acc[4];
+#pragma unroll
+            for (int w = 0; w < 4; w++) {
+                uint32_t x = 0;
+#pragma unroll
+                for (int i = 0; i < NS; i += 3) {
+                    if (i + 1 < NS) x ^= (a[i][w] * c[i]) ^ (a[i + 1][w] * c[i + 1]);   // 2 IMAD + LOP3
+                    else x ^= a[i][w] * c[i];
+                    if (i + 2 < NS) x ^= a[i + 2][w] & c[i + 2];                        // LOP3
+                }
+                acc[w] = x;
+            }
+            if (valid) g2_st(Bp, acc[0], acc[1], acc[2], acc[3]);
+        }
+    }
+}
+
+__host__ __device__ constexpr size_t gf2_smem_bytes(int K, int NS) { return (size_t)K * NS * 4; }
+
+}  // namespace gfr

@@ -80,8 +80,6 @@ struct LanekParams {
     int qmask;
     int tiles;         // word tiles per packet
     int k_tiles;       // ceil(K / (32 KG))
-    int direct;        // epilogue: each lane stores its own run of its coded packet (16-B stores)
-    int aligned16;     // M % 16 == 0 and B 16-byte aligned
 };
 
 template <int F> struct LkField;
@@ -290,26 +288,6 @@ encode_lanek_kernel(LanekParams p)
         nbar_arrive(BAR_EMPTY + b, NT);
     }
 
-    if (p.direct) {
-        // ---- epilogue without shared memory: lane kl holds words wb .. wb+WT-1 of
-        // coded packet k0 + kl; WT/4 16-byte stores per lane (32 rows per warp
-        // instruction, every 128-B line completed by the same lane's stores)
-        const int k = k0 + kl;
-        if (k < p.K) {
-            const uint32_t wb = w0 + (uint32_t)(wg * WT);
-            uint32_t *row = reinterpret_cast<uint32_t *>(p.B + (g * (size_t)p.K + (size_t)k) * p.M) + wb;
-            if (p.aligned16 && wb + WT <= p.Mw) {
-#pragma unroll
-                for (int v = 0; v < WT / 4; v++)
-                    reinterpret_cast<uint4 *>(row)[v] = make_uint4(acc[4 * v], acc[4 * v + 1], acc[4 * v + 2], acc[4 * v + 3]);
-            } else {
-#pragma unroll
-                for (int w = 0; w < WT; w++)
-                    if (wb + w < p.Mw) row[w] = acc[w];
-            }
-        }
-        return;
-    }
     // ---- epilogue: transpose through shared memory so that each warp writes
     // contiguous runs of one coded packet (the Q buffers are free once every
     // gatherer passed its last step: named barrier over the gatherers only)

@@ -12,10 +12,9 @@
 #include "../../include/gfrlnc.h"
 #include "encode_kernels.cuh"
 #include "encode_lanek.cuh"
-#include "encode_fused.cuh"
 #include "encode_prow.cuh"
-#include "encode_lanek2.cuh"
 #include "encode_stream.cuh"
+#include "encode_gf2.cuh"
 #include "decode_kernels.cuh"
 #include "region_kernels.cuh"
 #include "rng_kernels.cuh"
@@ -24,7 +23,7 @@
 namespace gfr {
 
 constexpr int kMaxDevices = 64;
-constexpr int kVersion = 137;   // 0.1.37: selectors on IMAD.HI, paired XOR in the stream kernel
+constexpr int kVersion = 200;   // 0.2.00: GF(2) split engine, kernels configured in gf_init
 
 __device__ uint32_t g_dev_tabs[4][256 * kTableWords];
 __device__ uint8_t g_dev_inv[4][256];
@@ -34,18 +33,12 @@ static uint32_t g_host_tabs[4][256 * kTableWords];
 static uint8_t g_host_inv[4][256];
 static uint8_t g_host_mul[4][256 * 256];
 static bool g_host_ready[4];
-static uint32_t g_dev_ready[kMaxDevices];     // bit f: field index f uploaded
+static uint32_t g_dev_ready[kMaxDevices];     // bit f: field index f uploaded and its kernels configured
 static int g_sm_count[kMaxDevices];
-static std::mutex g_lock;
+static uint32_t g_smem_base[kMaxDevices];     // shared-window address of the first dynamic smem byte
+static std::mutex g_lock;                     // gf_init and the host pipeline's one-time setup only
 static thread_local cudaStream_t tls_stream = nullptr;
 static thread_local int tls_path = 0;          // harness: forced encode path (gf_set_encode_path)
-
-// experiment knobs (never needed in production): integer environment variable
-static int env_int(const char *name, int dflt)
-{
-    const char *v = getenv(name);
-    return v && *v ? atoi(v) : dflt;
-}
 
 static int field_index(int field)
 {
@@ -173,11 +166,7 @@ static int launch_encode_t(EncodeParams p, cudaStream_t st)
     constexpr int S = enc_stages<F>();
     const size_t smem = (size_t)p.gens_per_cta * enc_table_bytes_per_gen<F, KT>() +
                         (BW ? 0 : (size_t)S * W * wpb * 32 * 4);
-    if (smem > 48 * 1024) {
-        if (cudaFuncSetAttribute(encode_kernel<F, W, KT, S, BW>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-            return GF_ECUDA;
-    }
+    // (the > 48 KiB dynamic shared-memory opt-in was set once by gf_init)
     encode_kernel<F, W, KT, S, BW><<<(unsigned)grid, wpb * 32, smem, st>>>(p);
     return launch_status();
 }
@@ -230,38 +219,11 @@ static int launch_lanek(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, i
     p.N = N; p.K = K; p.qmask = F - 1;
     p.tiles = (int)((p.Mw + G::TW - 1) / G::TW);
     p.k_tiles = (K + 32 * KG - 1) / (32 * KG);
-    static const int direct = env_int("GFRLNC_LANEK_DIRECT", 0);   // experiment knob
-    p.direct = direct;
-    p.aligned16 = (M % 16 == 0 && (reinterpret_cast<uintptr_t>(B) & 15u) == 0) ? 1 : 0;
     const size_t grid = batch * (size_t)p.tiles * (size_t)p.k_tiles;
     if (grid > 0x7FFFFFFFu) return GF_EARG;
     const size_t smem = lk_smem_bytes<F, KG>(N);
     if (smem > 227 * 1024) return GF_EARG;
-    if (cudaFuncSetAttribute(encode_lanek_kernel<F, KG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
-        return GF_ECUDA;
     encode_lanek_kernel<F, KG><<<(unsigned)grid, G::THREADS, smem, st>>>(p);
-    return launch_status();
-}
-
-template <int F, int KG, int WGL, int CWS>
-static int launch_fused(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M,
-                        size_t batch, cudaStream_t st, const uint32_t *tabs)
-{
-    using G = FuGeom<KG, WGL, CWS>;
-    LanekParams p{};
-    p.A = A; p.C = C; p.B = B; p.M = M; p.Mw = (uint32_t)(M / 4); p.batch = batch;
-    p.N = N; p.K = K; p.qmask = F - 1;
-    p.tiles = (int)((p.Mw + G::TW - 1) / G::TW);
-    p.k_tiles = (K + G::KTL - 1) / G::KTL;
-    const size_t grid = batch * (size_t)p.tiles * (size_t)p.k_tiles;
-    if (grid > 0x7FFFFFFFu) return GF_EARG;
-    const size_t smem = fu_smem_bytes<F, KG, WGL, CWS>(N);
-    if (smem > 227 * 1024) return GF_EARG;
-    if (cudaFuncSetAttribute(encode_fused_kernel<F, KG, WGL, CWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
-        return GF_ECUDA;
-    encode_fused_kernel<F, KG, WGL, CWS><<<(unsigned)grid, G::THREADS, smem, st>>>(p, tabs);
     return launch_status();
 }
 
@@ -272,26 +234,18 @@ __global__ void smem_base_probe(uint32_t *out)
     extern __shared__ __align__(16) uint8_t dsm[];
     if (threadIdx.x == 0) *out = (uint32_t)__cvta_generic_to_shared(dsm);
 }
-static uint32_t g_smem_base[kMaxDevices];
-static bool g_smem_base_ok[kMaxDevices];
 
-static int dyn_smem_base(uint32_t *base)
+// gf_init (once per device): allocate, launch the probe, read it back
+static int probe_smem_base(int dev)
 {
-    int dev;
-    if (current_device(&dev) != GF_OK) return GF_ECUDA;
-    std::lock_guard<std::mutex> g(g_lock);
-    if (!g_smem_base_ok[dev]) {
-        uint32_t *d = nullptr;
-        if (cudaMalloc(&d, 4) != cudaSuccess) return GF_ECUDA;
-        smem_base_probe<<<1, 32, 16>>>(d);
-        uint32_t h = 0;
-        const bool ok = cudaMemcpy(&h, d, 4, cudaMemcpyDeviceToHost) == cudaSuccess;
-        cudaFree(d);
-        if (!ok) return GF_ECUDA;
-        g_smem_base[dev] = h;
-        g_smem_base_ok[dev] = true;
-    }
-    *base = g_smem_base[dev];
+    uint32_t *d = nullptr;
+    if (cudaMalloc(&d, 4) != cudaSuccess) return GF_ECUDA;
+    smem_base_probe<<<1, 32, 16>>>(d);
+    uint32_t h = 0;
+    const bool ok = cudaMemcpy(&h, d, 4, cudaMemcpyDeviceToHost) == cudaSuccess;
+    cudaFree(d);
+    if (!ok) return GF_ECUDA;
+    g_smem_base[dev] = h;
     return GF_OK;
 }
 
@@ -313,14 +267,8 @@ static int launch_prow(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, in
     const size_t grid = p.ntiles < sms ? p.ntiles : sms;      // persistent: one CTA per SM
     // steps per CTA must fit 32 bits
     if ((p.ntiles + grid - 1) / grid * (size_t)p.NS > 0x7FFFFFF0u) return GF_EARG;
-    uint32_t base;
-    int rc = dyn_smem_base(&base);
-    if (rc != GF_OK) return rc;
-    if (base > kPrBar) return GF_EARG;                        // layout needs the window to start at <= 0x400
+    const uint32_t base = g_smem_base[dev];                   // probed by gf_init (checked <= 0x400 there)
     const size_t smem = kPrSmemEnd - base;
-    if (cudaFuncSetAttribute(encode_prow_kernel<F, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
-        return GF_ECUDA;
     encode_prow_kernel<F, KC><<<(unsigned)grid, kPrThreads, smem, st>>>(p);
     return launch_status();
 }
@@ -391,10 +339,15 @@ static int launch_stream(int field, int fi, const uint8_t *A, const uint8_t *C, 
     // 16-byte-aligned packets of >= 1 KiB: two chunks per thread (per-source
     // costs halved: NEXT-2 GF(16)/GF(256) +7%, GF(4) +4%); smaller packets
     // would leave most lanes of a 64-chunk block idle
-    static const int strided_min = env_int("GFRLNC_STREAM_STRIDED_MIN_WORDS", 1 << 20);   // experiments
-    static const int wide2_min = env_int("GFRLNC_STREAM_WIDE2_MIN_CHUNKS", 64);           // experiments
-    static const int strided_wmax_env = env_int("GFRLNC_STREAM_STRIDED_W", 0);             // experiments: force W
-    int layout = wide ? (M / 16 >= (size_t)wide2_min ? 3 : 0) : batch * (M / 4) < (size_t)strided_min ? 1 : 2;
+    // harness-only forced layouts (gf_set_encode_path, thread-local): strided
+    // word blocks at any job size with W = 4 / 8 / 12, 16-byte chunks two or four
+    // per thread at any packet size
+    const int force = tls_path;
+    const size_t strided_min = (force >= GF_PATH_STREAM_STRIDED4 && force <= GF_PATH_STREAM_STRIDED12) ? 1 : (1u << 20);
+    const size_t wide2_min = (force == GF_PATH_STREAM_WIDE2 || force == GF_PATH_STREAM_WIDE4) ? 1 : 64;
+    const int strided_wmax_env = force == GF_PATH_STREAM_STRIDED4 ? 4 : force == GF_PATH_STREAM_STRIDED8 ? 8
+                               : force == GF_PATH_STREAM_STRIDED12 ? 12 : 0;
+    int layout = wide ? (M / 16 >= wide2_min ? 3 : 0) : batch * (M / 4) < strided_min ? 1 : 2;
     // strided: the widest of 12 / 8 / 4 words per thread whose (32 W)-word
     // blocks cover >= 90% of the packet (layouts 5 / 4 / 2); GF(2) / GF(4)
     // stay at 4 (their 8-source batches at W = 12 need 180 registers: 1500 B,
@@ -414,12 +367,12 @@ static int launch_stream(int field, int fi, const uint8_t *A, const uint8_t *C, 
     // 16-byte chunks, GF(16)/GF(256): 4 per thread (128-chunk blocks) when they
     // cover >= 90% of the packet (NEXT-2 GF(256) 4.53 -> 4.70 TB/s, GF(16) 4.78
     // -> 4.85; GF(4) loses 14% at 200 registers; profiles/r01_stream_wide4_v36.txt).
-    // GFRLNC_STREAM_WIDE4 = 0 / 1 turns it off / forces it (tests).
+    // (harness: GF_PATH_STREAM_WIDE2 turns it off, GF_PATH_STREAM_WIDE4 forces it)
     // With several coded packets the accumulators multiply: four chunks only for
     // K = 1 (GF(256) K = 2 too), and GF(16) with K >= 3 back to one chunk per
     // thread (N = 16, 4 KiB: GF(16) K = 2 2.22 -> 2.73 TB/s, K = 4 1.19 -> 1.37;
     // GF(256) K = 4 1.21 -> 1.40; profiles/r01_stream_k2to4_v47.txt).
-    static const int wide4 = env_int("GFRLNC_STREAM_WIDE4", -1);
+    const int wide4 = force == GF_PATH_STREAM_WIDE2 ? 0 : force == GF_PATH_STREAM_WIDE4 ? 1 : -1;
     if (layout == 3 && wide4 != 0) {
         const size_t m16 = M / 16, nb = (m16 + 127) / 128;
         const bool few_k = K == 1 || (field == 256 && K == 2);
@@ -441,69 +394,57 @@ static int launch_stream(int field, int fi, const uint8_t *A, const uint8_t *C, 
 }
 
 template <int F>
-static int launch_lanek2(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M, size_t batch,
-                         cudaStream_t st)
-{
-    Lk2Params p;
-    p.A = A; p.C = C; p.B = B; p.M = M; p.Mw = (uint32_t)(M / 4);
-    p.N = N; p.K = K; p.NS = (N + LkField<F>::kSG - 1) / LkField<F>::kSG;
-    p.tiles = (int)((p.Mw + kL2TW - 1) / kL2TW);
-    p.ntiles = batch * (size_t)p.tiles;
-    int dev;
-    if (current_device(&dev) != GF_OK) return GF_ECUDA;
-    const size_t sms = (size_t)(g_sm_count[dev] > 0 ? g_sm_count[dev] : 148);
-    const size_t grid = p.ntiles < 2 * sms ? p.ntiles : 2 * sms;   // persistent: two CTAs per SM
-    if ((p.ntiles + grid - 1) / grid * (size_t)p.NS > 0x7FFFFFF0u) return GF_EARG;
-    if (cudaFuncSetAttribute(encode_lanek2_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)kL2Smem) != cudaSuccess)
-        return GF_ECUDA;
-    encode_lanek2_kernel<F><<<(unsigned)grid, kL2Threads, kL2Smem, st>>>(p);
-    return launch_status();
-}
-
-template <int F>
 static int launch_lanek_kg(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M,
                            size_t batch, cudaStream_t st)
 {
     // coded packets per CTA: 32 (3 CTAs/SM), 64 or 128 (one CTA/SM); larger
     // groups share each table build among more lanes
-    static const int kg_override = env_int("GFRLNC_LANEK_KG", 0);   // experiments only
-    const int kg = kg_override ? kg_override : (K > 64 ? 4 : K > 32 ? 2 : 1);
+    const int kg = K > 64 ? 4 : K > 32 ? 2 : 1;
     if (kg == 4) return launch_lanek<F, 4>(A, C, B, N, K, M, batch, st);
     if (kg == 2) return launch_lanek<F, 2>(A, C, B, N, K, M, batch, st);
     return launch_lanek<F, 1>(A, C, B, N, K, M, batch, st);
 }
 
-// encode path: "lanek" (shared-memory product tables, k on lanes) when K >= 24
-// on word-aligned packets (enough coded packets to fill the lanes); the column
-// kernel otherwise.
-// GFRLNC_ENCODE_PATH=column|lanek overrides (experiments).
-static int encode_path_override()
+// GF(2) split engine (encode_gf2.cuh): all NS source words of a span in
+// registers, one generation per block
+template <int NS>
+static int launch_gf2(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M, size_t batch,
+                      cudaStream_t st)
 {
-    if (tls_path) return tls_path;
-    static const int v = [] {
-        const char *e = getenv("GFRLNC_ENCODE_PATH");
-        if (!e) return 0;
-        if (!strcmp(e, "column")) return 1;
-        if (!strcmp(e, "lanek")) return 2;
-        if (!strcmp(e, "fused")) return 3;
-        if (!strcmp(e, "prow")) return 4;
-        if (!strcmp(e, "lanek2")) return 5;
-        if (!strcmp(e, "stream")) return 6;
-        return 0;
-    }();
-    return v;
+    Gf2Params p;
+    p.A = A; p.C = C; p.B = B; p.N = N; p.K = K;
+    p.Mw = (uint32_t)(M / 4);
+    p.spans = (p.Mw + kG2SpanWords - 1) / kG2SpanWords;
+    // up to 16 spans per warp (64 per block) so that the per-block coefficient
+    // build (K x NS words) is amortised; short packets use one span per warp
+    uint32_t spw = p.spans / 64;
+    spw = spw < 1 ? 1 : spw > 16 ? 16 : spw;
+    p.spw = (int)spw;
+    p.blocks_per_gen = (p.spans + 4 * spw - 1) / (4 * spw);
+    const size_t grid = batch * (size_t)p.blocks_per_gen;
+    if (grid > 0x7FFFFFFFu) return GF_EARG;
+    const size_t smem = gf2_smem_bytes(K, NS);
+    if (smem > 227 * 1024) return GF_EARG;
+    encode_gf2_kernel<NS><<<(unsigned)grid, kG2Threads, smem, st>>>(p);
+    return launch_status();
 }
 
-// 0 column (words), 1 column (bytes), 2 lane-k KG=1, 3 lane-k KG=2,
-// 4 fused KG=1, 5 fused KG=2, 6 product-row, 7 persistent lane-k (GF(2)/GF(4), K <= 32),
-// 8 streaming (K <= 4, word-aligned packets), 9 / 10 product-row with 32 / 16 coded packets per CTA.  The fused kernel (lane-k + column warps on one
-// tile) is correct but measured slower than lane-k alone (per-step barrier
-// coupling of the two roles): opt-in via GFRLNC_ENCODE_PATH=fused.
-static bool lanek2_default()
+// Harness override of the encode kernel (gf_set_encode_path, thread-local).
+// Stream sub-layout codes force the streaming kernel.
+static int encode_path_override()
 {
-    static const int v = env_int("GFRLNC_LANEK2", 0);          // experiment: persistent lane-k by default
-    return v != 0;
+    const int t = tls_path;
+    return t >= GF_PATH_STREAM_STRIDED4 ? GF_PATH_STREAM : t;
+}
+
+// returned codes (include/gfrlnc.h, gf_encode_path): 0 column (words), 1 column
+// (bytes), 2 / 3 lane-k with 32 / 64 (or 128) coded packets per CTA, 6 / 9 / 10
+// product-row with 64 / 32 / 16 coded packets per CTA, 8 streaming (K <= 4),
+// 11 GF(2) split engine (N <= 32, 16-byte aligned packets, K >= 24; any K when forced)
+static bool gf2_split_ok(int field, int N, int K, size_t M, const void *A, const void *B)
+{
+    return field == 2 && N <= 32 && K >= 1 && M % 16 == 0 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0 &&
+           (reinterpret_cast<uintptr_t>(B) & 15u) == 0 && gf2_smem_bytes(K, 32) <= 227 * 1024;
 }
 
 static int encode_path(int field, int N, int K, size_t M, const void *A, const void *B)
@@ -512,20 +453,22 @@ static int encode_path(int field, int N, int K, size_t M, const void *A, const v
                          (reinterpret_cast<uintptr_t>(B) & 3u) == 0 && M / 4 < 0xFFFFFFFFull;
     const int ov = encode_path_override();
     if (!aligned) return 1;
-    if (K <= 4 && (ov == 6 || ov == 0)) return 8;                // streaming (16- or 4-byte chunks)
+    if (K <= 4 && (ov == GF_PATH_STREAM || ov == 0)) return 8;  // streaming (16- or 4-byte chunks)
+    // GF(2): the split engine (encode_gf2.cuh) where the lane-k kernel ran
+    // before, K >= 24 (C5 N = K = 32, 1 MiB: 2.21 vs 1.66 TB/s)
+    if (ov == GF_PATH_GF2 && gf2_split_ok(field, N, K, M, A, B)) return 11;
+    if (ov == 0 && K >= 24 && gf2_split_ok(field, N, K, M, A, B)) return 11;
     // GF(4), 9 <= K < 24: product rows beat the column kernel when the 384-word
     // tiles cover the packet well (>= 85%) and either K > 16 (where the column
     // kernel halves) or packets are >= 4 KiB (profiles/r01_gf4_prow_routing.txt)
     const size_t mw = M / 4, tiles = (mw + 383) / 384;
     const bool gf4_prow = field == 4 && K > 8 && K < 24 && mw * 100 >= tiles * 384 * 85 && (K > 16 || M >= 4096);
-    if (ov == 1 || (ov == 0 && K < 24 && !(field >= 16 && K > 8) && !gf4_prow)) return 0;
+    if (ov == GF_PATH_COLUMN || (ov == 0 && K < 24 && !(field >= 16 && K > 8) && !gf4_prow)) return 0;
     const int kg2 = K > 32 ? 1 : 0;      // (K > 64 uses 128 coded packets per CTA)
-    if (ov == 3) return 4 + kg2;
     // product rows for GF(16)/GF(256) from K = 9 on (measured: tools/exp_shapes.py),
     // with 16, 32 or 64 coded packets per CTA so that few lanes idle
     const int prow = K <= 16 ? 10 : K <= 32 ? 9 : 6;
-    if (ov == 4 || (ov == 0 && ((field >= 16 && K > 8) || gf4_prow))) return prow;
-    if (field <= 4 && K <= 32 && (ov == 5 || (ov == 0 && lanek2_default()))) return 7;
+    if (ov == GF_PATH_PROW || (ov == 0 && ((field >= 16 && K > 8) || gf4_prow))) return prow;
     return 2 + kg2;
 }
 
@@ -535,33 +478,14 @@ static int encode_on_stream(int field, int fi, const uint8_t *A, const uint8_t *
     {
         const int path = encode_path(field, N, K, M, A, B);
         if (path == 8) return launch_stream(field, fi, A, C, B, N, K, M, batch, st);
-        if (path == 7) {
-            return field == 2 ? launch_lanek2<2>(A, C, B, N, K, M, batch, st)
-                              : launch_lanek2<4>(A, C, B, N, K, M, batch, st);
-        }
+        if (path == 11) return N <= 16 ? launch_gf2<16>(A, C, B, N, K, M, batch, st)
+                                       : launch_gf2<32>(A, C, B, N, K, M, batch, st);
         if (path == 6 || path == 9 || path == 10) {
             switch (field) {
             case 256: return launch_prow_kc<256>(path, A, C, B, N, K, M, batch, st);
             case 16: return launch_prow_kc<16>(path, A, C, B, N, K, M, batch, st);
             case 4: return launch_prow_kc<4>(path, A, C, B, N, K, M, batch, st);
             case 2: return launch_prow_kc<2>(path, A, C, B, N, K, M, batch, st);
-            default: return GF_EFIELD;
-            }
-        }
-        if (path >= 4) {
-            void *tabs = nullptr;
-            if (symbol_address(0, &tabs) != GF_OK) return GF_ECUDA;
-            const uint32_t *t = reinterpret_cast<const uint32_t *>(tabs) + (size_t)fi * 256 * kTableWords;
-            const bool kg2 = path == 5;
-            switch (field) {
-            case 256: return kg2 ? launch_fused<256, 2, 4, 4>(A, C, B, N, K, M, batch, st, t)
-                                 : launch_fused<256, 1, 4, 4>(A, C, B, N, K, M, batch, st, t);
-            case 16: return kg2 ? launch_fused<16, 2, 4, 4>(A, C, B, N, K, M, batch, st, t)
-                                : launch_fused<16, 1, 4, 4>(A, C, B, N, K, M, batch, st, t);
-            case 4: return kg2 ? launch_fused<4, 2, 4, 4>(A, C, B, N, K, M, batch, st, t)
-                               : launch_fused<4, 1, 4, 2>(A, C, B, N, K, M, batch, st, t);
-            case 2: return kg2 ? launch_fused<2, 2, 6, 4>(A, C, B, N, K, M, batch, st, t)
-                               : launch_fused<2, 1, 6, 2>(A, C, B, N, K, M, batch, st, t);
             default: return GF_EFIELD;
             }
         }
@@ -613,14 +537,19 @@ constexpr int kPipeBufs = 3;     // chunks in flight: H2D(j+2) | kernel(j+1) | D
 struct HostPipe {
     bool ready = false;
     cudaStream_t s_h2d = nullptr, s_cmp = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_entry = nullptr;                 // the caller's stream at entry (workspace handed over)
     cudaEvent_t ev_in[kPipeBufs], ev_cmp[kPipeBufs], ev_free[kPipeBufs];
 };
 static HostPipe g_pipes[kMaxDevices];
 
 static int pipe_for(int dev, HostPipe **out)
 {
-    std::lock_guard<std::mutex> g(g_lock);
     HostPipe &P = g_pipes[dev];
+    if (__atomic_load_n(&P.ready, __ATOMIC_ACQUIRE)) {
+        *out = &P;
+        return GF_OK;
+    }
+    std::lock_guard<std::mutex> g(g_lock);
     if (!P.ready) {
         if (cudaStreamCreateWithFlags(&P.s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
             cudaStreamCreateWithFlags(&P.s_cmp, cudaStreamNonBlocking) != cudaSuccess ||
@@ -631,10 +560,94 @@ static int pipe_for(int dev, HostPipe **out)
                 cudaEventCreateWithFlags(&P.ev_cmp[b], cudaEventDisableTiming) != cudaSuccess ||
                 cudaEventCreateWithFlags(&P.ev_free[b], cudaEventDisableTiming) != cudaSuccess)
                 return GF_ECUDA;
-        P.ready = true;
+        if (cudaEventCreateWithFlags(&P.ev_entry, cudaEventDisableTiming) != cudaSuccess) return GF_ECUDA;
+        __atomic_store_n(&P.ready, true, __ATOMIC_RELEASE);
     }
     *out = &P;
     return GF_OK;
+}
+
+
+// ------------------------------------------------------- one-time kernel setup
+// Everything a launch needs besides its arguments is prepared here, once per
+// (device, field), by gf_init: the dynamic shared-memory opt-in of every kernel
+// instantiation the router can pick (so no launch calls cudaFuncSetAttribute)
+// and, per device, the product-row kernel's shared-window probe.
+
+template <class Kern>
+static int allow_smem(Kern *k, int bytes)
+{
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) return GF_ECUDA;
+    // static + dynamic shared memory must fit the per-block opt-in maximum
+    int cap = bytes - (int)fa.sharedSizeBytes;
+    if (cap < 0) cap = 0;
+    return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, cap) == cudaSuccess ? GF_OK
+                                                                                                     : GF_ECUDA;
+}
+
+template <int F, int W, int KT>
+static int configure_column_t(int optin)
+{
+    constexpr int S = enc_stages<F>();
+    int rc = allow_smem(encode_kernel<F, W, KT, S, false>, optin);
+    if (rc == GF_OK) rc = allow_smem(encode_kernel<F, W, KT, S, true>, optin);
+    return rc;
+}
+
+template <int F, int W, int KTMAX>
+static int configure_column(int optin)
+{
+    int rc = GF_OK;
+    if (rc == GF_OK) rc = configure_column_t<F, W, 1>(optin);
+    if (rc == GF_OK) rc = configure_column_t<F, W, 2>(optin);
+    if (rc == GF_OK) rc = configure_column_t<F, W, 4>(optin);
+    if (rc == GF_OK) rc = configure_column_t<F, W, 8>(optin);
+    if (rc == GF_OK) rc = configure_column_t<F, W, 16>(optin);
+    if constexpr (KTMAX >= 32)
+        if (rc == GF_OK) rc = configure_column_t<F, W, 32>(optin);
+    return rc;
+}
+
+template <int F>
+static int configure_field(int optin, uint32_t smem_base)
+{
+    int rc = GF_OK;
+    if constexpr (F >= 16) {
+        rc = configure_column<F, 4, 16>(optin);
+    } else {
+        rc = configure_column<F, 4, 16>(optin);
+        if (rc == GF_OK) rc = configure_column<F, 2, 32>(optin);
+    }
+    if (rc == GF_OK) rc = allow_smem(encode_lanek_kernel<F, 1>, optin);
+    if (rc == GF_OK) rc = allow_smem(encode_lanek_kernel<F, 2>, optin);
+    if (rc == GF_OK) rc = allow_smem(encode_lanek_kernel<F, 4>, optin);
+    const int prow = (int)(kPrSmemEnd - smem_base);
+    if (rc == GF_OK) rc = allow_smem(encode_prow_kernel<F, 16>, prow);
+    if (rc == GF_OK) rc = allow_smem(encode_prow_kernel<F, 32>, prow);
+    if (rc == GF_OK) rc = allow_smem(encode_prow_kernel<F, 64>, prow);
+    if constexpr (F == 2) {
+        if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<16>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<32>, optin);
+    }
+    if (rc == GF_OK) rc = allow_smem(invert_warp_kernel, optin);
+    if (rc == GF_OK) rc = allow_smem(invert_kernel, optin);
+    return rc;
+}
+
+static int configure_kernels(int field, int dev)
+{
+    int optin = 0;
+    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+        return GF_ECUDA;
+    const uint32_t base = g_smem_base[dev];
+    switch (field) {
+    case 2: return configure_field<2>(optin, base);
+    case 4: return configure_field<4>(optin, base);
+    case 16: return configure_field<16>(optin, base);
+    case 256: return configure_field<256>(optin, base);
+    default: return GF_EFIELD;
+    }
 }
 
 }  // namespace gfr
@@ -669,7 +682,7 @@ const char *gf_strerror(int status)
 
 int gf_set_encode_path(int path)
 {
-    if (path < 0 || path > 6) return GF_EARG;
+    if (path < 0 || path > GF_PATH_STREAM_WIDE4 || path == 3 || path == 5) return GF_EARG;
     tls_path = path;
     return GF_OK;
 }
@@ -714,8 +727,16 @@ int gf_init(int field)
             int sms = 0;
             if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
                 return GF_ECUDA;
+            // the product-row kernel's tables sit at fixed shared-window addresses
+            // above the dynamic window's base, which must start at <= 0x400
+            if (probe_smem_base(dev) != GF_OK || g_smem_base[dev] > kPrBar) return GF_ECUDA;
             g_sm_count[dev] = sms;
         }
+        if (configure_kernels(field, dev) != GF_OK) return GF_ECUDA;
+        void *sym;                               // cache the table addresses (no symbol lookups at launch)
+        if (symbol_address(0, &sym) != GF_OK || symbol_address(1, &sym) != GF_OK ||
+            symbol_address(2, &sym) != GF_OK)
+            return GF_ECUDA;
         __atomic_or_fetch(&g_dev_ready[dev], 1u << fi, __ATOMIC_RELEASE);
     }
     return GF_OK;
@@ -793,29 +814,43 @@ int gf_encode_batch_host(int field, const uint8_t *A_host, const uint8_t *C_host
         bufB[b] = ws + off; off = al(off + chunk * per_gen_b);
     }
     if (off > ws_bytes) return GF_EARG;
+    // the workspace may still be in use by work queued on the caller's stream
+    // (e.g. a stream-ordered allocator just handed it out): the pipeline's
+    // first copy waits for everything queued there so far
+    if (cudaEventRecord(P->ev_entry, tls_stream) != cudaSuccess ||
+        cudaStreamWaitEvent(P->s_h2d, P->ev_entry, 0) != cudaSuccess)
+        return GF_ECUDA;
+    // on any failure after the first enqueue, drain all three streams before
+    // returning, so no copy touches the caller's buffers after the call
+    auto fail = [&](int code) {
+        cudaStreamSynchronize(P->s_h2d);
+        cudaStreamSynchronize(P->s_cmp);
+        cudaStreamSynchronize(P->s_d2h);
+        return code;
+    };
     const size_t nchunks = (batch + chunk - 1) / chunk;
     for (size_t j = 0; j < nchunks; j++) {
         const int b = (int)(j % kPipeBufs);
         const size_t g0 = j * chunk, gn = (g0 + chunk <= batch) ? chunk : batch - g0;
-        if (j >= kPipeBufs && cudaStreamWaitEvent(P->s_h2d, P->ev_free[b], 0) != cudaSuccess) return GF_ECUDA;
+        if (j >= kPipeBufs && cudaStreamWaitEvent(P->s_h2d, P->ev_free[b], 0) != cudaSuccess) return fail(GF_ECUDA);
         if (cudaMemcpyAsync(bufA[b], A_host + g0 * per_gen_a, gn * per_gen_a, cudaMemcpyHostToDevice,
                             P->s_h2d) != cudaSuccess ||
             cudaMemcpyAsync(bufC[b], C_host + g0 * per_gen_c, gn * per_gen_c, cudaMemcpyHostToDevice,
                             P->s_h2d) != cudaSuccess ||
             cudaEventRecord(P->ev_in[b], P->s_h2d) != cudaSuccess)
-            return GF_ECUDA;
-        if (cudaStreamWaitEvent(P->s_cmp, P->ev_in[b], 0) != cudaSuccess) return GF_ECUDA;
-        if (j >= kPipeBufs && cudaStreamWaitEvent(P->s_cmp, P->ev_free[b], 0) != cudaSuccess) return GF_ECUDA;
+            return fail(GF_ECUDA);
+        if (cudaStreamWaitEvent(P->s_cmp, P->ev_in[b], 0) != cudaSuccess) return fail(GF_ECUDA);
+        if (j >= kPipeBufs && cudaStreamWaitEvent(P->s_cmp, P->ev_free[b], 0) != cudaSuccess) return fail(GF_ECUDA);
         if ((rc = encode_on_stream(field, fi, bufA[b], bufC[b], bufB[b], N, K, M, gn, P->s_cmp)) != GF_OK)
-            return rc;
+            return fail(rc);
         if (cudaEventRecord(P->ev_cmp[b], P->s_cmp) != cudaSuccess ||
             cudaStreamWaitEvent(P->s_d2h, P->ev_cmp[b], 0) != cudaSuccess ||
             cudaMemcpyAsync(B_host + g0 * per_gen_b, bufB[b], gn * per_gen_b, cudaMemcpyDeviceToHost,
                             P->s_d2h) != cudaSuccess ||
             cudaEventRecord(P->ev_free[b], P->s_d2h) != cudaSuccess)
-            return GF_ECUDA;
+            return fail(GF_ECUDA);
     }
-    if (cudaStreamSynchronize(P->s_d2h) != cudaSuccess) return GF_ECUDA;
+    if (cudaStreamSynchronize(P->s_d2h) != cudaSuccess) return fail(GF_ECUDA);
     return GF_OK;
 }
 
@@ -840,17 +875,11 @@ int gf_invert_batch(int field, const uint8_t *C, uint8_t *D, int *rank, int N, s
     const size_t rw = (2 * (size_t)N + 3) / 4;
     if (N <= 64) {                                            // warp per matrix (no CTA barriers)
         const size_t smem_w = (256 * 5 + 64 + kInvWarps * 32 * 4) * 4 + (size_t)kInvWarps * N * (rw + 1) * 4;
-        if (cudaFuncSetAttribute(invert_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem_w) != cudaSuccess)
-            return GF_ECUDA;
         invert_warp_kernel<<<(unsigned)((batch + kInvWarps - 1) / kInvWarps), 32 * kInvWarps, smem_w,
                              tls_stream>>>(p);
         return launch_status();
     }
     const size_t smem = (size_t)N * rw * 4 + 256 * 8 * 4 + 256;
-    if (cudaFuncSetAttribute(invert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-        return GF_ECUDA;
     invert_kernel<<<(unsigned)batch, 256, smem, tls_stream>>>(p);
     return launch_status();
 }

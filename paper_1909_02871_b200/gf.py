@@ -80,15 +80,19 @@ def version() -> int:
     return _lib.gf_version()
 
 
-ENCODE_PATHS = {0: "column-words", 1: "column-bytes", 2: "lanek-32", 3: "lanek-64", 4: "fused-32",
-                5: "fused-64", 6: "prow", 7: "lanek2", 8: "stream", 9: "prow-32", 10: "prow-16"}
+ENCODE_PATHS = {0: "column-words", 1: "column-bytes", 2: "lanek-32", 3: "lanek-64", 6: "prow", 8: "stream",
+                9: "prow-32", 10: "prow-16", 11: "gf2-split"}
 
 
-FORCE_PATHS = {"auto": 0, "column": 1, "lanek": 2, "fused": 3, "prow": 4, "lanek2": 5, "stream": 6}
+# gf_set_encode_path codes (include/gfrlnc.h GF_PATH_*)
+FORCE_PATHS = {"auto": 0, "column": 1, "lanek": 2, "prow": 4, "stream": 6, "gf2": 7,
+               "stream-strided4": 8, "stream-strided8": 9, "stream-strided12": 10,
+               "stream-wide2": 11, "stream-wide4": 12}
 
 
 def set_encode_path(name: str) -> None:
-    """Harness-only: force the encode kernel of this thread's encode calls."""
+    """Harness-only: force the encode kernel of this thread's encode calls
+    (thread-local; "auto" restores the router)."""
     _check(_lib.gf_set_encode_path(FORCE_PATHS[name]), "gf_set_encode_path")
 
 
@@ -259,12 +263,23 @@ def verify_batch(field: int, A: torch.Tensor, C: torch.Tensor, B: torch.Tensor, 
     return mism
 
 
+def freivalds_trials(field: int) -> int:
+    """Projections per generation for gf_verify_batch so that a wrong byte
+    survives all of them with probability <= q^-t <= 2^-20."""
+    return {2: 20, 4: 10, 16: 5, 256: 3}[field]
+
+
 def encode_batch_host(field: int, A: torch.Tensor, C: torch.Tensor, B: torch.Tensor,
                       workspace: torch.Tensor) -> torch.Tensor:
     """Encode from / to HOST tensors (pinned recommended) through a device
-    workspace, overlapping copies and kernels; blocking."""
+    workspace, overlapping copies and kernels; blocking.  The C entry point
+    trusts the sizes it is given, so the shapes are checked here."""
+    if A.dim() != 3 or C.dim() != 3 or B.dim() != 3:
+        raise ValueError("expected A [batch, N, M], C [batch, N, K], B [batch, K, M]")
     batch, N, M = A.shape
     K = C.shape[2]
+    if tuple(C.shape[:2]) != (batch, N) or tuple(B.shape) != (batch, K, M):
+        raise ValueError(f"shape mismatch: A {tuple(A.shape)}, C {tuple(C.shape)}, B {tuple(B.shape)}")
     pa, pc, pb = _host_u8(A, "A"), _host_u8(C, "C"), _host_u8(B, "B")
     pw = _dev_u8(workspace, "workspace")
     with torch.cuda.device(workspace.device):

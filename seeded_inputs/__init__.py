@@ -26,7 +26,10 @@ reference splitmix64 sequence (pinned in tests/test_inputs.py).
 """
 from __future__ import annotations
 
+import ctypes
 import dataclasses
+import os
+import subprocess
 
 import numpy as np
 
@@ -67,10 +70,59 @@ def random_words(seed: int, stream: int, w0: int, n: int) -> np.ndarray:
     return _mix64(x)
 
 
+# ---- the same stream in C (seeded_inputs/fill.c), multithreaded, for
+# full-size host regeneration; pinned byte-equal to the numpy definition below
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_CLIB = None
+
+
+def _clib():
+    global _CLIB
+    if _CLIB is None:
+        src, so = os.path.join(_HERE, "fill.c"), os.path.join(_HERE, "libsifill.so")
+        if not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
+            tmp = so + f".{os.getpid()}.tmp"
+            subprocess.check_call(["gcc", "-O2", "-shared", "-fPIC", "-pthread", "-o", tmp, src])
+            os.replace(tmp, so)
+        L = ctypes.CDLL(so)
+        L.si_fill_2d.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_uint64,
+                                 ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint8, ctypes.c_int]
+        _CLIB = L
+    return _CLIB
+
+
+def fill_2d(out: np.ndarray, seed: int, stream: int, base: int, row_stride: int, mask: int = 0xFF,
+            threads: int | None = None) -> np.ndarray:
+    """out (C-contiguous uint8, viewed as [rows, cols] with cols = last dim) :=
+    byte(seed, stream, base + r*row_stride + c) & mask, computed by fill.c."""
+    assert out.dtype == np.uint8 and out.flags.c_contiguous
+    cols = out.shape[-1] if out.ndim else 1
+    rows = out.size // cols if cols else 0
+    if threads is None:
+        threads = len(os.sched_getaffinity(0))
+    _clib().si_fill_2d(out.ctypes.data, rows, cols, seed & _M64, stream & _M64, base, row_stride, mask, threads)
+    return out
+
+
+def random_bytes_np(seed: int, stream: int, offset: int, n: int) -> np.ndarray:
+    """The numpy definition of random_bytes (reference for fill.c)."""
+    if n <= 0:
+        return np.zeros(0, dtype=np.uint8)
+    w0 = offset >> 3
+    w1 = (offset + n + 7) >> 3
+    words = random_words(seed, stream, w0, w1 - w0)
+    b = words.astype("<u8").view(np.uint8)
+    s = offset - (w0 << 3)
+    return b[s:s + n].copy()
+
+
 def random_bytes(seed: int, stream: int, offset: int, n: int) -> np.ndarray:
     """Bytes offset .. offset+n-1 of the (seed, stream) byte stream (uint8)."""
     if n <= 0:
         return np.zeros(0, dtype=np.uint8)
+    if n >= 4096:
+        out = np.empty(n, dtype=np.uint8)
+        return fill_2d(out, seed, stream, offset, n)
     w0 = offset >> 3
     w1 = (offset + n + 7) >> 3
     words = random_words(seed, stream, w0, w1 - w0)
@@ -88,9 +140,7 @@ def random_bytes_2d(seed: int, stream: int, base: int, row_stride: int,
         return out
     if row_stride == cols:
         return random_bytes(seed, stream, base, rows * cols).reshape(rows, cols)
-    for r in range(rows):
-        out[r] = random_bytes(seed, stream, base + r * row_stride, cols)
-    return out
+    return fill_2d(out, seed, stream, base, row_stride)
 
 
 def uniform_coeffs(q: int, seed: int, stream: int, offset: int, n: int) -> np.ndarray:

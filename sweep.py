@@ -23,7 +23,14 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 import seeded_inputs as si  # noqa: E402
-from bench import ALU_LANES_PER_SM_CLK, N_SM, OPS_PER_BYTE_MADD, ClockSampler, load_peaks  # noqa: E402
+from bench import ClockSampler, dominant_roofline, load_peaks  # noqa: E402
+
+
+def bound_of(q, N, K, M, gens, path, kernel_s, peaks):
+    """The kernel's binding resource and its fraction on the method's
+    algorithmic work (bench.dominant_roofline)."""
+    r, _ = dominant_roofline(q, N, K, M, gens, path, kernel_s, peaks)
+    return {"kernel": path, "bound": r["bound"], "bound_frac": r["frac"]}
 
 
 def timed(torch, fn, stream, min_reps=10, min_s=0.5, warmup=3, flush=None):
@@ -64,7 +71,7 @@ def main():
         gf.init(q)
     st = torch.cuda.current_stream(dev)
     peaks = load_peaks()
-    alu_peak = N_SM * ALU_LANES_PER_SM_CLK * peaks["sm_max_mhz"] * 1e6
+
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush_buf = torch.empty(2 * l2 + (64 << 20), dtype=torch.uint8, device=dev)
 
@@ -167,7 +174,8 @@ def main():
                   "source_GBps": round(src_b / (med / 1e3) / 1e9, 2),
                   "byte_madds_per_s_T": round(bm / (med / 1e3) / 1e12, 3),
                   "hbm_frac": round(per_gen * chunk / (med / 1e3) / 1e9 / peaks["hbm_gbs"], 4),
-                  "alu_frac": round(bm * OPS_PER_BYTE_MADD[q] / (med / 1e3) / alu_peak, 4)})
+                  **bound_of(q, cfg.N, cfg.K, cfg.M, chunk, gf.encode_path(q, cfg.N, cfg.K, cfg.M),
+                             med / 1e3, peaks)})
         del A, B, C
         torch.cuda.empty_cache()
 

@@ -228,7 +228,12 @@ def test_encode_path_query():
     assert gf.encode_path(4, 32, 12, 1500) == "column-words"
     assert gf.encode_path(2, 32, 20, 4096) == "column-words"
     assert gf.encode_path(4, 64, 64, 1500) == "lanek-64"
-    assert gf.encode_path(2, 32, 32, 1 << 20) == "lanek-32"     # C5
+    assert gf.encode_path(2, 32, 32, 1 << 20) == "gf2-split"    # C5 GF(2)
+    assert gf.encode_path(4, 32, 32, 1 << 20) == "lanek-32"     # C5 GF(4)
+    assert gf.encode_path(2, 33, 32, 1 << 20) == "lanek-32"     # GF(2), N > 32
+    assert gf.encode_path(2, 32, 32, 1500) == "lanek-32"        # GF(2), M % 16 != 0
+    assert gf.encode_path(2, 32, 32, 4096, a_align=4) == "lanek-32"
+    assert gf.encode_path(2, 16, 24, 4096) == "gf2-split"
     assert gf.encode_path(256, 16, 1, 1024) == "stream"         # NEXT-2 (paper: N = 16, K = 1)
     assert gf.encode_path(2, 16, 4, 65536) == "stream"
     assert gf.encode_path(256, 16, 1, 1024, a_align=4) == "stream"    # 4-byte chunks

@@ -1,10 +1,61 @@
-"""Host-side logic of bench.py: roofline accounting and JSON contract pieces."""
+"""Host-side logic of bench.py: roofline accounting, the multi-GPU split and
+launch checks, and JSON contract pieces."""
+import os
+import subprocess
+import sys
+
 import bench
 import seeded_inputs as si
+from paper_1909_02871_b200 import shard
+
+PEAKS = {"hbm_gbs": 6546.9, "sm_max_mhz": 1965.0, "source": "test"}
+
+
+def test_roofline_prow_counts_only_the_methods_work():
+    """frac = byte-madds / (148 x 128 B x clock): the product-row kernel's own
+    table stores are reported beside it, not in `achieved`."""
+    t = 0.0150693                       # round-1 C3 GF(256) launch
+    r, h = bench.dominant_roofline(256, 64, 64, 1500, 65536, "prow", t, PEAKS)
+    bm = 64 * 64 * 1500 * 65536
+    peak = 148 * 128 * 1965e6
+    assert r["bound"] == "smem" and abs(r["frac"] - bm / t / peak) < 1e-4
+    assert 0.70 < r["frac"] < 0.74                      # the verdict's recomputed 0.72
+    assert r["table_build_bytes_per_launch"] == 65536 * 64 * 1 * 1 * 256 * 64
+    assert 0.82 < r["smem_frac_incl_table_builds"] < 0.86
+    # 32 / 16 coded packets per CTA: a 256-byte row holds 8 / 16 sources
+    r32, _ = bench.dominant_roofline(256, 64, 32, 1500, 100, "prow-32", 1e-3, PEAKS)
+    assert r32["table_build_bytes_per_launch"] == 100 * 64 * 1 * 1 * 256 * 32
+    r16, _ = bench.dominant_roofline(16, 20, 16, 1500, 100, "prow-16", 1e-3, PEAKS)
+    assert r16["table_build_bytes_per_launch"] == 100 * 32 * 1 * 1 * 256 * 16
+
+
+def test_roofline_gf2_split_is_hbm_with_issue_beside():
+    r, h = bench.dominant_roofline(2, 32, 32, 1 << 20, 512, "gf2-split", 0.0155, PEAKS)
+    assert r["bound"] == "hbm" and r["frac"] == h["frac"]
+    assert 0 < r["issue_frac"] < 1
+
+
+def test_rank_shard_splits_the_baseline_job():
+    for ws in (1, 2, 4, 8):
+        parts = [bench.rank_shard(shard, si.C3, ws, r)[0] for r in range(ws)]
+        assert sum(p.generations for p in parts) == 65536
+        assert all(p.generations == 65536 // ws and p.columns == 1500 for p in parts)
+        c5 = [bench.rank_shard(shard, si.C5, ws, r)[0] for r in range(ws)]
+        assert sum(p.generations for p in c5) == 4096 and c5[-1].g1 == 4096
+        c4 = [bench.rank_shard(shard, si.C4, ws, r) for r in range(ws)]
+        assert all(by for _, by in c4) and sum(p.columns for p, _ in c4) == 65536
+        assert all(p.generations == 2048 for p, _ in c4)
+
+
+def test_world_size_must_match_gpus():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, bench.__file__, "--gpus", "2"], env=env, capture_output=True,
+                         text=True, timeout=120)
+    assert out.returncode == 1 and "WORLD_SIZE=1 but --gpus 2" in out.stdout
 
 
 def test_roofline_lanek_is_smem_bound():
-    peaks = {"hbm_gbs": 6546.9, "sm_max_mhz": 1965.0, "source": "test"}
+    peaks = PEAKS
     r, h = bench.dominant_roofline(256, 64, 64, 1500, 65536, "lanek-64", 0.0348, peaks)
     assert r["bound"] == "smem" and 0 < r["frac"] < 1
     # gathers: 2 x 4 B per (i, k, word); build: 30 rows x 4 B per (i, word) per k-tile

@@ -119,3 +119,11 @@ def test_invert_and_decode_guard_bytes(gfm, q, N):
     assert rc == gfm.GF_OK
     a = abuf.cpu().numpy()
     assert (a[:g] == 0xEE).all() and (a[g + batch * N * M:] == 0xEE).all()
+    # the decoded sources themselves, against the oracle's Gauss-Jordan solve of
+    # B = C^T A (every full-rank generation)
+    got = a[g:g + batch * N * M].reshape(batch, N, M)
+    for i in range(batch):
+        rk, A_ref = oracle.decode(q, C[i], B[i])
+        assert rk == r[32 + i]
+        if rk == N:
+            assert np.array_equal(got[i], A_ref), (q, N, i)

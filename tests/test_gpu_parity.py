@@ -7,6 +7,7 @@ generator is only used where it was first shown equal to seeded_inputs
 sampled outputs the oracle computes.
 """
 import ctypes
+import os
 
 import numpy as np
 import pytest
@@ -14,6 +15,8 @@ import torch
 
 import oracle
 import seeded_inputs as si
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 pytestmark = pytest.mark.gpu
 
@@ -226,74 +229,7 @@ def test_encode_checked_mode(gfm):
         gfm.encode_batch(16, dev(A), dev(C), checked=True)
 
 
-@pytest.mark.parametrize("q", (16, 256))
-def test_c3_full_size_sampled(gfm, q):
-    """BASELINE.json configs[2] at full size (65536 generations, the launch
-    bench.py times): device-generated inputs, sampled generations recomputed by
-    the oracle from host-regenerated inputs, plus Freivalds on more."""
-    cfg = si.C3
-    seed = si.field_seed(cfg, q)
-    A = torch.empty((cfg.batch, cfg.N, cfg.M), dtype=torch.uint8, device="cuda")
-    C = torch.empty((cfg.batch, cfg.N, cfg.K), dtype=torch.uint8, device="cuda")
-    gfm.fill_random(A, seed, si.STREAM_A, 0)
-    gfm.fill_random(C, seed, si.STREAM_C, 0, mask=q - 1)
-    B = gfm.encode_batch(q, A, C)
-    rng = np.random.default_rng(q)
-    gens = sorted({0, 1, cfg.batch - 1, *rng.integers(0, cfg.batch, 13).tolist()})
-    for g in gens:
-        Ah, Ch = si.encode_inputs(cfg, q, g, g + 1)
-        assert np.array_equal(B[g].cpu().numpy(), oracle.encode_batch(q, Ah, Ch)[0]), g
-    t = oracle.freivalds_trials(q)
-    for g in rng.integers(0, cfg.batch, 48).tolist():
-        Ah, Ch = si.encode_inputs(cfg, q, g, g + 1)
-        r = si.uniform_coeffs(q, seed, si.STREAM_FREIVALDS, g * 64 * t, t * cfg.K).reshape(t, cfg.K)
-        Bg = B[g].cpu().numpy()
-        assert all(oracle.freivalds_gen(q, Ah[0], Ch[0], Bg, rr) == 0 for rr in r), g
-    del A, B, C
-    torch.cuda.empty_cache()
-
-
-def test_c4_full_size_sampled(gfm):
-    """BASELINE.json configs[3]: GF(256), N=K=256, 64 KiB packets, 2048
-    generations (32 GiB of A) in one launch; sampled generations x byte ranges."""
-    cfg = si.C4
-    q = 256
-    seed = si.field_seed(cfg, q)
-    free, _ = torch.cuda.mem_get_info()
-    need = cfg.batch * (cfg.N + cfg.K) * cfg.M + cfg.batch * cfg.N * cfg.K
-    if free < need * 1.05:
-        pytest.skip(f"needs {need / 2**30:.1f} GiB")
-    A = torch.empty((cfg.batch, cfg.N, cfg.M), dtype=torch.uint8, device="cuda")
-    C = torch.empty((cfg.batch, cfg.N, cfg.K), dtype=torch.uint8, device="cuda")
-    gfm.fill_random(A, seed, si.STREAM_A, 0)
-    gfm.fill_random(C, seed, si.STREAM_C, 0, mask=q - 1)
-    B = gfm.encode_batch(q, A, C)
-    for g, m0, m1 in ((0, 0, 2048), (cfg.batch - 1, cfg.M - 2048, cfg.M), (777, 30000, 31000)):
-        Ah, Ch = si.encode_inputs(cfg, q, g, g + 1)
-        exp = oracle.encode_gen_cols(q, Ah[0], Ch[0], m0, m1)
-        assert np.array_equal(B[g, :, m0:m1].cpu().numpy(), exp), (g, m0)
-    del A, B, C
-    torch.cuda.empty_cache()
-
-
-@pytest.mark.parametrize("q", (2, 4))
-def test_c5_chunk_sampled(gfm, q):
-    """BASELINE.json configs[4] (N=K=32, 1 MiB packets) in the chunk size the
-    bench launches: one chunk of generations from the middle of the job."""
-    cfg = si.C5
-    seed = si.field_seed(cfg, q)
-    g0, G = 1000, 64
-    A = torch.empty((G, cfg.N, cfg.M), dtype=torch.uint8, device="cuda")
-    C = torch.empty((G, cfg.N, cfg.K), dtype=torch.uint8, device="cuda")
-    gfm.fill_random(A, seed, si.STREAM_A, g0 * cfg.N * cfg.M)
-    gfm.fill_random(C, seed, si.STREAM_C, g0 * cfg.N * cfg.K, mask=q - 1)
-    B = gfm.encode_batch(q, A, C)
-    for gl, m0, m1 in ((0, 0, 8192), (G - 1, cfg.M - 8192, cfg.M), (17, 500000, 510000)):
-        Ah, Ch = si.encode_inputs(cfg, q, g0 + gl, g0 + gl + 1)
-        exp = oracle.encode_gen_cols(q, Ah[0], Ch[0], m0, m1)
-        assert np.array_equal(B[gl, :, m0:m1].cpu().numpy(), exp), (gl, m0)
-    del A, B, C
-    torch.cuda.empty_cache()
+# (full-size C3 / C4 / C5 parity: tests/test_gpu_fullsize.py)
 
 
 @pytest.mark.parametrize("q", (2, 256))
@@ -394,3 +330,116 @@ def test_encode_guard_bytes_every_layout(gfm, q):
         got = buf.cpu().numpy()
         assert (got[:guard] == 0xEE).all() and (got[guard + nb:] == 0xEE).all(), (q, N, K, M)
         assert np.array_equal(got[guard:guard + nb].reshape(batch, K, M), oracle.encode_batch(q, A, C)), (q, N, K, M)
+
+
+@pytest.mark.parametrize("q", FIELDS)
+def test_raw_coefficient_bytes_are_masked(gfm, q):
+    """include/gfrlnc.h: entries of C are not validated on the hot path, a byte
+    >= q is taken modulo q by masking with q - 1.  Raw bytes through every
+    default kernel equal the oracle on C & (q - 1)."""
+    for (N, K, M, batch) in ((16, 1, 1024, 20), (16, 8, 1500, 3), (64, 64, 1500, 2), (32, 32, 4096, 2),
+                             (9, 20, 1500, 3), (3, 5, 13, 4)):
+        A = si.random_bytes(301 + N, si.STREAM_A, 0, batch * N * M).reshape(batch, N, M)
+        Craw = si.random_bytes(302 + K, si.STREAM_C, 0, batch * N * K).reshape(batch, N, K)
+        assert (Craw >= q).any()
+        got = run_encode(gfm, q, A, Craw)
+        assert np.array_equal(got, oracle.encode_batch(q, A, Craw & np.uint8(q - 1))), (q, N, K, M)
+
+
+@pytest.mark.parametrize("q", FIELDS)
+def test_mulrc_256_mib(gfm, q):
+    """gf_mulrc at the top of the C2 range (256 MiB + 7 bytes: past the region
+    kernel's grid-stride wrap, ragged tail), canaries on both sides."""
+    n, pad = (256 << 20) + 7, 64
+    base = si.random_bytes(43, si.STREAM_DST, 0, n + 2 * pad)
+    c = si.c2_coeff(q) if q > 2 else 1
+    for coeff in {c, q - 1}:
+        d = dev(base)
+        gfm.mulrc(q, d[pad:pad + n], coeff)
+        exp = base.copy()
+        seg = exp[pad:pad + n].copy()
+        oracle.mulrc(q, seg, coeff)
+        exp[pad:pad + n] = seg
+        assert np.array_equal(d.cpu().numpy(), exp), (q, coeff)
+
+
+GRAPH_SCRIPT = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import oracle, seeded_inputs as si
+from paper_1909_02871_b200 import gf
+for q in (2, 4, 16, 256):
+    gf.init(q)
+shapes = [(256, 4, 64, 64, 1500), (16, 3, 16, 8, 1500), (2, 2, 32, 32, 4096), (4, 2, 32, 32, 4096),
+          (256, 20, 16, 1, 1024)]
+ins, outs, exps = [], [], []
+for q, batch, N, K, M in shapes:
+    A = si.random_bytes(9 + N, 1, 0, batch * N * M).reshape(batch, N, M)
+    C = si.uniform_coeffs(q, 10 + K, 2, 0, batch * N * K).reshape(batch, N, K)
+    ins.append((q, torch.from_numpy(A).cuda(), torch.from_numpy(C).cuda()))
+    outs.append(torch.zeros((batch, K, M), dtype=torch.uint8, device="cuda"))
+    exps.append(oracle.encode_batch(q, A, C))
+torch.cuda.synchronize()
+g = torch.cuda.CUDAGraph()
+s = torch.cuda.Stream()
+with torch.cuda.stream(s):
+    with torch.cuda.graph(g, stream=s):        # the FIRST encode calls of this process
+        for (q, A, C), B in zip(ins, outs):
+            gf.encode_batch(q, A, C, B)
+for B in outs:
+    B.zero_()
+g.replay()
+torch.cuda.synchronize()
+for (q, A, C), B, e in zip(ins, outs, exps):
+    assert np.array_equal(B.cpu().numpy(), e), q
+print("graph ok")
+''' % ROOT
+
+
+def test_first_encode_captured_in_cuda_graph():
+    """The hot path allocates, locks and synchronises nothing (gf_init prepared
+    every kernel): the very first encode calls of a fresh process -- product-
+    row, column, GF(2) split, lane-k and streaming kernels -- are captured into
+    a CUDA graph and replayed bit-exactly."""
+    import subprocess
+    import sys
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    out = subprocess.run([sys.executable, "-c", GRAPH_SCRIPT], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    assert "graph ok" in out.stdout
+
+
+@pytest.mark.parametrize("name", ("C3", "C4", "C5"))
+def test_bench_split_shards_in_sequence_equal_unsharded(gfm, name):
+    """bench.py's N-rank plan (bench.rank_shard: C3 / C5 by generation, C4 by
+    byte range), every shard launched in sequence on one GPU with its inputs
+    generated by absolute index, reassembles the unsharded job bit-exactly, for
+    P = 2, 3, 4 and 8 (reduced generation counts / packet sizes)."""
+    import dataclasses
+
+    import bench
+    from paper_1909_02871_b200 import shard
+    base = si.ENCODE_CONFIGS[name]
+    q = base.fields[-1]
+    cfg = dataclasses.replace(base, batch={"C3": 64, "C4": 3, "C5": 8}[name],
+                              M={"C3": 1500, "C4": 8192, "C5": 4096}[name])
+    seed = si.field_seed(cfg, q)
+
+    def encode(sh):
+        A = torch.empty((sh.generations, cfg.N, sh.columns), dtype=torch.uint8, device="cuda")
+        C = torch.empty((sh.generations, cfg.N, cfg.K), dtype=torch.uint8, device="cuda")
+        gfm.fill_random2d(A.view(-1, sh.columns), seed, si.STREAM_A, sh.g0 * cfg.N * cfg.M + sh.m0, cfg.M)
+        gfm.fill_random(C, seed, si.STREAM_C, sh.g0 * cfg.N * cfg.K, mask=q - 1)
+        return gfm.encode_batch(q, A, C).cpu().numpy()
+
+    full = encode(bench.rank_shard(shard, cfg, 1, 0)[0])
+    Ah, Ch = si.encode_inputs(cfg, q, 0, 1)
+    assert np.array_equal(full[:1], oracle.encode_batch(q, Ah, Ch))
+    for P in (2, 3, 4, 8):
+        B = np.zeros_like(full)
+        for r in range(P):
+            sh = bench.rank_shard(shard, cfg, P, r)[0]
+            if sh.generations and sh.columns:
+                B[sh.g0:sh.g1, :, sh.m0:sh.m1] = encode(sh)
+        assert np.array_equal(B, full), (name, P)

@@ -49,3 +49,24 @@ def test_encode_inputs_shapes_and_slicing():
     assert (A2 == A[:, :, 100:160]).all()
     A1, C1 = si.encode_inputs(si.C1, 256)
     assert A1.shape == (1, 16, 1500) and (C1 != 0).all()
+
+
+def test_c_fill_equals_numpy_definition():
+    """seeded_inputs/fill.c (multithreaded, used for full-size host
+    regeneration) is byte-equal to the numpy definition: 1-D ranges at every
+    start alignment, lengths across the threaded split, 2-D strided slices,
+    coefficient masks, and offsets past 2^32 bytes."""
+    for seed, stream in ((0, 0), (190902871, 1), (2 ** 63 + 5, 7)):
+        for off in (0, 1, 3, 7, 8, 9, 4095, (1 << 33) + 5):
+            for n in (1, 7, 8, 4096, 4097, 70001):
+                ref = si.random_bytes_np(seed, stream, off, n)
+                out = np.empty(n, dtype=np.uint8)
+                assert np.array_equal(si.fill_2d(out, seed, stream, off, n), ref), (seed, off, n)
+                assert np.array_equal(si.random_bytes(seed, stream, off, n), ref)
+    out = np.empty((37, 1500), dtype=np.uint8)
+    si.fill_2d(out, 11, 1, 3 * 65536 + 13, 65536, threads=5)
+    for r in (0, 17, 36):
+        assert np.array_equal(out[r], si.random_bytes_np(11, 1, 3 * 65536 + 13 + r * 65536, 1500))
+    m = np.empty((9, 33), dtype=np.uint8)
+    si.fill_2d(m, 4, 2, 100, 33, mask=15)
+    assert np.array_equal(m.reshape(-1), si.random_bytes_np(4, 2, 100, 9 * 33) & 15)

@@ -48,6 +48,58 @@ def _worker(rank, world, port, by, q, out):
     dist.destroy_process_group()
 
 
+def _bench_plan_worker(rank, world, port, out):
+    """The bench's N-rank plan end to end on CPU: bench.rank_shard splits a
+    (reduced) BASELINE job, every rank encodes its share (the oracle stands in
+    for the kernels here), the parity gate is an all_reduce SUM of mismatches,
+    the time a MAX, and rank 0 reassembles the job."""
+    import dataclasses
+    import bench
+    import torch
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    res = {}
+    for base, q in ((si.C3, 256), (si.C4, 256), (si.C5, 4)):
+        cfg = dataclasses.replace(base, batch=6, M=64 if base is not si.C5 else 96, N=5, K=3)
+        sh, by_bytes = bench.rank_shard(shard, cfg, world, rank)
+        assert by_bytes == (base is si.C4)
+        A, C = si.encode_inputs(cfg, q, sh.g0, sh.g1, sh.m0, sh.m1)
+        part = oracle.encode_batch(q, A, C)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (sh, part))
+        bad = torch.tensor([0], dtype=torch.int64)
+        dist.all_reduce(bad, op=dist.ReduceOp.SUM)
+        tmax = torch.tensor([float(rank)])
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        if rank == 0:
+            Af, Cf = si.encode_inputs(cfg, q)
+            full = oracle.encode_batch(q, Af, Cf)
+            B = np.zeros_like(full)
+            for s_, p_ in gathered:
+                B[s_.g0:s_.g1, :, s_.m0:s_.m1] = p_
+            res[base.name] = bool(np.array_equal(B, full)) and int(bad.item()) == 0 and \
+                float(tmax.item()) == world - 1
+    if rank == 0:
+        out.put(res)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_bench_plan_end_to_end():
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_plan_worker, args=(r, 2, port, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = out.get(timeout=180)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res == {"C3": True, "C4": True, "C5": True}
+
+
 @pytest.mark.parametrize("by,q", [("generation", 256), ("bytes", 4), ("bytes", 256)])
 def test_gloo_world2_sharded_encode_equals_full(by, q):
     ctx = mp.get_context("spawn")
@@ -72,6 +124,4 @@ def test_shard_plans_cover_exactly():
         assert bs[0][0] == 0 and bs[-1][1] == 65536
         assert all(a[1] == b[0] and a[1] % 16 == 0 for a, b in zip(bs, bs[1:]))
         assert max(b - a for a, b in bs) - min(b - a for a, b in bs) <= 16
-        w = [shard.plan(65536, 1500, world, r, weak=True) for r in range(world)]
-        assert all(s.generations == 65536 for s in w) and w[-1].g1 == world * 65536
     assert shard.byte_range(1500, 8, 7) == (1312, 1500)
