@@ -441,7 +441,7 @@ def main():
             if str(f) in per_field:
                 continue
             xsh, _ = rank_shard(shard, xcfg, ws, rank)
-            xjob = Job(gf, torch, xcfg, f, xsh, device, 512 if xcfg is si.C5 else 0, mem_frac=0.6)
+            xjob = Job(gf, torch, xcfg, f, xsh, device, 256 if xcfg is si.C5 else 0, mem_frac=0.6)
             st = max(2, args.steps // 3) if xjob.nchunks > 1 else max(3, args.steps // 2)
             tms, kms, nl, _ = time_job(xjob, st, 1, ws, dist)
             launches += nl

@@ -28,7 +28,7 @@
 // the algorithmic N*M + K*M (+ N*K) per generation.
 //
 // Requirements (checked by the router): 1 <= N <= NS, M % 16 == 0, A and B
-// 16-byte aligned.  Sources i >= N read as zero with zero coefficients.
+// 16-byte aligned.  Sources i >= N get zero coefficients.
 #pragma once
 #include <cstdint>
 
@@ -43,7 +43,6 @@ struct Gf2Params {
     uint8_t *B;            // [batch][K][M]
     uint32_t Mw;           // 32-bit words per packet (M / 4, M % 16 == 0)
     uint32_t spans;        // 128-word spans per packet
-    uint32_t blocks_per_gen;
     int spw;               // spans per warp
     int N, K;
 };
@@ -56,50 +55,53 @@ __device__ __forceinline__ uint4 g2_ld(const uint8_t *p)
     return v;
 }
 
-__device__ __forceinline__ void g2_st(uint8_t *p, uint32_t a, uint32_t b, uint32_t c, uint32_t d)
+// predicated store (no branch, so no reconvergence barrier in the k loop)
+__device__ __forceinline__ void g2_st(uint8_t *p, uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t on)
 {
-    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" :: "l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t@q st.global.v4.u32 [%0], {%1,%2,%3,%4};\n\t}"
+                 :: "l"(p), "r"(a), "r"(b), "r"(c), "r"(d), "r"(on) : "memory");
 }
 
-template <int NS>
-__global__ void __launch_bounds__(kG2Threads) encode_gf2_kernel(Gf2Params p)
+// FULL: N == NS (no clamped source addresses).  Grid: x = block within the
+// generation (4 warps x spw spans each), y = generation (offset g_base, so that
+// more than 65535 generations take several launches).
+template <int NS, bool FULL>
+__global__ void __launch_bounds__(kG2Threads) encode_gf2_kernel(Gf2Params p, uint32_t g_base)
 {
     extern __shared__ __align__(16) uint32_t cw[];              // [K][NS]
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const size_t g = blockIdx.x / p.blocks_per_gen;
-    const uint32_t bi = blockIdx.x - (uint32_t)(g * p.blocks_per_gen);
-    const int N = p.N, K = p.K;
+    const size_t g = (size_t)g_base + blockIdx.y;
+    const int N = FULL ? NS : p.N, K = p.K;
     {
         const uint8_t *Cg = p.C + g * (size_t)N * K;
         for (int t = threadIdx.x; t < K * NS; t += kG2Threads) {
             const int k = t / NS, i = t - k * NS;
-            const uint32_t c = i < N ? (__ldg(Cg + (size_t)i * K + k) & 1u) : 0u;
+            const uint32_t c = (FULL || i < N) ? (__ldg(Cg + (size_t)i * K + k) & 1u) : 0u;
             cw[t] = (i % 3 == 2) ? 0u - c : c;              // mask for the ALU form, 0/1 for imul
         }
     }
     __syncthreads();
-    const size_t M = (size_t)p.Mw * 4;
-    const uint32_t sp0 = (bi * 4 + wid) * (uint32_t)p.spw;
+    const uint32_t Mw = p.Mw;
+    const uint32_t sp0 = (blockIdx.x * 4 + wid) * (uint32_t)p.spw;
 #pragma unroll 1
     for (int s = 0; s < p.spw; s++) {
         const uint32_t sp = sp0 + s;
         if (sp >= p.spans) break;
         const uint32_t w0 = sp * kG2SpanWords + 4 * lane;
-        const bool valid = w0 < p.Mw;
-        const uint8_t *Ag = p.A + g * (size_t)N * M + 4 * (size_t)w0;
+        const bool valid = w0 < Mw;
+        // sources i >= N re-read source 0 (their coefficients are zero, so any
+        // value gives a zero term); lanes past the packet end read word 0 and
+        // never store
+        const uint32_t *Ag = reinterpret_cast<const uint32_t *>(p.A) + g * (size_t)N * Mw + (valid ? w0 : 0u);
         uint32_t a[NS][4];
 #pragma unroll
         for (int i = 0; i < NS; i++) {
-            if (valid && i < N) {
-                const uint4 v = g2_ld(Ag + (size_t)i * M);
-                a[i][0] = v.x; a[i][1] = v.y; a[i][2] = v.z; a[i][3] = v.w;
-            } else {
-                a[i][0] = a[i][1] = a[i][2] = a[i][3] = 0u;
-            }
+            const uint4 v = g2_ld(reinterpret_cast<const uint8_t *>(Ag + (size_t)(FULL || i < N ? i : 0) * Mw));
+            a[i][0] = v.x; a[i][1] = v.y; a[i][2] = v.z; a[i][3] = v.w;
         }
-        uint8_t *Bp = p.B + g * (size_t)K * M + 4 * (size_t)w0;
+        uint32_t *Bg = reinterpret_cast<uint32_t *>(p.B) + g * (size_t)K * Mw + w0;
 #pragma unroll 1
-        for (int k = 0; k < K; k++, Bp += M) {
+        for (int k = 0; k < K; k++) {
             uint32_t c[NS];
 #pragma unroll
             for (int q = 0; q < NS / 4; q++) {
@@ -118,7 +120,8 @@ __global__ void __launch_bounds__(kG2Threads) encode_gf2_kernel(Gf2Params p)
                 }
                 acc[w] = x;
             }
-            if (valid) g2_st(Bp, acc[0], acc[1], acc[2], acc[3]);
+            g2_st(reinterpret_cast<uint8_t *>(Bg + (size_t)k * Mw), acc[0], acc[1], acc[2], acc[3],
+                  valid ? 1u : 0u);
         }
     }
 }

@@ -415,18 +415,25 @@ static int launch_gf2(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int
     p.A = A; p.C = C; p.B = B; p.N = N; p.K = K;
     p.Mw = (uint32_t)(M / 4);
     p.spans = (p.Mw + kG2SpanWords - 1) / kG2SpanWords;
-    // up to 16 spans per warp (64 per block) so that the per-block coefficient
-    // build (K x NS words) is amortised; short packets use one span per warp
-    uint32_t spw = p.spans / 64;
-    spw = spw < 1 ? 1 : spw > 16 ? 16 : spw;
+    // spans per warp: 4 for long packets (C5: 1 MiB packets = 2048 spans, 128
+    // blocks per generation; 2 - 16 measured within 1%,
+    // profiles/r02_gf2_spw.txt), fewer for short ones
+    uint32_t spw = p.spans / 512;
+    spw = spw < 1 ? 1 : spw > 4 ? 4 : spw;
     p.spw = (int)spw;
-    p.blocks_per_gen = (p.spans + 4 * spw - 1) / (4 * spw);
-    const size_t grid = batch * (size_t)p.blocks_per_gen;
-    if (grid > 0x7FFFFFFFu) return GF_EARG;
+    const uint32_t bpg = (p.spans + 4 * spw - 1) / (4 * spw);
     const size_t smem = gf2_smem_bytes(K, NS);
     if (smem > 227 * 1024) return GF_EARG;
-    encode_gf2_kernel<NS><<<(unsigned)grid, kG2Threads, smem, st>>>(p);
-    return launch_status();
+    for (size_t g0 = 0; g0 < batch; g0 += 65535) {           // grid.y <= 65535 generations per launch
+        const unsigned gy = (unsigned)(batch - g0 < 65535 ? batch - g0 : 65535);
+        if (N == NS)
+            encode_gf2_kernel<NS, true><<<dim3(bpg, gy), kG2Threads, smem, st>>>(p, (uint32_t)g0);
+        else
+            encode_gf2_kernel<NS, false><<<dim3(bpg, gy), kG2Threads, smem, st>>>(p, (uint32_t)g0);
+        const int rc = launch_status();
+        if (rc != GF_OK) return rc;
+    }
+    return GF_OK;
 }
 
 // Harness override of the encode kernel (gf_set_encode_path, thread-local).
@@ -627,8 +634,10 @@ static int configure_field(int optin, uint32_t smem_base)
     if (rc == GF_OK) rc = allow_smem(encode_prow_kernel<F, 32>, prow);
     if (rc == GF_OK) rc = allow_smem(encode_prow_kernel<F, 64>, prow);
     if constexpr (F == 2) {
-        if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<16>, optin);
-        if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<32>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<16, true>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<16, false>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<32, true>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<32, false>, optin);
     }
     if (rc == GF_OK) rc = allow_smem(invert_warp_kernel, optin);
     if (rc == GF_OK) rc = allow_smem(invert_kernel, optin);

@@ -341,7 +341,7 @@ def test_raw_coefficient_bytes_are_masked(gfm, q):
                              (9, 20, 1500, 3), (3, 5, 13, 4)):
         A = si.random_bytes(301 + N, si.STREAM_A, 0, batch * N * M).reshape(batch, N, M)
         Craw = si.random_bytes(302 + K, si.STREAM_C, 0, batch * N * K).reshape(batch, N, K)
-        assert (Craw >= q).any()
+        assert q == 256 or (Craw >= q).any()
         got = run_encode(gfm, q, A, Craw)
         assert np.array_equal(got, oracle.encode_batch(q, A, Craw & np.uint8(q - 1))), (q, N, K, M)
 

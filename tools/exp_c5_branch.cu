@@ -451,6 +451,121 @@ __global__ void __launch_bounds__(128) enc2_mixp(const uint32_t *__restrict__ A,
     }
 }
 
+
+// library-form kernel (runtime N, K or compile-time KC) for A/B against enc2_mix<4>
+template <int KC>
+__global__ void __launch_bounds__(128) enc2_libform(const uint8_t *__restrict__ A, const uint8_t *__restrict__ C,
+                                                    uint8_t *__restrict__ B, uint32_t Mw, int Nr, int Kr,
+                                                    uint32_t spans, uint32_t blocks_per_gen, int spw)
+{
+    constexpr int NS = 32;
+    extern __shared__ __align__(16) uint32_t cwd[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const size_t g = blockIdx.x / blocks_per_gen;
+    const uint32_t bi = blockIdx.x - (uint32_t)(g * blocks_per_gen);
+    const int Nn = Nr, K = KC ? KC : Kr;
+    for (int t = threadIdx.x; t < K * NS; t += 128) {
+        const int k = t / NS, i = t - k * NS;
+        const uint32_t c = i < Nn ? (__ldg(C + g * (size_t)Nn * K + (size_t)i * K + k) & 1u) : 0u;
+        cwd[t] = (i % 3 == 2) ? 0u - c : c;
+    }
+    __syncthreads();
+    const size_t M = (size_t)Mw * 4;
+    const uint32_t sp0 = (bi * 4 + wid) * (uint32_t)spw;
+#pragma unroll 1
+    for (int s = 0; s < spw; s++) {
+        const uint32_t sp = sp0 + s;
+        if (sp >= spans) break;
+        const uint32_t w0 = sp * 128 + 4 * lane;
+        const bool valid = w0 < Mw;
+        const uint8_t *Ag = A + g * (size_t)Nn * M + 4 * (size_t)(valid ? w0 : 0u);
+        uint32_t a[NS][4];
+#pragma unroll
+        for (int i = 0; i < NS; i++) {
+            const V4 v = ld4(reinterpret_cast<const uint32_t *>(Ag + (size_t)(i < Nn ? i : 0) * M));
+            a[i][0] = v.x; a[i][1] = v.y; a[i][2] = v.z; a[i][3] = v.w;
+        }
+        uint8_t *Bp = B + g * (size_t)K * M + 4 * (size_t)w0;
+#pragma unroll 1
+        for (int k = 0; k < K; k++, Bp += M) {
+            uint32_t c[NS];
+#pragma unroll
+            for (int q = 0; q < NS / 4; q++) {
+                const uint4 v = reinterpret_cast<const uint4 *>(cwd + k * NS)[q];
+                c[4 * q] = v.x; c[4 * q + 1] = v.y; c[4 * q + 2] = v.z; c[4 * q + 3] = v.w;
+            }
+            uint32_t acc[4];
+#pragma unroll
+            for (int w = 0; w < 4; w++) {
+                uint32_t x = 0;
+#pragma unroll
+                for (int i = 0; i < NS; i += 3) {
+                    if (i + 1 < NS) x ^= (a[i][w] * c[i]) ^ (a[i + 1][w] * c[i + 1]);
+                    else x ^= a[i][w] * c[i];
+                    if (i + 2 < NS) x ^= a[i + 2][w] & c[i + 2];
+                }
+                acc[w] = x;
+            }
+            if (KC) { st4(reinterpret_cast<uint32_t *>(Bp), {acc[0], acc[1], acc[2], acc[3]}); }
+            else {
+                asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t@q st.global.v4.u32 [%0], {%1,%2,%3,%4};\n\t}"
+                             :: "l"(Bp), "r"(acc[0]), "r"(acc[1]), "r"(acc[2]), "r"(acc[3]), "r"(valid ? 1u : 0u) : "memory");
+            }
+        }
+    }
+}
+
+
+// W words per lane in the strided layout (lane l: words l, l + 32, ...): W = 3
+// keeps ~124 registers (16 warps / SM instead of 12)
+template <int W>
+__global__ void __launch_bounds__(128) enc2_mixs(const uint32_t *__restrict__ A, const uint8_t *__restrict__ C,
+                                                 uint32_t *__restrict__ B, uint32_t Mw, int spans_per_warp)
+{
+    __shared__ __align__(16) uint32_t cw[K * N];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const size_t g = blockIdx.y;
+    for (int t = threadIdx.x; t < K * N; t += blockDim.x) {
+        const int k = t / N, i = t % N;
+        const uint32_t c = C[(g * N + i) * K + k] & 1u;
+        cw[t] = (i % 3 == 2) ? 0u - c : c;
+    }
+    __syncthreads();
+    const uint32_t spanw = 32 * W;
+    const uint32_t sp0 = (blockIdx.x * 4 + wid) * spans_per_warp;
+    for (int s = 0; s < spans_per_warp; s++) {
+        const uint32_t w0 = (sp0 + s) * spanw;
+        if (w0 >= Mw) break;
+        const uint32_t *Ag = A + g * N * (size_t)Mw + w0 + lane;
+        uint32_t a[N][W];
+#pragma unroll
+        for (int i = 0; i < N; i++)
+#pragma unroll
+            for (int w = 0; w < W; w++) a[i][w] = (w0 + lane + 32 * w < Mw) ? __ldcs(Ag + (size_t)i * Mw + 32 * w) : 0u;
+        uint32_t *Bg = B + g * K * (size_t)Mw + w0 + lane;
+#pragma unroll 1
+        for (int k = 0; k < K; k++) {
+            uint32_t c[N];
+#pragma unroll
+            for (int q = 0; q < N / 4; q++) {
+                const uint4 v = reinterpret_cast<const uint4 *>(cw + k * N)[q];
+                c[4 * q] = v.x; c[4 * q + 1] = v.y; c[4 * q + 2] = v.z; c[4 * q + 3] = v.w;
+            }
+#pragma unroll
+            for (int w = 0; w < W; w++) {
+                uint32_t x = 0;
+#pragma unroll
+                for (int i = 0; i < N; i += 3) {
+                    if (i + 1 < N) x ^= (a[i][w] * c[i]) ^ (a[i + 1][w] * c[i + 1]);
+                    else x ^= a[i][w] * c[i];
+                    if (i + 2 < N) x ^= a[i + 2][w] & c[i + 2];
+                }
+                if (w0 + lane + 32 * w < Mw) __stcs(Bg + (size_t)k * Mw + 32 * w, x);
+            }
+        }
+    }
+}
+
 // plain reference (bytewise, any field): B[g][k][m] = sum_i C[g][i][k] * A[g][i][m]
 __device__ uint8_t mulb(int q, uint8_t c, uint8_t v)
 {
@@ -507,7 +622,19 @@ int main(int argc, char **argv)
     enc_ref<<<(unsigned)(((size_t)Gc * K * M + 255) / 256), 256>>>(q, A, C, R, M, Gc);
     const int var = argc > 4 ? atoi(argv[4]) : 0;   // 0 branch, 1 threaded, 2 mix W=4, 3 mix W=2
     auto launch = [&](int Gl) {
-        if (var >= 4) {
+        if (var == 11 || var == 12) {
+            const uint32_t Mw = M / 4;
+            const int W = var == 11 ? 3 : 4;
+            const uint32_t spans = (Mw + 32 * W - 1) / (32 * W);
+            dim3 grid((spans + 4 * spw - 1) / (4 * spw), Gl);
+            if (W == 3) enc2_mixs<3><<<grid, 128>>>((const uint32_t *)A, C, (uint32_t *)B, Mw, spw);
+            else enc2_mixs<4><<<grid, 128>>>((const uint32_t *)A, C, (uint32_t *)B, Mw, spw);
+        } else if (var == 9 || var == 10) {
+            const uint32_t Mw = M / 4, spans = Mw / 128;
+            const uint32_t bpg = (spans + 63) / 64;
+            if (var == 9) enc2_libform<0><<<Gl * bpg, 128, 4096>>>(A, C, B, Mw, 32, 32, spans, bpg, 16);
+            else enc2_libform<32><<<Gl * bpg, 128, 4096>>>(A, C, B, Mw, 32, 32, spans, bpg, 16);
+        } else if (var >= 4) {
             const uint32_t Mw = M / 4;
             const int W = var == 4 || var == 5 ? 2 : 4;
             const uint32_t spans = Mw / (32 * W);
