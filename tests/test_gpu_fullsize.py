@@ -4,7 +4,7 @@ bench.py times, against the CPU oracle on host-regenerated inputs:
   * C3 (65536 generations, GF(16) and GF(256)): EVERY byte of every
     generation, oracle.encode_batch on all host cores;
   * C4 (2048 generations, 64 KiB packets) and the whole C5 job (4096
-    generations of 32 x 1 MiB, GF(2) and GF(4), in the bench's 512-generation
+    generations of 32 x 1 MiB, GF(2) and GF(4), in the bench's 256-generation
     chunks): >= 1% of the generations compared byte for byte with the oracle,
     plus the oracle's Freivalds projection check (oracle.freivalds_gen, Eq. 2
     PAPER.md:84-88 projected on random r) over EVERY generation.
