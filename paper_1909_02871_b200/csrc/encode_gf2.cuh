@@ -55,10 +55,11 @@ __device__ __forceinline__ uint4 g2_ld(const uint8_t *p)
     return v;
 }
 
-// predicated store (no branch, so no reconvergence barrier in the k loop)
+// predicated streaming store (no branch, so no reconvergence barrier in the k
+// loop; .cs: B is written once and not re-read: +0.4%, profiles/r02_gf2_cs.txt)
 __device__ __forceinline__ void g2_st(uint8_t *p, uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t on)
 {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t@q st.global.v4.u32 [%0], {%1,%2,%3,%4};\n\t}"
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t@q st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};\n\t}"
                  :: "l"(p), "r"(a), "r"(b), "r"(c), "r"(d), "r"(on) : "memory");
 }
 

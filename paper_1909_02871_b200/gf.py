@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 
 import torch
 
@@ -69,6 +70,9 @@ class GFError(RuntimeError):
 
 
 def lib() -> ctypes.CDLL:
+    """The raw C ABI.  A caller may set the stream itself through it, so the
+    binding's cached copy of this thread's stream is dropped."""
+    _tls.stream = None
     return _lib
 
 
@@ -136,8 +140,20 @@ def _coeff(c: int) -> int:
     return c
 
 
+# the raw current-stream pointer without building a torch.cuda.Stream object
+# (torch.cuda.current_stream costs about a microsecond per call)
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+_tls = threading.local()
+
+
 def _use_stream(device: torch.device) -> None:
-    _lib.gf_set_stream(torch.cuda.current_stream(device).cuda_stream)
+    """Hand torch's current stream of `device` to the library (gf_set_stream is
+    thread-local on both sides; the call is skipped while it is unchanged)."""
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    s = _raw_stream(idx) if _raw_stream is not None else torch.cuda.current_stream(device).cuda_stream
+    if getattr(_tls, "stream", None) != s:
+        _lib.gf_set_stream(s)
+        _tls.stream = s
 
 
 class _on_device:
@@ -145,11 +161,13 @@ class _on_device:
     __slots__ = ("idx", "prev")
 
     def __init__(self, device: torch.device):
-        self.idx = device.index if device.index is not None else torch.cuda.current_device()
+        self.idx = device.index
 
     def __enter__(self):
         self.prev = torch.cuda.current_device()
-        if self.prev != self.idx:
+        if self.idx is None:
+            self.idx = self.prev
+        elif self.prev != self.idx:
             torch.cuda.set_device(self.idx)
         return self
 
