@@ -134,6 +134,26 @@ int gf_verify_batch(int field, const uint8_t *A, const uint8_t *C, const uint8_t
                     int N, int K, size_t M, size_t batch, unsigned long long *mismatch, void *dev_ws,
                     size_t ws_bytes);
 
+/* Encode with a fused Freivalds check:
+ * B = A C exactly as gf_encode_batch, and for every generation g
+ *     mismatch[g] = sum over j < t and blocks b of 64 coded packets of
+ *                   #{ m : y1_jb[m] != y2_jb[m] },
+ *     y2_jb = sum_{k in b} r_jk b_k,   y1_jb = sum_i u_jbi a_i,
+ *     u_jbi = sum_{k in b} r_jk C[g][i][k]          (Eq. 2 projected on r_j)
+ * with BINARY projection vectors r_jk = R[g][k][j] & 1 (R: [batch][K][t]
+ * device bytes, t in {1, 2}).  B == A C gives 0; a wrong byte of B escapes one
+ * projection with probability <= 1/2 for uniform random r.  The product-row
+ * kernel (GF(16)/GF(256), K > 32: C3, C4) and the GF(2) split engine (K <= 64:
+ * C5) project the coded words while they are still in registers and the
+ * source words they already hold (one pass over A and B); every other shape
+ * runs the encode and then the same check in plain code.  dev_ws: 16-byte
+ * aligned device workspace of at least
+ *     round16(batch * ceil(K/64) * 2 * N) + batch * 2 * ceil(K/32) * 4 bytes.
+ * Returns the codes of gf_encode_batch, or GF_EARG (t, R, mismatch, workspace). */
+int gf_encode_verify_batch(int field, const uint8_t *A, const uint8_t *C, uint8_t *B, const uint8_t *R, int t,
+                           int N, int K, size_t M, size_t batch, unsigned long long *mismatch, void *dev_ws,
+                           size_t ws_bytes);
+
 /* Set the calling thread's stream (a cudaStream_t; NULL = legacy default). */
 int gf_set_stream(void *cuda_stream);
 
@@ -199,6 +219,13 @@ enum {
     GF_PATH_STREAM_WIDE4 = 12        /* streaming, four 16-byte chunks per thread                   */
 };
 int gf_set_encode_path(int path);
+
+/* Harness-only (tests of the fused check): make the calling thread's next
+ * gf_encode_verify_batch calls corrupt one byte (XOR 0x5A) of coded packet k,
+ * 32-bit word `word`, of generation g -- in the kernel before the store and
+ * the projection (fused paths) or in B after the encode (other paths).
+ * enable = 0 turns it off.  Returns GF_OK or GF_EARG. */
+int gf_set_verify_fault(int enable, size_t g, int k, size_t word);
 
 /* Library version (major * 10000 + minor * 100 + patch). */
 int gf_version(void);

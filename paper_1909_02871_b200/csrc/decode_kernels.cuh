@@ -258,6 +258,76 @@ __global__ void __launch_bounds__(256) project_coeffs_kernel(const uint8_t *C, c
     U[e] = (uint8_t)acc;
 }
 
+// gf_encode_verify_batch (NEXT-4): binary projections r_j (j < t <= 2), applied
+// per block of 64 coded packets.  U[g][b][j][i] = sum_{k in block b, r_jk = 1}
+// C[g][i][k] (an element of F_q, the A-side coefficient of projection j), and
+// RB[g][j][w] = the bits r_jk, k = 32 w .. 32 w + 31.  R: [batch][K][t] bytes,
+// r_jk = R[g][k][j] & 1.  One thread per (g, b, j, i), then per (g, j, w).
+__global__ void __launch_bounds__(256) verify_prep_kernel(const uint8_t *C, const uint8_t *R, uint8_t *U,
+                                                          uint32_t *RB, int N, int K, int t, int kblocks, int kw,
+                                                          size_t batch, int qmask)
+{
+    const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t nu = batch * (size_t)kblocks * 2 * N;
+    if (e < nu) {
+        const size_t g = e / ((size_t)kblocks * 2 * N);
+        const int rest = (int)(e % ((size_t)kblocks * 2 * N));
+        const int b = rest / (2 * N), j = (rest / N) & 1, i = rest % N;
+        uint32_t acc = 0;
+        if (j < t) {
+            const uint8_t *Cr = C + (g * N + i) * (size_t)K;
+            const uint8_t *Rg = R + g * (size_t)K * t;
+            const int k1 = min(K, 64 * b + 64);
+            for (int k = 64 * b; k < k1; k++)
+                if (Rg[(size_t)k * t + j] & 1u) acc ^= Cr[k] & (uint32_t)qmask;
+        }
+        U[e] = (uint8_t)acc;
+        return;
+    }
+    const size_t f = e - nu;
+    if (f >= batch * 2 * (size_t)kw) return;
+    const size_t g = f / (2 * (size_t)kw);
+    const int j = (int)((f / kw) & 1), w = (int)(f % kw);
+    uint32_t bits = 0;
+    if (j < t)
+        for (int k = 32 * w; k < min(K, 32 * w + 32); k++)
+            bits |= (uint32_t)(R[(g * K + k) * (size_t)t + j] & 1u) << (k - 32 * w);
+    RB[f] = bits;
+}
+
+// The same check for the encode kernels without a fused form (plain code,
+// after the encode): per (g, byte m), for every block b and projection j,
+// y1 = sum_i U[g][b][j][i] * A[g][i][m] and y2 = sum_{k in b, r_jk} B[g][k][m].
+// (packed byte products through the split tables: tabs = the field's table of
+// tables, 16 words per coefficient)
+__global__ void __launch_bounds__(256) verify_plain_kernel(const uint8_t *A, const uint8_t *B, const uint8_t *U,
+                                                           const uint32_t *RB, const uint32_t *__restrict__ tabs,
+                                                           int N, int K, int kblocks, int kw, size_t M, size_t batch,
+                                                           unsigned long long *mismatch)
+{
+    const size_t g = blockIdx.y;
+    const uint8_t *Ag = A + g * (size_t)N * M, *Bg = B + g * (size_t)K * M;
+    unsigned long long n = 0;
+    for (size_t m = (size_t)blockIdx.x * blockDim.x + threadIdx.x; m < M; m += (size_t)gridDim.x * blockDim.x)
+        for (int b = 0; b < kblocks; b++)
+            for (int j = 0; j < 2; j++) {
+                const uint8_t *Ub = U + ((g * kblocks + b) * 2 + j) * (size_t)N;
+                uint32_t y1 = 0, y2 = 0;
+                for (int i = 0; i < N; i++) {
+                    const uint32_t *t = tabs + (size_t)Ub[i] * 16u;
+                    PrmtTab T;
+                    T.t0lo = __ldg(t); T.t0hi = __ldg(t + 1); T.t1lo = __ldg(t + 2); T.t1hi = __ldg(t + 3);
+                    T.t2 = __ldg(t + 4);
+                    y1 ^= mul_word(T, Ag[(size_t)i * M + m]) & 0xFFu;
+                }
+                for (int k = 64 * b; k < min(K, 64 * b + 64); k++)
+                    if ((RB[(g * 2 + j) * kw + (k >> 5)] >> (k & 31)) & 1u) y2 ^= Bg[(size_t)k * M + m];
+                n += y1 != y2;
+            }
+    for (int o = 16; o > 0; o >>= 1) n += __shfl_down_sync(0xffffffffu, n, o);
+    if ((threadIdx.x & 31) == 0 && n) atomicAdd(mismatch + g, n);
+}
+
 // mismatch[g] += #{ positions where Y1[g] and Y2[g] differ }, Y: [batch][len]
 __global__ void __launch_bounds__(256) count_mismatch_kernel(const uint8_t *Y1, const uint8_t *Y2, size_t len,
                                                              unsigned long long *mismatch)

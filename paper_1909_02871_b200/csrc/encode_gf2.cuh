@@ -32,6 +32,8 @@
 #pragma once
 #include <cstdint>
 
+#include "gf_device.cuh"
+
 namespace gfr {
 
 constexpr int kG2Threads = 128;            // 4 warps, one generation per block
@@ -45,7 +47,15 @@ struct Gf2Params {
     uint32_t spans;        // 128-word spans per packet
     int spw;               // spans per warp
     int N, K;
+    // fused Freivalds check (T > 0 instantiations; gf_encode_verify_batch)
+    const uint8_t *U;      // [batch][1][2][N]: u_j = C r_j (bit 0), r_j binary
+    const uint32_t *RB;    // [batch][2][kw]: bit k of word k / 32 = r_jk
+    int kw;                // 32-bit words per RB row: ceil(K / 32)
+    int t;                 // projections in use (1 or 2)
+    unsigned long long *mismatch;   // [batch] += differing bytes
+    uint64_t fault;        // harness fault injection: bit 63 on, g << 32 | k << 20 | word
 };
+
 
 __device__ __forceinline__ uint4 g2_ld(const uint8_t *p)
 {
@@ -66,13 +76,22 @@ __device__ __forceinline__ void g2_st(uint8_t *p, uint32_t a, uint32_t b, uint32
 // FULL: N == NS (no clamped source addresses).  Grid: x = block within the
 // generation (4 warps x spw spans each), y = generation (offset g_base, so that
 // more than 65535 generations take several launches).
-template <int NS, bool FULL>
+//
+// T = 2: the fused Freivalds check of gf_encode_verify_batch (SURVEY 8(c) step
+// 7, 8(f) NEXT-4) on binary projection vectors r_j (j < t): while a coded
+// packet's words are still in registers, y2_j ^= b_k & -(r_jk) (one LOP3 per
+// projection and word); once per span, y1_j = XOR_i a_i & -(u_ji) with
+// u_j = C r_j from the source words already in registers; then the bytes
+// where y1_j != y2_j are counted into mismatch[g].  B == A C gives zero; a
+// wrong byte escapes one binary projection with probability <= 1/2.
+template <int NS, bool FULL, int T = 0>
 __global__ void __launch_bounds__(kG2Threads) encode_gf2_kernel(Gf2Params p, uint32_t g_base)
 {
-    extern __shared__ __align__(16) uint32_t cw[];              // [K][NS]
+    extern __shared__ __align__(16) uint32_t cw[];              // [K][NS] (+ T: mr [K][T], mu [T][NS])
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const size_t g = (size_t)g_base + blockIdx.y;
     const int N = FULL ? NS : p.N, K = p.K;
+    uint32_t *mr = cw + K * NS, *mu = mr + K * T;
     {
         const uint8_t *Cg = p.C + g * (size_t)N * K;
         for (int t = threadIdx.x; t < K * NS; t += kG2Threads) {
@@ -80,8 +99,19 @@ __global__ void __launch_bounds__(kG2Threads) encode_gf2_kernel(Gf2Params p, uin
             const uint32_t c = (FULL || i < N) ? (__ldg(Cg + (size_t)i * K + k) & 1u) : 0u;
             cw[t] = (i % 3 == 2) ? 0u - c : c;              // mask for the ALU form, 0/1 for imul
         }
+        if constexpr (T > 0) {
+            for (int e = threadIdx.x; e < K * T; e += kG2Threads) {
+                const int k = e / T, j = e - k * T;
+                mr[e] = j < p.t ? 0u - ((__ldg(p.RB + (g * 2 + j) * p.kw + (k >> 5)) >> (k & 31)) & 1u) : 0u;
+            }
+            for (int e = threadIdx.x; e < T * NS; e += kG2Threads) {
+                const int j = e / NS, i = e - j * NS;
+                mu[e] = (j < p.t && i < N) ? 0u - (__ldg(p.U + (g * 2 + j) * (size_t)N + i) & 1u) : 0u;
+            }
+        }
     }
     __syncthreads();
+    uint32_t bad = 0;
     const uint32_t Mw = p.Mw;
     const uint32_t sp0 = (blockIdx.x * 4 + wid) * (uint32_t)p.spw;
 #pragma unroll 1
@@ -101,6 +131,15 @@ __global__ void __launch_bounds__(kG2Threads) encode_gf2_kernel(Gf2Params p, uin
             a[i][0] = v.x; a[i][1] = v.y; a[i][2] = v.z; a[i][3] = v.w;
         }
         uint32_t *Bg = reinterpret_cast<uint32_t *>(p.B) + g * (size_t)K * Mw + w0;
+        // harness fault injection: the coded packet to corrupt if this lane holds the word
+        const int fk = ((p.fault >> 63) && g == ((p.fault >> 32) & 0x7FFFFFFFu) &&
+                        w0 == ((uint32_t)p.fault & 0xFFFFCu)) ? (int)((p.fault >> 20) & 0xFFFu) : -1;
+        (void)fk;
+        uint32_t y2[T > 0 ? T : 1][4];
+#pragma unroll
+        for (int j = 0; j < (T > 0 ? T : 1); j++)
+#pragma unroll
+            for (int w = 0; w < 4; w++) y2[j][w] = 0;
 #pragma unroll 1
         for (int k = 0; k < K; k++) {
             uint32_t c[NS];
@@ -121,12 +160,48 @@ __global__ void __launch_bounds__(kG2Threads) encode_gf2_kernel(Gf2Params p, uin
                 }
                 acc[w] = x;
             }
+            if constexpr (T > 0) {
+                if (k == fk) acc[p.fault & 3u] ^= 0x5Au;                // harness: one wrong byte
+#pragma unroll
+                for (int j = 0; j < T; j++) {
+                    const uint32_t m = mr[k * T + j];
+#pragma unroll
+                    for (int w = 0; w < 4; w++) y2[j][w] ^= acc[w] & m;
+                }
+            }
             g2_st(reinterpret_cast<uint8_t *>(Bg + (size_t)k * Mw), acc[0], acc[1], acc[2], acc[3],
                   valid ? 1u : 0u);
         }
+        if constexpr (T > 0) {                     // y1 from the source words, still in registers
+            const uint32_t mus = (uint32_t)__cvta_generic_to_shared(mu);
+#pragma unroll
+            for (int j = 0; j < T; j++) {
+                uint32_t x[4] = {y2[j][0], y2[j][1], y2[j][2], y2[j][3]};
+#pragma unroll
+                for (int q = 0; q < NS / 4; q++) {
+                    uint4 m;                          // volatile: read here, not hoisted across the k loop
+                    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(m.x), "=r"(m.y), "=r"(m.z), "=r"(m.w) : "r"(mus + (uint32_t)(j * NS + 4 * q) * 4u));
+#pragma unroll
+                    for (int w = 0; w < 4; w++)
+                        x[w] ^= (a[4 * q][w] & m.x) ^ (a[4 * q + 1][w] & m.y) ^ (a[4 * q + 2][w] & m.z) ^
+                                (a[4 * q + 3][w] & m.w);
+                }
+                if (valid)
+#pragma unroll
+                    for (int w = 0; w < 4; w++) bad += nz_bytes(x[w]);
+            }
+        }
+    }
+    if constexpr (T > 0) {
+        bad = __reduce_add_sync(0xffffffffu, bad);
+        if (lane == 0 && bad) atomicAdd(p.mismatch + g, (unsigned long long)bad);
     }
 }
 
-__host__ __device__ constexpr size_t gf2_smem_bytes(int K, int NS) { return (size_t)K * NS * 4; }
+__host__ __device__ constexpr size_t gf2_smem_bytes(int K, int NS, int T = 0)
+{
+    return (size_t)K * NS * 4 + (size_t)T * (K + NS) * 4;
+}
 
 }  // namespace gfr

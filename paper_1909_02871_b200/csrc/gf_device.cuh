@@ -82,6 +82,15 @@ __device__ __forceinline__ uint32_t lookup_perm(const PrmtTab &T, const Sel &s)
 
 __device__ __forceinline__ uint32_t unperm(uint32_t y) { return prmt(y, y, 0x3120u); }
 
+// number of nonzero bytes of x (the fused Freivalds checks count differing bytes)
+__device__ __forceinline__ uint32_t nz_bytes(uint32_t x)
+{
+    x |= x >> 4;
+    x |= x >> 2;
+    x |= x >> 1;
+    return __popc(x & 0x01010101u);
+}
+
 // GF(4) on packed 2-bit words (PAPER.md:276-277 masks 0x55 / 0xaa):
 // x * (a1 x + a0) = (a0 + a1) x + a1 mod x^2 + x + 1.
 __device__ __forceinline__ uint32_t gf4_xtime(uint32_t a)

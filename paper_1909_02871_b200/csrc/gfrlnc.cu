@@ -39,6 +39,7 @@ static uint32_t g_smem_base[kMaxDevices];     // shared-window address of the fi
 static std::mutex g_lock;                     // gf_init and the host pipeline's one-time setup only
 static thread_local cudaStream_t tls_stream = nullptr;
 static thread_local int tls_path = 0;          // harness: forced encode path (gf_set_encode_path)
+static thread_local uint64_t tls_fault = 0;    // harness: gf_set_verify_fault (bit 63 on)
 
 static int field_index(int field)
 {
@@ -249,11 +250,12 @@ static int probe_smem_base(int dev)
     return GF_OK;
 }
 
-template <int F, int KC>
+template <int F, int KC, int T = 0>
 static int launch_prow(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M,
-                       size_t batch, cudaStream_t st)
+                       size_t batch, cudaStream_t st, const ProwParams *vp = nullptr)
 {
     ProwParams p;
+    if (vp) p = *vp;                                           // verification fields (T > 0)
     p.A = A; p.C = C; p.B = B; p.M = M; p.Mw = (uint32_t)(M / 4);
     p.N = N; p.K = K; p.NS = (N + PrCfg<KC>::S - 1) / PrCfg<KC>::S;
     p.tiles = (int)((p.Mw + kPrTW - 1) / kPrTW);
@@ -268,8 +270,8 @@ static int launch_prow(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, in
     // steps per CTA must fit 32 bits
     if ((p.ntiles + grid - 1) / grid * (size_t)p.NS > 0x7FFFFFF0u) return GF_EARG;
     const uint32_t base = g_smem_base[dev];                   // probed by gf_init (checked <= 0x400 there)
-    const size_t smem = kPrSmemEnd - base;
-    encode_prow_kernel<F, KC><<<(unsigned)grid, kPrThreads, smem, st>>>(p);
+    const size_t smem = (T > 0 ? kPrSmemEndV : kPrSmemEnd) - base;
+    encode_prow_kernel<F, KC, T><<<(unsigned)grid, kPrThreads, smem, st>>>(p);
     return launch_status();
 }
 
@@ -407,11 +409,12 @@ static int launch_lanek_kg(const uint8_t *A, const uint8_t *C, uint8_t *B, int N
 
 // GF(2) split engine (encode_gf2.cuh): all NS source words of a span in
 // registers, one generation per block
-template <int NS>
+template <int NS, int T = 0>
 static int launch_gf2(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M, size_t batch,
-                      cudaStream_t st)
+                      cudaStream_t st, const Gf2Params *vp = nullptr)
 {
     Gf2Params p;
+    if (vp) p = *vp;                                           // verification fields (T > 0)
     p.A = A; p.C = C; p.B = B; p.N = N; p.K = K;
     p.Mw = (uint32_t)(M / 4);
     p.spans = (p.Mw + kG2SpanWords - 1) / kG2SpanWords;
@@ -422,14 +425,14 @@ static int launch_gf2(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int
     spw = spw < 1 ? 1 : spw > 4 ? 4 : spw;
     p.spw = (int)spw;
     const uint32_t bpg = (p.spans + 4 * spw - 1) / (4 * spw);
-    const size_t smem = gf2_smem_bytes(K, NS);
+    const size_t smem = gf2_smem_bytes(K, NS, T);
     if (smem > 227 * 1024) return GF_EARG;
     for (size_t g0 = 0; g0 < batch; g0 += 65535) {           // grid.y <= 65535 generations per launch
         const unsigned gy = (unsigned)(batch - g0 < 65535 ? batch - g0 : 65535);
         if (N == NS)
-            encode_gf2_kernel<NS, true><<<dim3(bpg, gy), kG2Threads, smem, st>>>(p, (uint32_t)g0);
+            encode_gf2_kernel<NS, true, T><<<dim3(bpg, gy), kG2Threads, smem, st>>>(p, (uint32_t)g0);
         else
-            encode_gf2_kernel<NS, false><<<dim3(bpg, gy), kG2Threads, smem, st>>>(p, (uint32_t)g0);
+            encode_gf2_kernel<NS, false, T><<<dim3(bpg, gy), kG2Threads, smem, st>>>(p, (uint32_t)g0);
         const int rc = launch_status();
         if (rc != GF_OK) return rc;
     }
@@ -575,6 +578,9 @@ static int pipe_for(int dev, HostPipe **out)
 }
 
 
+// harness fault injection for the unfused verify path: one wrong byte of B
+__global__ void fault_byte_kernel(uint8_t *b) { *b ^= 0x5Au; }
+
 // ------------------------------------------------------- one-time kernel setup
 // Everything a launch needs besides its arguments is prepared here, once per
 // (device, field), by gf_init: the dynamic shared-memory opt-in of every kernel
@@ -638,7 +644,18 @@ static int configure_field(int optin, uint32_t smem_base)
         if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<16, false>, optin);
         if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<32, true>, optin);
         if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<32, false>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<16, true, 2>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<16, false, 2>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<32, true, 2>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<32, false, 2>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<16, true, 1>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<16, false, 1>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<32, true, 1>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<32, false, 1>, optin);
     }
+    if constexpr (F >= 16)
+        if (rc == GF_OK) rc = allow_smem(encode_prow_kernel<F, 64, 2>, (int)(kPrSmemEndV - smem_base));
+    (void)0;
     if (rc == GF_OK) rc = allow_smem(invert_warp_kernel, optin);
     if (rc == GF_OK) rc = allow_smem(invert_kernel, optin);
     return rc;
@@ -947,6 +964,85 @@ int gf_verify_batch(int field, const uint8_t *A, const uint8_t *C, const uint8_t
         count_mismatch_kernel<<<dim3(gx, (unsigned)batch), 256, 0, st>>>(Y1, Y2, len, mismatch);
     }
     return launch_status();
+}
+
+int gf_set_verify_fault(int enable, size_t g, int k, size_t word)
+{
+    if (!enable) {
+        tls_fault = 0;
+        return GF_OK;
+    }
+    if (k < 0 || k > 0xFFF || word > 0xFFFFF || g > 0x7FFFFFFF) return GF_EARG;
+    tls_fault = (1ull << 63) | ((uint64_t)g << 32) | ((uint64_t)k << 20) | (uint64_t)word;
+    return GF_OK;
+}
+
+int gf_encode_verify_batch(int field, const uint8_t *A, const uint8_t *C, uint8_t *B, const uint8_t *R, int t,
+                           int N, int K, size_t M, size_t batch, unsigned long long *mismatch, void *dev_ws,
+                           size_t ws_bytes)
+{
+    int fi, dev;
+    int rc = check_ready(field, &fi, &dev);
+    if (rc != GF_OK) return rc;
+    size_t ab, bb, cb;
+    rc = validate_encode(field, A, C, B, N, K, M, batch, &ab, &bb, &cb);
+    if (rc != GF_OK || M == 0 || batch == 0) return rc;
+    if (t < 1 || t > 2 || !R || !mismatch || !dev_ws || (reinterpret_cast<uintptr_t>(dev_ws) & 15u)) return GF_EARG;
+    auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+    const int kblocks = (K + 63) / 64, kw = (K + 31) / 32;
+    const size_t u_bytes = al(batch * (size_t)kblocks * 2 * N), rb_bytes = batch * 2 * (size_t)kw * 4;
+    if (ws_bytes < u_bytes + rb_bytes) return GF_EARG;
+    uint8_t *U = static_cast<uint8_t *>(dev_ws);
+    uint32_t *RB = reinterpret_cast<uint32_t *>(U + u_bytes);
+    if (overlaps(U, u_bytes + rb_bytes, A, ab) || overlaps(U, u_bytes + rb_bytes, B, bb) ||
+        overlaps(U, u_bytes + rb_bytes, C, cb))
+        return GF_EOVERLAP;
+    const cudaStream_t st = tls_stream;
+    if (cudaMemsetAsync(mismatch, 0, batch * sizeof(unsigned long long), st) != cudaSuccess) return GF_ECUDA;
+    const size_t nprep = batch * (size_t)kblocks * 2 * N + batch * 2 * (size_t)kw;
+    verify_prep_kernel<<<(unsigned)((nprep + 255) / 256), 256, 0, st>>>(C, R, U, RB, N, K, t, kblocks, kw, batch,
+                                                                       field - 1);
+    if ((rc = launch_status()) != GF_OK) return rc;
+    const int path = encode_path(field, N, K, M, A, B);
+    if (path == 6 && field >= 16) {                            // fused: product-row, 64 coded packets per CTA
+        void *tabs = nullptr;
+        if (symbol_address(0, &tabs) != GF_OK) return GF_ECUDA;
+        ProwParams vp;
+        std::memset(&vp, 0, sizeof(vp));
+        vp.tabs = reinterpret_cast<const uint32_t *>(tabs) + (size_t)fi * 256 * kTableWords;
+        vp.U = U; vp.RB = RB; vp.kw = kw; vp.t = t; vp.mismatch = mismatch; vp.fault = tls_fault;
+        return field == 256 ? launch_prow<256, 64, 2>(A, C, B, N, K, M, batch, st, &vp)
+                            : launch_prow<16, 64, 2>(A, C, B, N, K, M, batch, st, &vp);
+    }
+    if (path == 11 && K <= 64) {                               // fused: GF(2) split engine
+        Gf2Params vp;
+        std::memset(&vp, 0, sizeof(vp));
+        vp.U = U; vp.RB = RB; vp.kw = kw; vp.t = t; vp.mismatch = mismatch; vp.fault = tls_fault;
+        if (t == 1)                                            // one projection: 12 warps / SM as the encode
+            return N <= 16 ? launch_gf2<16, 1>(A, C, B, N, K, M, batch, st, &vp)
+                           : launch_gf2<32, 1>(A, C, B, N, K, M, batch, st, &vp);
+        return N <= 16 ? launch_gf2<16, 2>(A, C, B, N, K, M, batch, st, &vp)
+                       : launch_gf2<32, 2>(A, C, B, N, K, M, batch, st, &vp);
+    }
+    // every other kernel: the encode, then the same check in plain code
+    if ((rc = encode_on_stream(field, fi, A, C, B, N, K, M, batch, st)) != GF_OK) return rc;
+    if (tls_fault >> 63) {
+        const size_t fg = (tls_fault >> 32) & 0x7FFFFFFFu, fk = (tls_fault >> 20) & 0xFFFu, fw = tls_fault & 0xFFFFFu;
+        if (fg < batch && fk < (size_t)K && 4 * fw < M) fault_byte_kernel<<<1, 1, 0, st>>>(B + (fg * K + fk) * M + 4 * fw);
+    }
+    void *tabs = nullptr;
+    if (symbol_address(0, &tabs) != GF_OK) return GF_ECUDA;
+    unsigned gx = (unsigned)((M + 255) / 256);
+    if (gx > 64) gx = 64;
+    for (size_t g0 = 0; g0 < batch; g0 += 65535) {
+        const size_t gn = batch - g0 < 65535 ? batch - g0 : 65535;
+        verify_plain_kernel<<<dim3(gx, (unsigned)gn), 256, 0, st>>>(
+            A + g0 * (size_t)N * M, B + g0 * (size_t)K * M, U + g0 * (size_t)kblocks * 2 * N, RB + g0 * 2 * (size_t)kw,
+            reinterpret_cast<const uint32_t *>(tabs) + (size_t)fi * 256 * kTableWords, N, K, kblocks, kw, M, gn,
+            mismatch + g0);
+        if ((rc = launch_status()) != GF_OK) return rc;
+    }
+    return GF_OK;
 }
 
 int gf_fill_random2d(uint8_t *dst, size_t rows, size_t cols, uint64_t seed, uint64_t stream,

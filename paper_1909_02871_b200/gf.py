@@ -48,6 +48,9 @@ _lib.gf_set_encode_path.argtypes = [ctypes.c_int]
 _lib.gf_encode_path.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _sz, _sz, _sz]
 _lib.gf_verify_batch.argtypes = [ctypes.c_int, _u8p, _u8p, _u8p, _u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                  _sz, _sz, ctypes.c_void_p, _u8p, _sz]
+_lib.gf_encode_verify_batch.argtypes = [ctypes.c_int, _u8p, _u8p, _u8p, _u8p, ctypes.c_int, ctypes.c_int,
+                                        ctypes.c_int, _sz, _sz, ctypes.c_void_p, _u8p, _sz]
+_lib.gf_set_verify_fault.argtypes = [ctypes.c_int, _sz, ctypes.c_int, _sz]
 _lib.gf_invert_batch.argtypes = [ctypes.c_int, _u8p, _u8p, ctypes.c_void_p, ctypes.c_int, _sz]
 _lib.gf_decode_batch.argtypes = [ctypes.c_int, _u8p, _u8p, _u8p, ctypes.c_void_p, ctypes.c_int, _sz, _sz,
                                  _u8p, _sz]
@@ -60,7 +63,7 @@ TABLE_WORDS = 16          # uint32 words per coefficient in gf_host_tables
 ABI_SYMBOLS = ("gf_init", "gf_maddrc", "gf_mulrc", "gf_encode_batch", "gf_encode_batch_host",
                "gf_set_stream", "gf_strerror", "gf_fill_random", "gf_fill_random2d",
                "gf_host_tables", "gf_version", "gf_encode_path", "gf_invert_batch", "gf_decode_batch",
-               "gf_verify_batch", "gf_set_encode_path")
+               "gf_verify_batch", "gf_set_encode_path", "gf_encode_verify_batch", "gf_set_verify_fault")
 
 
 class GFError(RuntimeError):
@@ -285,6 +288,48 @@ def freivalds_trials(field: int) -> int:
     """Projections per generation for gf_verify_batch so that a wrong byte
     survives all of them with probability <= q^-t <= 2^-20."""
     return {2: 20, 4: 10, 16: 5, 256: 3}[field]
+
+
+def verify_workspace_bytes(N: int, K: int, batch: int) -> int:
+    """Device workspace of gf_encode_verify_batch."""
+    return ((batch * -(-K // 64) * 2 * N + 15) // 16) * 16 + batch * 2 * -(-K // 32) * 4
+
+
+def encode_verify_batch(field: int, A: torch.Tensor, C: torch.Tensor, R: torch.Tensor,
+                        B: torch.Tensor | None = None, workspace: torch.Tensor | None = None):
+    """B = A C (as encode_batch) with the fused Freivalds check on binary
+    projections r_j = R[g, :, j] & 1 (R: uint8 [batch, K, t], t in {1, 2});
+    returns (B, mismatch) with mismatch an int64 tensor [batch] of differing
+    projection bytes (0 when B == A C; include/gfrlnc.h)."""
+    if A.dim() != 3 or C.dim() != 3 or R.dim() != 3 or A.shape[:2] != C.shape[:2]:
+        raise ValueError("expected A [batch, N, M], C [batch, N, K], R [batch, K, t]")
+    batch, N, M = A.shape
+    K = C.shape[2]
+    if tuple(R.shape[:2]) != (batch, K):
+        raise ValueError(f"R must have shape ({batch}, {K}, t)")
+    t = R.shape[2]
+    if B is None:
+        B = torch.empty((batch, K, M), dtype=torch.uint8, device=A.device)
+    elif tuple(B.shape) != (batch, K, M):
+        raise ValueError(f"B must have shape {(batch, K, M)}")
+    if workspace is None:
+        workspace = torch.empty(verify_workspace_bytes(N, K, batch), dtype=torch.uint8, device=A.device)
+    mism = torch.empty(batch, dtype=torch.int64, device=A.device)
+    ptrs = [_dev_u8(x, n) for x, n in ((A, "A"), (C, "C"), (B, "B"), (R, "R"), (workspace, "workspace"))]
+    with _on_device(A.device):
+        _use_stream(A.device)
+        _check(_lib.gf_encode_verify_batch(field, ptrs[0], ptrs[1], ptrs[2], ptrs[3], t, N, K, M, batch,
+                                           mism.data_ptr(), ptrs[4], workspace.numel()), "gf_encode_verify_batch")
+    return B, mism
+
+
+def set_verify_fault(g: int = -1, k: int = 0, word: int = 0) -> None:
+    """Harness-only: the calling thread's gf_encode_verify_batch calls corrupt
+    one byte of coded packet k, word `word` of generation g (g < 0: off)."""
+    if g < 0:
+        _check(_lib.gf_set_verify_fault(0, 0, 0, 0), "gf_set_verify_fault")
+    else:
+        _check(_lib.gf_set_verify_fault(1, g, k, word), "gf_set_verify_fault")
 
 
 def encode_batch_host(field: int, A: torch.Tensor, C: torch.Tensor, B: torch.Tensor,

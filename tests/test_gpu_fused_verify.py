@@ -1,0 +1,90 @@
+"""gf_encode_verify_batch: the encode with the fused
+Freivalds check -- B bit-exact against the oracle, per-generation mismatch
+counts equal to the oracle's Freivalds projections (oracle.freivalds_gen with
+the same binary r, per block of 64 coded packets), zero on a correct encode, and
+a single corrupted byte (harness fault injection inside the kernel, before the
+store and the projection) caught in exactly its generation; for the fused
+product-row and GF(2) kernels and for the plain fallback."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import seeded_inputs as si
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gfm():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1909_02871_b200 import gf
+    for q in (2, 4, 16, 256):
+        gf.init(q)
+    return gf
+
+
+def oracle_counts(q, A, C, B, R):
+    """sum over projections j and 64-coded-packet blocks of the oracle's
+    Freivalds mismatch count with r restricted to the block (binary r)."""
+    batch, N, M = A.shape
+    K = C.shape[2]
+    out = np.zeros(batch, dtype=np.int64)
+    for g in range(batch):
+        for j in range(R.shape[2]):
+            r = (R[g, :, j] & 1).astype(np.uint8)
+            for b0 in range(0, K, 64):
+                rb = np.zeros(K, dtype=np.uint8)
+                rb[b0:b0 + 64] = r[b0:b0 + 64]
+                out[g] += oracle.freivalds_gen(q, A[g], C[g], B[g], rb)
+    return out
+
+
+CASES = [  # (q, N, K, M, batch, expected kernel)
+    (256, 64, 64, 1500, 5, "prow"), (16, 64, 64, 1500, 4, "prow"), (256, 40, 100, 2000, 3, "prow"),
+    (2, 32, 32, 4096, 3, "gf2-split"), (2, 17, 40, 1040, 4, "gf2-split"), (2, 5, 24, 400, 6, "gf2-split"),
+    (4, 32, 32, 4096, 2, "lanek-32"), (256, 16, 8, 1500, 3, "column-words"), (16, 16, 1, 1024, 9, "stream"),
+    (2, 32, 80, 512, 2, "gf2-split")]
+
+
+@pytest.mark.parametrize("q,N,K,M,batch,kern", CASES)
+@pytest.mark.parametrize("t", (1, 2))
+def test_fused_verify_matches_oracle(gfm, q, N, K, M, batch, kern, t):
+    assert gfm.encode_path(q, N, K, M) == kern
+    A = si.random_bytes(500 + N, si.STREAM_A, 0, batch * N * M).reshape(batch, N, M)
+    C = si.uniform_coeffs(q, 501 + K, si.STREAM_C, 0, batch * N * K).reshape(batch, N, K)
+    R = si.random_bytes(502, si.STREAM_FREIVALDS, 0, batch * K * t).reshape(batch, K, t)
+    B, mism = gfm.encode_verify_batch(q, *(torch.from_numpy(x).cuda() for x in (A, C, R)))
+    Bh = B.cpu().numpy()
+    assert np.array_equal(Bh, oracle.encode_batch(q, A, C)), (q, N, K, M)
+    assert (mism.cpu().numpy() == 0).all()
+    # one wrong byte, injected in the kernel before the store and the projection
+    gfm.set_verify_fault(batch // 2, K - 1, (M // 4) // 3)
+    try:
+        B2, mism2 = gfm.encode_verify_batch(q, *(torch.from_numpy(x).cuda() for x in (A, C, R)))
+    finally:
+        gfm.set_verify_fault(-1)
+    B2h, got = B2.cpu().numpy(), mism2.cpu().numpy()
+    assert int((B2h != Bh).sum()) == 1 and B2h[batch // 2, K - 1, 4 * ((M // 4) // 3)] != Bh[batch // 2, K - 1, 4 * ((M // 4) // 3)]
+    exp = oracle_counts(q, A, C, B2h, R)
+    assert np.array_equal(got, exp), (got, exp)
+    rsel = R[batch // 2, K - 1, :t] & 1
+    assert (got[batch // 2] > 0) == bool(rsel.any())       # caught iff some r_j selects coded packet K-1
+    assert got.sum() == got[batch // 2]
+
+
+def test_fused_verify_full_c3_shape_every_generation(gfm):
+    """The C3 job (65536 generations, GF(256)) through the fused product-row
+    path: B identical to the plain encode, no mismatch anywhere."""
+    cfg, q = si.C3, 256
+    seed = si.field_seed(cfg, q)
+    A = torch.empty((cfg.batch, cfg.N, cfg.M), dtype=torch.uint8, device="cuda")
+    C = torch.empty((cfg.batch, cfg.N, cfg.K), dtype=torch.uint8, device="cuda")
+    R = torch.empty((cfg.batch, cfg.K, 2), dtype=torch.uint8, device="cuda")
+    gfm.fill_random(A, seed, si.STREAM_A, 0)
+    gfm.fill_random(C, seed, si.STREAM_C, 0, mask=q - 1)
+    gfm.fill_random(R, seed, si.STREAM_FREIVALDS, 0)
+    B, mism = gfm.encode_verify_batch(q, A, C, R)
+    assert int(mism.sum()) == 0
+    assert torch.equal(B, gfm.encode_batch(q, A, C))
