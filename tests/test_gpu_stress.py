@@ -1,0 +1,91 @@
+"""Race evidence without compute-sanitizer (closed on this pool): every kernel
+with an intra-CTA hand-off protocol -- the product-row kernel's producer /
+gatherer mbarrier rings (64 / 32 / 16 coded packets per CTA, plain and fused
+verify), the lane-k kernel's named FULL / EMPTY barriers, the warp-per-matrix
+and CTA-per-matrix inversions -- and the GF(2) split engine are launched many
+times while a memory-bound kernel runs concurrently on a second stream (so SMs,
+L2 and DRAM are shared with a changing neighbour and warp timing varies from
+launch to launch).  Every output must be bitwise identical to the first and
+equal to the oracle on sampled generations.  A missing barrier or a stale
+table read shows up as a launch-dependent output here."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import seeded_inputs as si
+
+pytestmark = pytest.mark.gpu
+
+REPS = 25
+
+
+@pytest.fixture(scope="module")
+def gfm():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1909_02871_b200 import gf
+    for q in (2, 4, 16, 256):
+        gf.init(q)
+    return gf
+
+
+def perturbed(fn, reps=REPS):
+    """fn() REPS times on the current stream while a 1 GiB fill kernel keeps
+    another stream busy; returns the list of outputs."""
+    noise = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
+    side = torch.cuda.Stream()
+    from paper_1909_02871_b200 import gf
+    outs = []
+    for r in range(reps):
+        with torch.cuda.stream(side):
+            gf.fill_random(noise[: (1 << 20) << (r % 11)], r, 9, 0)
+        outs.append(fn())
+    torch.cuda.synchronize()
+    return outs
+
+
+@pytest.mark.parametrize("q,N,K,M,G,kern", [
+    (256, 64, 64, 1500, 2048, "prow"), (16, 64, 32, 1500, 2048, "prow-32"), (256, 20, 16, 1500, 4096, "prow-16"),
+    (4, 32, 32, 65536, 24, "lanek-32"), (4, 64, 64, 4096, 96, "lanek-64"), (2, 32, 32, 65536, 24, "gf2-split")])
+def test_encode_kernels_deterministic_under_perturbation(gfm, q, N, K, M, G, kern):
+    assert gfm.encode_path(q, N, K, M) == kern
+    A = torch.empty((G, N, M), dtype=torch.uint8, device="cuda")
+    C = torch.empty((G, N, K), dtype=torch.uint8, device="cuda")
+    gfm.fill_random(A, 31 + q, si.STREAM_A, 0)
+    gfm.fill_random(C, 31 + q, si.STREAM_C, 0, mask=q - 1)
+    outs = perturbed(lambda: gfm.encode_batch(q, A, C))
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0]), kern
+    for g in (0, G // 2, G - 1):
+        Ah = si.random_bytes(31 + q, si.STREAM_A, g * N * M, N * M).reshape(1, N, M)
+        Ch = si.uniform_coeffs(q, 31 + q, si.STREAM_C, g * N * K, N * K).reshape(1, N, K)
+        assert np.array_equal(outs[0][g].cpu().numpy(), oracle.encode_batch(q, Ah, Ch)[0]), (kern, g)
+
+
+@pytest.mark.parametrize("q", (2, 256))
+def test_fused_verify_deterministic_under_perturbation(gfm, q):
+    N, K, M, G = (64, 64, 1500, 2048) if q == 256 else (32, 32, 65536, 24)
+    A = torch.empty((G, N, M), dtype=torch.uint8, device="cuda")
+    C = torch.empty((G, N, K), dtype=torch.uint8, device="cuda")
+    R = torch.empty((G, K, 2), dtype=torch.uint8, device="cuda")
+    gfm.fill_random(A, 41, si.STREAM_A, 0)
+    gfm.fill_random(C, 41, si.STREAM_C, 0, mask=q - 1)
+    gfm.fill_random(R, 41, si.STREAM_FREIVALDS, 0)
+    ref = gfm.encode_batch(q, A, C)
+    outs = perturbed(lambda: gfm.encode_verify_batch(q, A, C, R))
+    for B, mism in outs:
+        assert torch.equal(B, ref) and int(mism.sum()) == 0
+
+
+@pytest.mark.parametrize("q,N", [(256, 64), (16, 33), (256, 80), (2, 130)])
+def test_inversion_deterministic_under_perturbation(gfm, q, N):
+    G = 4096 if N <= 64 else 256
+    C = torch.empty((G, N, N), dtype=torch.uint8, device="cuda")
+    gfm.fill_random(C, 51 + N, si.STREAM_C, 0, mask=q - 1)
+    outs = perturbed(lambda: gfm.invert_batch(q, C))
+    D0, r0 = outs[0]
+    for D, r in outs[1:]:
+        assert torch.equal(r, r0) and torch.equal(D[r0 == N], D0[r0 == N])
+    Ch = si.uniform_coeffs(q, 51 + N, si.STREAM_C, 0, 16 * N * N).reshape(16, N, N)
+    assert all(oracle.rank(q, Ch[g]) == int(r0[g]) for g in range(16))
