@@ -443,7 +443,8 @@ def main():
             xsh, _ = rank_shard(shard, xcfg, ws, rank)
             xjob = Job(gf, torch, xcfg, f, xsh, device, 256 if xcfg is si.C5 else 0, mem_frac=0.6)
             st = max(2, args.steps // 3) if xjob.nchunks > 1 else max(3, args.steps // 2)
-            tms, kms, nl, _ = time_job(xjob, st, 1, ws, dist)
+            xsampler = ClockSampler(local)
+            tms, kms, nl, xclk = time_job(xjob, st, 1, ws, dist, xsampler)
             launches += nl
             xsrc = xcfg.batch * xcfg.N * xcfg.M
             xval = xsrc * st / (tms / 1e3) / 1e9
@@ -453,6 +454,7 @@ def main():
             xpath = gf.encode_path(f, xcfg.N, xcfg.K, xjob.Ms)
             per_field[str(f)] = field_entry(xval, xcfg, f, xpath, tms / st, tms, kms, xsrc, st, peaks, xsh, ws,
                                             chunk=xjob.chunk, nchunks=xjob.nchunks)
+            per_field[str(f)]["clocks"] = xclk
             xjob.free()
             del xjob
             torch.cuda.empty_cache()
