@@ -53,6 +53,12 @@ def test_abi_validation_without_gpu():
     assert L.gf_init(3) == gf.GF_EFIELD
     assert L.gf_maddrc(5, None, None, 1, 16) == gf.GF_EFIELD
     assert L.gf_encode_batch(7, None, None, None, 1, 1, 1, 1) == gf.GF_EFIELD
+    assert L.gf_encode_verify_batch(3, None, None, None, None, 1, 1, 1, 1, 1, None, None, 0) == gf.GF_EFIELD
+    assert L.gf_set_verify_fault(1, 0, 4096, 0) == gf.GF_EARG           # k > 4095
+    assert L.gf_set_verify_fault(1, 0, 3, 1 << 21) == gf.GF_EARG        # word > 2^20 - 1
+    assert L.gf_set_verify_fault(0, 0, 0, 0) == gf.GF_OK
+    assert gf.verify_workspace_bytes(64, 64, 65536) == 65536 * 2 * 64 + 65536 * 2 * 2 * 4
+    assert gf.verify_workspace_bytes(256, 256, 3) == ((3 * 4 * 2 * 256 + 15) // 16) * 16 + 3 * 2 * 8 * 4
 
 
 # ---- PRMT emulation ------------------------------------------------------------

@@ -88,3 +88,29 @@ def test_fused_verify_full_c3_shape_every_generation(gfm):
     B, mism = gfm.encode_verify_batch(q, A, C, R)
     assert int(mism.sum()) == 0
     assert torch.equal(B, gfm.encode_batch(q, A, C))
+
+
+def test_encode_verify_argument_errors(gfm):
+    L = gfm.lib()
+    batch, N, K, M = 2, 8, 4, 64
+    A = torch.zeros((batch, N, M), dtype=torch.uint8, device="cuda")
+    C = torch.zeros((batch, N, K), dtype=torch.uint8, device="cuda")
+    B = torch.zeros((batch, K, M), dtype=torch.uint8, device="cuda")
+    R = torch.zeros((batch, K, 2), dtype=torch.uint8, device="cuda")
+    mism = torch.zeros(batch, dtype=torch.int64, device="cuda")
+    need = gfm.verify_workspace_bytes(N, K, batch)
+    ws = torch.zeros(need + 32, dtype=torch.uint8, device="cuda")
+
+    def call(t=2, r=R, m=mism, w=ws.data_ptr(), n=need, b=B.data_ptr()):
+        return L.gf_encode_verify_batch(256, A.data_ptr(), C.data_ptr(), b, r.data_ptr() if r is not None else None,
+                                        t, N, K, M, batch, m.data_ptr() if m is not None else None, w, n)
+    assert call() == gfm.GF_OK
+    assert call(t=0) == gfm.GF_EARG and call(t=3) == gfm.GF_EARG
+    assert call(r=None) == gfm.GF_EARG and call(m=None) == gfm.GF_EARG
+    assert call(n=need - 1) == gfm.GF_EARG                           # short workspace
+    assert call(w=ws.data_ptr() + 4) == gfm.GF_EARG                  # not 16-byte aligned
+    assert call(w=A.data_ptr()) == gfm.GF_EOVERLAP                   # workspace over A
+    assert call(b=A.data_ptr()) == gfm.GF_EOVERLAP                   # B over A
+    assert L.gf_encode_verify_batch(256, A.data_ptr(), C.data_ptr(), B.data_ptr(), R.data_ptr(), 2, N, K, M, 0,
+                                    mism.data_ptr(), ws.data_ptr(), need) == gfm.GF_OK   # empty batch
+    torch.cuda.synchronize()
