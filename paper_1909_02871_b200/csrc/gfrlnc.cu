@@ -13,6 +13,7 @@
 #include "encode_kernels.cuh"
 #include "encode_lanek.cuh"
 #include "encode_prow.cuh"
+#include "encode_prow16.cuh"
 #include "encode_stream.cuh"
 #include "encode_gf2.cuh"
 #include "decode_kernels.cuh"
@@ -275,6 +276,29 @@ static int launch_prow(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, in
     return launch_status();
 }
 
+// GF(16), 64 coded packets per CTA: the nibble-table product-row kernel (encode_prow16.cuh)
+static int launch_prow16(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M, size_t batch,
+                         cudaStream_t st)
+{
+    ProwParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.A = A; p.C = C; p.B = B; p.M = M; p.Mw = (uint32_t)(M / 4);
+    p.N = N; p.K = K; p.NS = (N + 3) / 4;
+    p.tiles = (int)((p.Mw + kPrTW - 1) / kPrTW);
+    p.k_tiles = (K + 63) / 64;
+    p.qmask4 = 0x0F0F0F0Fu;
+    p.cword = (K % 4 == 0 && (reinterpret_cast<uintptr_t>(C) & 3u) == 0) ? 1 : 0;
+    p.ntiles = batch * (size_t)p.tiles * (size_t)p.k_tiles;
+    int dev;
+    if (current_device(&dev) != GF_OK) return GF_ECUDA;
+    const size_t sms = (size_t)(g_sm_count[dev] > 0 ? g_sm_count[dev] : 148);
+    const size_t grid = p.ntiles < sms ? p.ntiles : sms;
+    if ((p.ntiles + grid - 1) / grid * (size_t)p.NS > 0x7FFFFFF0u) return GF_EARG;
+    const size_t smem = kNbSmemEnd - g_smem_base[dev];
+    encode_prow16_kernel<<<(unsigned)grid, kPrThreads, smem, st>>>(p);
+    return launch_status();
+}
+
 // product-row kernel with 64 (path 6), 32 (path 9) or 16 (path 10) coded packets per CTA
 template <int F>
 static int launch_prow_kc(int path, const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M,
@@ -450,7 +474,8 @@ static int encode_path_override()
 // returned codes (include/gfrlnc.h, gf_encode_path): 0 column (words), 1 column
 // (bytes), 2 / 3 lane-k with 32 / 64 (or 128) coded packets per CTA, 6 / 9 / 10
 // product-row with 64 / 32 / 16 coded packets per CTA, 8 streaming (K <= 4),
-// 11 GF(2) split engine (N <= 32, 16-byte aligned packets, K >= 24; any K when forced)
+// 11 GF(2) split engine (N <= 32, 16-byte aligned packets, K >= 24; any K when forced),
+// 12 GF(16) product-row with nibble-indexed tables (K > 32)
 static bool gf2_split_ok(int field, int N, int K, size_t M, const void *A, const void *B)
 {
     return field == 2 && N <= 32 && K >= 1 && M % 16 == 0 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0 &&
@@ -477,7 +502,8 @@ static int encode_path(int field, int N, int K, size_t M, const void *A, const v
     const int kg2 = K > 32 ? 1 : 0;      // (K > 64 uses 128 coded packets per CTA)
     // product rows for GF(16)/GF(256) from K = 9 on (measured: tools/exp_shapes.py),
     // with 16, 32 or 64 coded packets per CTA so that few lanes idle
-    const int prow = K <= 16 ? 10 : K <= 32 ? 9 : 6;
+    // (GF(16) with 64 coded packets per CTA: the nibble-table kernel, path 12)
+    const int prow = K <= 16 ? 10 : K <= 32 ? 9 : field == 16 ? 12 : 6;
     if (ov == GF_PATH_PROW || (ov == 0 && ((field >= 16 && K > 8) || gf4_prow))) return prow;
     return 2 + kg2;
 }
@@ -488,6 +514,7 @@ static int encode_on_stream(int field, int fi, const uint8_t *A, const uint8_t *
     {
         const int path = encode_path(field, N, K, M, A, B);
         if (path == 8) return launch_stream(field, fi, A, C, B, N, K, M, batch, st);
+        if (path == 12) return launch_prow16(A, C, B, N, K, M, batch, st);
         if (path == 11) return N <= 16 ? launch_gf2<16>(A, C, B, N, K, M, batch, st)
                                        : launch_gf2<32>(A, C, B, N, K, M, batch, st);
         if (path == 6 || path == 9 || path == 10) {
@@ -639,6 +666,8 @@ static int configure_field(int optin, uint32_t smem_base)
     if (rc == GF_OK) rc = allow_smem(encode_prow_kernel<F, 16>, prow);
     if (rc == GF_OK) rc = allow_smem(encode_prow_kernel<F, 32>, prow);
     if (rc == GF_OK) rc = allow_smem(encode_prow_kernel<F, 64>, prow);
+    if constexpr (F == 16)
+        if (rc == GF_OK) rc = allow_smem(encode_prow16_kernel, (int)(kNbSmemEnd - smem_base));
     if constexpr (F == 2) {
         if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<16, true>, optin);
         if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<16, false>, optin);
@@ -1004,7 +1033,7 @@ int gf_encode_verify_batch(int field, const uint8_t *A, const uint8_t *C, uint8_
                                                                        field - 1);
     if ((rc = launch_status()) != GF_OK) return rc;
     const int path = encode_path(field, N, K, M, A, B);
-    if (path == 6 && field >= 16) {                            // fused: product-row, 64 coded packets per CTA
+    if ((path == 6 || path == 12) && field >= 16) {           // fused: product-row (byte tables), 64 per CTA
         void *tabs = nullptr;
         if (symbol_address(0, &tabs) != GF_OK) return GF_ECUDA;
         ProwParams vp;

@@ -88,7 +88,7 @@ def version() -> int:
 
 
 ENCODE_PATHS = {0: "column-words", 1: "column-bytes", 2: "lanek-32", 3: "lanek-64", 6: "prow", 8: "stream",
-                9: "prow-32", 10: "prow-16", 11: "gf2-split"}
+                9: "prow-32", 10: "prow-16", 11: "gf2-split", 12: "prow-nib"}
 
 
 # gf_set_encode_path codes (include/gfrlnc.h GF_PATH_*)

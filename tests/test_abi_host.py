@@ -221,7 +221,7 @@ def test_gf16_permuted_imul_matches_prmt_order():
 
 def test_encode_path_query():
     assert gf.encode_path(256, 64, 64, 1500) == "prow"          # C3
-    assert gf.encode_path(16, 64, 64, 1500) == "prow"
+    assert gf.encode_path(16, 64, 64, 1500) == "prow-nib"       # C3 GF(16): nibble tables
     assert gf.encode_path(256, 256, 256, 65536) == "prow"       # C4
     assert gf.encode_path(256, 64, 32, 1500) == "prow-32"
     assert gf.encode_path(16, 32, 16, 1500) == "prow-16"

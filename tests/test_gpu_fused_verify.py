@@ -42,7 +42,7 @@ def oracle_counts(q, A, C, B, R):
 
 
 CASES = [  # (q, N, K, M, batch, expected kernel)
-    (256, 64, 64, 1500, 5, "prow"), (16, 64, 64, 1500, 4, "prow"), (256, 40, 100, 2000, 3, "prow"),
+    (256, 64, 64, 1500, 5, "prow"), (16, 64, 64, 1500, 4, "prow-nib"), (256, 40, 100, 2000, 3, "prow"),
     (2, 32, 32, 4096, 3, "gf2-split"), (2, 17, 40, 1040, 4, "gf2-split"), (2, 5, 24, 400, 6, "gf2-split"),
     (4, 32, 32, 4096, 2, "lanek-32"), (256, 16, 8, 1500, 3, "column-words"), (16, 16, 1, 1024, 9, "stream"),
     (2, 32, 80, 512, 2, "gf2-split")]
