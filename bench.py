@@ -544,12 +544,12 @@ def dominant_roofline(q, N, K, Ms, gens, path, kernel_s, peaks):
     smem_src = (f"{N_SM} SMs x {SMEM_BYTES_PER_SM_CLK} B/clk shared-memory pipe x "
                 f"{peaks['sm_max_mhz']:.0f} MHz (max SM clock; DESIGN.md 6)")
     if path.startswith("prow"):
-        kc = {"prow": 64, "prow-32": 32, "prow-16": 16, "prow-nib": 64}[path]
-        m_tiles = -(-(Ms // 4) // 384)
+        kc = {"prow": 64, "prow-32": 32, "prow-16": 16, "prow-nib": 64, "prow-32w": 32}[path]
+        m_tiles = -(-(Ms // 4) // (768 if path == "prow-32w" else 384))
         k_tiles = -(-K // kc)
         s = 256 // kc                                   # sources per step (a table row is 256 B)
         n_pad = -(-N // s) * s
-        builds = gens * n_pad * k_tiles * m_tiles * 256 * kc
+        builds = gens * n_pad * k_tiles * m_tiles * 256 * kc * (2 if path == "prow-32w" else 1)
         if path == "prow-nib":                          # 16 rows of 256 B per step of 4 sources
             builds = gens * (n_pad // 4) * k_tiles * m_tiles * 16 * 256
         ach = bm / kernel_s
@@ -592,7 +592,7 @@ def dominant_roofline(q, N, K, Ms, gens, path, kernel_s, peaks):
 
 
 KERNEL_SOURCES = {"prow": "encode_prow.cuh", "prow-32": "encode_prow.cuh", "prow-16": "encode_prow.cuh",
-                  "prow-nib": "encode_prow16.cuh",
+                  "prow-nib": "encode_prow16.cuh", "prow-32w": "encode_prow.cuh",
                   "lanek-32": "encode_lanek.cuh", "lanek-64": "encode_lanek.cuh", "stream": "encode_stream.cuh",
                   "column-words": "encode_kernels.cuh", "gf2-split": "encode_gf2.cuh"}
 

@@ -197,7 +197,9 @@ int gf_host_tables(int field, uint32_t *out, size_t cap_words);
  * two or four per thread, or 4-byte words one or 4 / 8 / 12 strided per
  * thread -- follows from M, the alignment and the job size), 11 = GF(2) split
  * engine (GF(2), K >= 24, N <= 32, M % 16 == 0, 16-byte aligned A and B: C5),
- * 12 = GF(16) product-row kernel with nibble-indexed tables (K > 32: C3 GF(16))
+ * 12 = GF(16) product-row kernel with nibble-indexed tables (K > 32: C3 GF(16)),
+ * 13 = GF(256) product-row kernel with 32 coded packets per CTA on 768-word
+ * tiles (K > 32, packets of >= 6144 words tiled >= 90%: C4)
  * (DESIGN.md section 6), or GF_EFIELD / GF_EARG. */
 int gf_encode_path(int field, int N, int K, size_t M, size_t a_align, size_t b_align);
 

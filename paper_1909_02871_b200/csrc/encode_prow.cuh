@@ -65,13 +65,13 @@ constexpr int kPrTW = 384;                    // words per tile
 // source packets, a quarter-warp is WQ words x NKC 16-byte coefficient chunks
 // (8 lanes on 8 distinct bank slots) and a lane holds R words (64 or 32
 // accumulator registers).
-template <int KC> struct PrCfg {
+template <int KC, int TW = kPrTW> struct PrCfg {
     static constexpr int S = 256 / KC;                         // sources per step (4 / 8)
     static constexpr int NKC = KC / 16;                        // 16-B chunks per source row (4 / 2)
     static constexpr int WQ = 8 / NKC;                         // words per quarter-warp (2 / 4)
     static constexpr int WPW = 4 * WQ;                         // words per warp per round
-    static constexpr int R = kPrTW / (kPrGW * WPW);            // words per gatherer lane (4 / 2)
-    static_assert(R * kPrGW * WPW == kPrTW, "tile geometry");
+    static constexpr int R = TW / (kPrGW * WPW);               // words per gatherer lane (4 / 2; 4 for KC = 32, TW = 768)
+    static_assert(R * kPrGW * WPW == TW, "tile geometry");
 };
 constexpr uint32_t kPrBar = 0x0400u;          // mbarriers: BUILT[4], DONE[4] at the dynamic window base
 constexpr uint32_t kPrTab0 = 0x1000u;         // tables u = 0, 1, 2 at kPrTab0 + u * 0x10000
@@ -201,11 +201,13 @@ template <uint32_t V> struct PrU { static constexpr uint32_t value = V; };
 // per word) into y1_j; at write-back, y2_j ^= b_k & -(r_jk) for the lane's 16
 // coded packets; the four chunk lanes of a word XOR-reduce y1 ^ y2 and count
 // the nonzero bytes into mismatch[g].
-template <int F, int KC, int VT = 0>
+// TW: words per tile (384; 768 with 32 coded packets per CTA for long packets:
+// a table then serves twice the gathers, halving the build share)
+template <int F, int KC, int VT = 0, int TW = kPrTW>
 __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p)
 {
-    static_assert(VT == 0 || KC == 64, "fused verification: 64 coded packets per CTA");
-    using Cf = PrCfg<KC>;
+    static_assert(VT == 0 || (KC == 64 && TW == kPrTW), "fused verification: 64 coded packets per CTA");
+    using Cf = PrCfg<KC, TW>;
     constexpr int kPrS = Cf::S, NKC = Cf::NKC;
     // mbarrier rings, object x & 3 for step x: BUILT(x) (4 producer-warp
     // arrivals) is phase x >> 2; DONE(x) (12 gatherer-warp arrivals) is phase
@@ -222,7 +224,7 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
         PrTile r;
         const int kt = (int)(t % (size_t)p.k_tiles);
         const size_t rest = t / (size_t)p.k_tiles;
-        r.w0 = (uint32_t)(rest % (size_t)p.tiles) * kPrTW;
+        r.w0 = (uint32_t)(rest % (size_t)p.tiles) * TW;
         r.g = rest / (size_t)p.tiles;
         r.k0 = kt * KC;
         return r;
@@ -326,7 +328,7 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
             const uint32_t j = x / (uint32_t)p.NS, st = x - j * (uint32_t)p.NS;
             if (j >= ntj) return;
             const PrTile T = tile_of(j);
-            const uint32_t nw = min((uint32_t)kPrTW, p.Mw - T.w0);
+            const uint32_t nw = min((uint32_t)TW, p.Mw - T.w0);
             const uint8_t *row0 = p.A + T.g * (size_t)p.N * p.M + 4 * (size_t)T.w0;
             if (st == 0) {                                      // a new tile: its coefficient block too
                 const uintptr_t c = reinterpret_cast<uintptr_t>(p.C + T.g * (size_t)p.N * p.K);

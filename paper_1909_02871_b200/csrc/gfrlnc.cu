@@ -251,15 +251,15 @@ static int probe_smem_base(int dev)
     return GF_OK;
 }
 
-template <int F, int KC, int T = 0>
+template <int F, int KC, int T = 0, int TW = kPrTW>
 static int launch_prow(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M,
                        size_t batch, cudaStream_t st, const ProwParams *vp = nullptr)
 {
     ProwParams p;
     if (vp) p = *vp;                                           // verification fields (T > 0)
     p.A = A; p.C = C; p.B = B; p.M = M; p.Mw = (uint32_t)(M / 4);
-    p.N = N; p.K = K; p.NS = (N + PrCfg<KC>::S - 1) / PrCfg<KC>::S;
-    p.tiles = (int)((p.Mw + kPrTW - 1) / kPrTW);
+    p.N = N; p.K = K; p.NS = (N + PrCfg<KC, TW>::S - 1) / PrCfg<KC, TW>::S;
+    p.tiles = (int)((p.Mw + TW - 1) / TW);
     p.k_tiles = (K + KC - 1) / KC;
     p.qmask4 = (uint32_t)(F - 1) * 0x01010101u;
     p.cword = (K % 4 == 0 && (reinterpret_cast<uintptr_t>(C) & 3u) == 0) ? 1 : 0;
@@ -272,7 +272,7 @@ static int launch_prow(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, in
     if ((p.ntiles + grid - 1) / grid * (size_t)p.NS > 0x7FFFFFF0u) return GF_EARG;
     const uint32_t base = g_smem_base[dev];                   // probed by gf_init (checked <= 0x400 there)
     const size_t smem = (T > 0 ? kPrSmemEndV : kPrSmemEnd) - base;
-    encode_prow_kernel<F, KC, T><<<(unsigned)grid, kPrThreads, smem, st>>>(p);
+    encode_prow_kernel<F, KC, T, TW><<<(unsigned)grid, kPrThreads, smem, st>>>(p);
     return launch_status();
 }
 
@@ -305,6 +305,7 @@ static int launch_prow_kc(int path, const uint8_t *A, const uint8_t *C, uint8_t 
                           size_t batch, cudaStream_t st)
 {
     if (path == 10) return launch_prow<F, 16>(A, C, B, N, K, M, batch, st);
+    if (path == 13) return launch_prow<F, 32, 0, 768>(A, C, B, N, K, M, batch, st);
     if (path == 9) return launch_prow<F, 32>(A, C, B, N, K, M, batch, st);
     return launch_prow<F, 64>(A, C, B, N, K, M, batch, st);
 }
@@ -475,7 +476,8 @@ static int encode_path_override()
 // (bytes), 2 / 3 lane-k with 32 / 64 (or 128) coded packets per CTA, 6 / 9 / 10
 // product-row with 64 / 32 / 16 coded packets per CTA, 8 streaming (K <= 4),
 // 11 GF(2) split engine (N <= 32, 16-byte aligned packets, K >= 24; any K when forced),
-// 12 GF(16) product-row with nibble-indexed tables (K > 32)
+// 12 GF(16) product-row with nibble-indexed tables (K > 32), 13 GF(256)
+// product-row with 32 coded packets per CTA on 768-word tiles (K > 32, long packets)
 static bool gf2_split_ok(int field, int N, int K, size_t M, const void *A, const void *B)
 {
     return field == 2 && N <= 32 && K >= 1 && M % 16 == 0 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0 &&
@@ -502,8 +504,13 @@ static int encode_path(int field, int N, int K, size_t M, const void *A, const v
     const int kg2 = K > 32 ? 1 : 0;      // (K > 64 uses 128 coded packets per CTA)
     // product rows for GF(16)/GF(256) from K = 9 on (measured: tools/exp_shapes.py),
     // with 16, 32 or 64 coded packets per CTA so that few lanes idle
-    // (GF(16) with 64 coded packets per CTA: the nibble-table kernel, path 12)
-    const int prow = K <= 16 ? 10 : K <= 32 ? 9 : field == 16 ? 12 : 6;
+    // (GF(16) with 64 coded packets per CTA: the nibble-table kernel, path 12;
+    // GF(256), K > 32, long packets whose 768-word tiles cover >= 90%: 32 coded
+    // packets per CTA on 768-word tiles, half the table-build share, path 13:
+    // C4 112.9 -> 115.8 GB/s, profiles/r02_c4_768.txt)
+    const size_t tiles768 = (mw + 767) / 768;
+    const bool long768 = field == 256 && K > 32 && mw >= 8 * 768 && mw * 10 >= tiles768 * 768 * 9;
+    const int prow = K <= 16 ? 10 : K <= 32 ? 9 : field == 16 ? 12 : long768 ? 13 : 6;
     if (ov == GF_PATH_PROW || (ov == 0 && ((field >= 16 && K > 8) || gf4_prow))) return prow;
     return 2 + kg2;
 }
@@ -517,7 +524,7 @@ static int encode_on_stream(int field, int fi, const uint8_t *A, const uint8_t *
         if (path == 12) return launch_prow16(A, C, B, N, K, M, batch, st);
         if (path == 11) return N <= 16 ? launch_gf2<16>(A, C, B, N, K, M, batch, st)
                                        : launch_gf2<32>(A, C, B, N, K, M, batch, st);
-        if (path == 6 || path == 9 || path == 10) {
+        if (path == 6 || path == 9 || path == 10 || path == 13) {
             switch (field) {
             case 256: return launch_prow_kc<256>(path, A, C, B, N, K, M, batch, st);
             case 16: return launch_prow_kc<16>(path, A, C, B, N, K, M, batch, st);
@@ -666,6 +673,7 @@ static int configure_field(int optin, uint32_t smem_base)
     if (rc == GF_OK) rc = allow_smem(encode_prow_kernel<F, 16>, prow);
     if (rc == GF_OK) rc = allow_smem(encode_prow_kernel<F, 32>, prow);
     if (rc == GF_OK) rc = allow_smem(encode_prow_kernel<F, 64>, prow);
+    if (rc == GF_OK) rc = allow_smem(encode_prow_kernel<F, 32, 0, 768>, prow);
     if constexpr (F == 16)
         if (rc == GF_OK) rc = allow_smem(encode_prow16_kernel, (int)(kNbSmemEnd - smem_base));
     if constexpr (F == 2) {

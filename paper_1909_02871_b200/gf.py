@@ -88,7 +88,8 @@ def version() -> int:
 
 
 ENCODE_PATHS = {0: "column-words", 1: "column-bytes", 2: "lanek-32", 3: "lanek-64", 6: "prow", 8: "stream",
-                9: "prow-32", 10: "prow-16", 11: "gf2-split", 12: "prow-nib"}
+                9: "prow-32", 10: "prow-16", 11: "gf2-split", 12: "prow-nib",
+                13: "prow-32w"}
 
 
 # gf_set_encode_path codes (include/gfrlnc.h GF_PATH_*)

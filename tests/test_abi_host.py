@@ -222,7 +222,11 @@ def test_gf16_permuted_imul_matches_prmt_order():
 def test_encode_path_query():
     assert gf.encode_path(256, 64, 64, 1500) == "prow"          # C3
     assert gf.encode_path(16, 64, 64, 1500) == "prow-nib"       # C3 GF(16): nibble tables
-    assert gf.encode_path(256, 256, 256, 65536) == "prow"       # C4
+    assert gf.encode_path(256, 256, 256, 65536) == "prow-32w"   # C4: 768-word tiles
+    assert gf.encode_path(256, 64, 64, 8192) == "prow"          # 2048 words: < 8 tiles of 768
+    assert gf.encode_path(256, 64, 64, 4 * 6200) == "prow"      # 768-word tiles would cover 6200 words at 89.7%
+    assert gf.encode_path(256, 64, 64, 4 * 7000) == "prow-32w"  # 91.1%
+    assert gf.encode_path(16, 256, 256, 65536) == "prow-nib"
     assert gf.encode_path(256, 64, 32, 1500) == "prow-32"
     assert gf.encode_path(16, 32, 16, 1500) == "prow-16"
     assert gf.encode_path(256, 16, 8, 1500) == "column-words"

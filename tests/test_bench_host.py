@@ -25,6 +25,8 @@ def test_roofline_prow_counts_only_the_methods_work():
     # 32 / 16 coded packets per CTA: a 256-byte row holds 8 / 16 sources
     r32, _ = bench.dominant_roofline(256, 64, 32, 1500, 100, "prow-32", 1e-3, PEAKS)
     assert r32["table_build_bytes_per_launch"] == 100 * 64 * 1 * 1 * 256 * 32
+    r32w, _ = bench.dominant_roofline(256, 256, 256, 65536, 2, "prow-32w", 1e-3, PEAKS)
+    assert r32w["table_build_bytes_per_launch"] == 2 * 256 * 8 * 22 * 256 * 32 * 2    # 8 k-tiles, 22 tiles of 768
     r16, _ = bench.dominant_roofline(16, 20, 16, 1500, 100, "prow-16", 1e-3, PEAKS)
     assert r16["table_build_bytes_per_launch"] == 100 * 32 * 1 * 1 * 256 * 16
 

@@ -21,7 +21,8 @@ CASES = {
     "lanek": [(q, s) for q in ALL for s in GENERIC],
     "prow": [(q, s) for q in ALL for s in GENERIC] +
             [(q, s) for q in (16, 256) for s in ((1, 64, 1500, 5), (3, 1, 1536, 9), (4, 70, 4, 400),
-                                                 (19, 12, 1500, 3), (16, 16, 16384, 2), (40, 9, 388, 7))],
+                                                 (19, 12, 1500, 3), (16, 16, 16384, 2), (40, 9, 388, 7),
+                                                 (33, 65, 28000, 2), (5, 40, 24576, 2))],
     # GF(2) split engine: N <= 32, 16-byte multiple packets (ragged last span,
     # N < 16 and 16 < N < 32 instances, K from 1 to 96)
     "gf2": [(2, s) for s in ((32, 32, 4096, 3), (17, 33, 1504, 3), (5, 24, 400, 3), (32, 1, 512, 4),

@@ -48,6 +48,7 @@ def perturbed(fn, reps=REPS):
 @pytest.mark.parametrize("q,N,K,M,G,kern", [
     (256, 64, 64, 1500, 2048, "prow"), (16, 64, 32, 1500, 2048, "prow-32"), (256, 20, 16, 1500, 4096, "prow-16"),
     (16, 64, 64, 1500, 2048, "prow-nib"), (16, 40, 100, 2000, 1024, "prow-nib"),
+    (256, 256, 256, 65536, 4, "prow-32w"),
     (4, 32, 32, 65536, 24, "lanek-32"), (4, 64, 64, 4096, 96, "lanek-64"), (2, 32, 32, 65536, 24, "gf2-split")])
 def test_encode_kernels_deterministic_under_perturbation(gfm, q, N, K, M, G, kern):
     assert gfm.encode_path(q, N, K, M) == kern
