@@ -643,6 +643,7 @@ int main(int argc, char **argv)
             else if (var == 5) enc4_mix<99><<<grid, 128>>>((const uint32_t *)A, C, (uint32_t *)B, Mw, spw);
             else if (var == 6) enc2_mixp<4, 3><<<grid, 128>>>((const uint32_t *)A, C, (uint32_t *)B, Mw, spw);
             else if (var == 7) enc2_mixp<4, 4><<<grid, 128>>>((const uint32_t *)A, C, (uint32_t *)B, Mw, spw);
+            else if (var == 13) enc2_mixp<4, 1><<<grid, 128>>>((const uint32_t *)A, C, (uint32_t *)B, Mw, spw);
             else enc2_mixp<4, 2><<<grid, 128>>>((const uint32_t *)A, C, (uint32_t *)B, Mw, spw);
         } else if (var >= 2) {
             const uint32_t Mw = M / 4;
@@ -673,7 +674,7 @@ int main(int argc, char **argv)
     size_t bad = 0;
     for (size_t j = 0; j < (size_t)Gc * K * M; j++) bad += hb[j] != hr[j];
     for (int it = 0; it < 3; it++) launch(G);
-    const int reps = 10;
+    const int reps = argc > 5 ? atoi(argv[5]) : 10;
     cudaEventRecord(e0);
     for (int it = 0; it < reps; it++) launch(G);
     cudaEventRecord(e1);
