@@ -307,6 +307,8 @@ class Job:
         up to max_gens generations spread over the chunk; returns the number of
         mismatching bytes."""
         torch, gf, q = self.torch, self.gf, self.q
+        if n <= 0:
+            return 0, 0
         step = max(1, n // max(1, max_gens))
         idx = torch.arange(0, n, step, device=self.device)[:max_gens]
         t = gf.freivalds_trials(q)
@@ -410,11 +412,12 @@ def main():
 
     # roofline of the dominant kernel: the encode launch (every launch of the
     # timed region is one); algorithmic work per launch / mean launch duration
-    avg_kernel_s = statistics.mean(kern_ms) / 1e3
+    # (a rank without generations -- C1 at N > 1 -- launches nothing)
+    avg_kernel_s = max(statistics.mean(kern_ms) if kern_ms else 0.0, 1e-6) / 1e3
     path = gf.encode_path(q, N, K, job.Ms)
     roof, hbm = dominant_roofline(q, N, K, job.Ms, job.chunk, path, avg_kernel_s, peaks)
     roof["traffic"] = lookup_traffic(q, cfg, job.chunk, job.Ms, path)
-    roof["kernel_ms"] = round(statistics.mean(kern_ms), 4)
+    roof["kernel_ms"] = round(statistics.mean(kern_ms), 4) if kern_ms else None
 
     # the oracle's sample compared with the GPU's bytes (rank 0, N = 1): the
     # first generations of the job, still resident when the job is one chunk
@@ -493,7 +496,7 @@ def main():
             "e2e": e2e,
             "clocks": clocks,
             "gpu_launches": launches,
-            "kernel_ms_per_launch": round(statistics.mean(kern_ms), 4),
+            "kernel_ms_per_launch": round(statistics.mean(kern_ms), 4) if kern_ms else None,
             "parity": "ok" if nbad == 0 else "FAIL",
             "parity_detail": parity,
         }

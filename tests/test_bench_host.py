@@ -99,3 +99,13 @@ def test_reference_arm_c1_line(capsys):
     line = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] == 0
     assert line["cpu_baseline"]["kind"] == "oracle"
+
+
+def test_job_plan_for_a_rank_without_work():
+    """C1 has one generation: at N = 8 seven ranks hold none.  Their shard is
+    empty and the bench code paths that divide by a launch time do not."""
+    for r in range(1, 8):
+        sh, _ = bench.rank_shard(shard, si.C1, 8, r)
+        assert sh.generations == 0
+    r, h = bench.dominant_roofline(256, 16, 1, 1500, 0, "stream", 1e-9, PEAKS)
+    assert r["byte_madds_per_launch"] == 0
