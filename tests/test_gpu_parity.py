@@ -443,3 +443,42 @@ def test_bench_split_shards_in_sequence_equal_unsharded(gfm, name):
             if sh.generations and sh.columns:
                 B[sh.g0:sh.g1, :, sh.m0:sh.m1] = encode(sh)
         assert np.array_equal(B, full), (name, P)
+
+
+def test_round2_kernels_edge_cases(gfm):
+    """Edge cases of the round-2 kernels against the oracle: the GF(2) split
+    engine over more than 65535 generations (several grid-y launches) and
+    through the fused check (absolute generation index of the counts); the
+    GF(16) nibble-table kernel with a misaligned coefficient pointer and
+    K % 4 != 0 (scalar coefficient loads, partial 64-packet tile); the GF(256)
+    768-word-tile kernel with a ragged last tile and two coded-packet tiles."""
+    # GF(2), 70000 generations of N = 2, K = 24, 16-byte packets
+    q, G, N, K, M = 2, 70000, 2, 24, 16
+    A = si.random_bytes(61, si.STREAM_A, 0, G * N * M).reshape(G, N, M)
+    C = si.uniform_coeffs(q, 62, si.STREAM_C, 0, G * N * K).reshape(G, N, K)
+    assert gfm.encode_path(q, N, K, M) == "gf2-split"
+    exp = oracle.encode_batch(q, A, C)
+    assert np.array_equal(run_encode(gfm, q, A, C), exp)
+    R = si.random_bytes(63, si.STREAM_FREIVALDS, 0, G * K).reshape(G, K, 1)
+    gfm.set_verify_fault(69999, 5, 2)
+    try:
+        B, mism = gfm.encode_verify_batch(q, dev(A), dev(C), dev(R))
+    finally:
+        gfm.set_verify_fault(-1)
+    m = mism.cpu().numpy()
+    assert int(m.sum()) == int(m[69999]) == int(R[69999, 5, 0] & 1)
+    # GF(16) nibble tables: C viewed at an odd address, K = 67
+    q, G, N, K, M = 16, 3, 37, 67, 1500
+    A = si.random_bytes(64, si.STREAM_A, 0, G * N * M).reshape(G, N, M)
+    C = si.random_bytes(65, si.STREAM_C, 0, G * N * K).reshape(G, N, K)
+    assert gfm.encode_path(q, N, K, M) == "prow-nib"
+    cbuf = torch.zeros(C.size + 1, dtype=torch.uint8, device="cuda")
+    cbuf[1:] = dev(C.reshape(-1))
+    got = gfm.encode_batch(q, dev(A), cbuf[1:].view(G, N, K)).cpu().numpy()
+    assert np.array_equal(got, oracle.encode_batch(q, A, C & 15))
+    # GF(256) 768-word tiles: 6400 words (9 tiles, the last 256 words), K = 100 (four 32-packet tiles)
+    q, G, N, K, M = 256, 2, 9, 100, 4 * 6400
+    A = si.random_bytes(66, si.STREAM_A, 0, G * N * M).reshape(G, N, M)
+    C = si.uniform_coeffs(q, 67, si.STREAM_C, 0, G * N * K).reshape(G, N, K)
+    assert gfm.encode_path(q, N, K, M) == "prow-32w"
+    assert np.array_equal(run_encode(gfm, q, A, C), oracle.encode_batch(q, A, C))
