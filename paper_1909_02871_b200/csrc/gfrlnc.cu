@@ -255,7 +255,7 @@ template <int F, int KC, int T = 0, int TW = kPrTW>
 static int launch_prow(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M,
                        size_t batch, cudaStream_t st, const ProwParams *vp = nullptr)
 {
-    ProwParams p;
+    ProwParams p{};
     if (vp) p = *vp;                                           // verification fields (T > 0)
     p.A = A; p.C = C; p.B = B; p.M = M; p.Mw = (uint32_t)(M / 4);
     p.N = N; p.K = K; p.NS = (N + PrCfg<KC, TW>::S - 1) / PrCfg<KC, TW>::S;
