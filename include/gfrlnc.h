@@ -134,7 +134,7 @@ int gf_verify_batch(int field, const uint8_t *A, const uint8_t *C, const uint8_t
                     int N, int K, size_t M, size_t batch, unsigned long long *mismatch, void *dev_ws,
                     size_t ws_bytes);
 
-/* Encode with a fused Freivalds check:
+/* Encode with a Freivalds check:
  * B = A C exactly as gf_encode_batch, and for every generation g
  *     mismatch[g] = sum over j < t and blocks b of 64 coded packets of
  *                   #{ m : y1_jb[m] != y2_jb[m] },
@@ -142,11 +142,12 @@ int gf_verify_batch(int field, const uint8_t *A, const uint8_t *C, const uint8_t
  *     u_jbi = sum_{k in b} r_jk C[g][i][k]          (Eq. 2 projected on r_j)
  * with BINARY projection vectors r_jk = R[g][k][j] & 1 (R: [batch][K][t]
  * device bytes, t in {1, 2}).  B == A C gives 0; a wrong byte of B escapes one
- * projection with probability <= 1/2 for uniform random r.  The product-row
- * kernel (GF(16)/GF(256), K > 32: C3, C4) and the GF(2) split engine (K <= 64:
- * C5) project the coded words while they are still in registers and the
- * source words they already hold (one pass over A and B); every other shape
- * runs the encode and then the same check in plain code.  dev_ws: 16-byte
+ * projection with probability <= 1/2 for uniform random r.  The GF(2) split
+ * engine (K <= 64: C5) projects the coded words while they are still in
+ * registers and the source words it already holds (HBM-bound, so no second
+ * pass over A and B); every other kernel (the product-row kernels of C3 / C4
+ * among them) runs the encode and then one streaming pass over A and B in the
+ * same call, on the same stream.  dev_ws: 16-byte
  * aligned device workspace of at least
  *     round16(batch * ceil(K/64) * 2 * N) + batch * 2 * ceil(K/32) * 4 bytes.
  * Returns the codes of gf_encode_batch, or GF_EARG (t, R, mismatch, workspace). */
@@ -223,10 +224,10 @@ enum {
 };
 int gf_set_encode_path(int path);
 
-/* Harness-only (tests of the fused check): make the calling thread's next
+/* Harness-only (tests of the check): make the calling thread's next
  * gf_encode_verify_batch calls corrupt one byte (XOR 0x5A) of coded packet k,
  * 32-bit word `word`, of generation g -- in the kernel before the store and
- * the projection (fused paths) or in B after the encode (other paths).
+ * the projection (GF(2) split engine) or in B after the encode (other paths).
  * enable = 0 turns it off.  Returns GF_OK or GF_EARG. */
 int gf_set_verify_fault(int enable, size_t g, int k, size_t word);
 

@@ -328,6 +328,119 @@ __global__ void __launch_bounds__(256) verify_plain_kernel(const uint8_t *A, con
     if ((threadIdx.x & 31) == 0 && n) atomicAdd(mismatch + g, n);
 }
 
+// The same check, word-parallel and streaming (M % 4 == 0, A and B 4-byte
+// aligned): one warp per (generation g, chunk of 128 words), lane = words
+// w0 + lane + 32 v (v < 4).  A and B are each read once from HBM; per source i
+// and projection j the split tables of u_ji come through warp-uniform loads
+// (the field's table of tables stays in L1); y1 accumulates in the permuted
+// byte order of lookup_perm and is un-permuted once per block.  r_jk is
+// warp-uniform, so y2 is a masked XOR per coded row.  Bytes where y1 != y2 are
+// counted per generation (same count as verify_plain_kernel).
+constexpr int kVwW = 4;                                       // words per lane
+template <int T>
+__global__ void __launch_bounds__(256) verify_words_kernel(const uint8_t *A, const uint8_t *B, const uint8_t *U,
+                                                           const uint32_t *RB, const uint32_t *__restrict__ tabs,
+                                                           int N, int K, int kblocks, int kw, size_t M, size_t batch,
+                                                           unsigned long long *mismatch)
+{
+    const size_t Mw = M / 4;
+    const size_t chunks = (Mw + 32 * kVwW - 1) / (32 * kVwW);
+    const size_t unit = (size_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (unit >= batch * chunks) return;
+    const int lane = threadIdx.x & 31;
+    const size_t g = unit / chunks;
+    const size_t w0 = (unit - g * chunks) * (32 * kVwW) + (size_t)lane;
+    const uint32_t *Ag = reinterpret_cast<const uint32_t *>(A + g * (size_t)N * M) + w0;
+    const uint32_t *Bg = reinterpret_cast<const uint32_t *>(B + g * (size_t)K * M) + w0;
+    bool ok[kVwW];
+#pragma unroll
+    for (int v = 0; v < kVwW; v++) ok[v] = w0 + 32 * v < Mw;
+    uint32_t bad = 0;
+    for (int b = 0; b < kblocks; b++) {
+        uint32_t y1[T][kVwW], y2[T][kVwW];
+#pragma unroll
+        for (int j = 0; j < T; j++)
+#pragma unroll
+            for (int v = 0; v < kVwW; v++) y1[j][v] = y2[j][v] = 0u;
+        const uint8_t *Ub = U + (g * kblocks + b) * 2 * (size_t)N;
+        // source words of four sources in flight while two are multiplied
+        // (HBM latency, not issue, bounds a warp that waits per source)
+        auto load2 = [&](int i, uint32_t (&a)[2][kVwW]) {
+#pragma unroll
+            for (int h = 0; h < 2; h++)
+#pragma unroll
+                for (int v = 0; v < kVwW; v++)
+                    a[h][v] = (ok[v] && i + h < N) ? __ldg(Ag + (size_t)(i + h) * Mw + 32 * v) : 0u;
+        };
+        uint32_t acur[2][kVwW], anext[2][kVwW];
+        load2(0, acur);
+        load2(2, anext);
+#pragma unroll 1
+        for (int i = 0; i < N; i += 2) {
+            uint32_t afar[2][kVwW];
+            load2(i + 4, afar);
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                if (i + h >= N) break;
+                PrmtTab Tj[T];
+#pragma unroll
+                for (int j = 0; j < T; j++) {
+                    const uint32_t *tp = tabs + (size_t)__ldg(Ub + (size_t)j * N + i + h) * 16u;
+                    const uint4 t0 = __ldg(reinterpret_cast<const uint4 *>(tp));
+                    Tj[j].t0lo = t0.x; Tj[j].t0hi = t0.y; Tj[j].t1lo = t0.z; Tj[j].t1hi = t0.w;
+                    Tj[j].t2 = __ldg(tp + 4);
+                }
+#pragma unroll
+                for (int v = 0; v < kVwW; v++) {
+                    const Sel s = make_sel(acur[h][v]);
+#pragma unroll
+                    for (int j = 0; j < T; j++) y1[j][v] ^= lookup_perm(Tj[j], s);
+                }
+            }
+#pragma unroll
+            for (int h = 0; h < 2; h++)
+#pragma unroll
+                for (int v = 0; v < kVwW; v++) {
+                    acur[h][v] = anext[h][v];
+                    anext[h][v] = afar[h][v];
+                }
+        }
+        // coded rows eight at a time; a row in no projection is not read
+        const int k1 = min(K, 64 * b + 64);
+#pragma unroll 1
+        for (int k0 = 64 * b; k0 < k1; k0 += 8) {
+            uint32_t rb[T];
+#pragma unroll
+            for (int j = 0; j < T; j++) rb[j] = __ldg(RB + (g * 2 + j) * kw + (k0 >> 5)) >> (k0 & 31);   // 8 | 32
+            uint32_t x[8][kVwW];
+#pragma unroll
+            for (int e = 0; e < 8; e++) {
+                uint32_t sel = 0u;
+#pragma unroll
+                for (int j = 0; j < T; j++) sel |= rb[j] >> e;
+                const bool need = (sel & 1u) && k0 + e < k1;
+#pragma unroll
+                for (int v = 0; v < kVwW; v++)
+                    x[e][v] = (need && ok[v]) ? __ldg(Bg + (size_t)(k0 + e) * Mw + 32 * v) : 0u;
+            }
+#pragma unroll
+            for (int e = 0; e < 8; e++)
+#pragma unroll
+                for (int j = 0; j < T; j++) {
+                    const uint32_t m = 0u - ((rb[j] >> e) & 1u);
+#pragma unroll
+                    for (int v = 0; v < kVwW; v++) y2[j][v] ^= x[e][v] & m;
+                }
+        }
+#pragma unroll
+        for (int j = 0; j < T; j++)
+#pragma unroll
+            for (int v = 0; v < kVwW; v++) bad += nz_bytes(unperm(y1[j][v]) ^ y2[j][v]);
+    }
+    const uint32_t nb = __reduce_add_sync(0xffffffffu, bad);
+    if (lane == 0 && nb) atomicAdd(mismatch + g, (unsigned long long)nb);
+}
+
 // mismatch[g] += #{ positions where Y1[g] and Y2[g] differ }, Y: [batch][len]
 __global__ void __launch_bounds__(256) count_mismatch_kernel(const uint8_t *Y1, const uint8_t *Y2, size_t len,
                                                              unsigned long long *mismatch)

@@ -76,10 +76,6 @@ template <int KC, int TW = kPrTW> struct PrCfg {
 constexpr uint32_t kPrBar = 0x0400u;          // mbarriers: BUILT[4], DONE[4] at the dynamic window base
 constexpr uint32_t kPrTab0 = 0x1000u;         // tables u = 0, 1, 2 at kPrTab0 + u * 0x10000
 constexpr uint32_t kPrSmemEnd = kPrTab0 + 3 * 0x10000u;
-// fused Freivalds (T > 0): per step, the split tables of u_ji for the step's 4
-// sources and 2 projections (8 words each), three buffers like the tables
-constexpr uint32_t kPrUbuf = kPrSmemEnd;                    // ring of 4 (step & 3): read lazily after DONE
-constexpr uint32_t kPrSmemEndV = kPrUbuf + 4 * 256u;
 
 struct ProwParams {
     const uint8_t *A;
@@ -94,14 +90,6 @@ struct ProwParams {
     size_t ntiles;     // batch * tiles * k_tiles
     uint32_t qmask4;   // q - 1 in every byte
     int cword;         // coefficient rows can be read as 32-bit words
-    // fused Freivalds check (T > 0 instantiations; gf_encode_verify_batch)
-    const uint32_t *tabs;  // the field's table of tables (16 words per coefficient)
-    const uint8_t *U;      // [batch][k_tiles][2][N]: u_j = sum over the tile's k of r_jk C[i][k]
-    const uint32_t *RB;    // [batch][2][kw]: bit k of word k / 32 = r_jk (binary projections)
-    int kw;
-    int t;                 // projections in use (1 or 2)
-    unsigned long long *mismatch;
-    uint64_t fault;        // harness fault injection: bit 63 on, g << 32 | k << 20 | word
 };
 
 // x * v for packed elements (every w-bit slot of every byte, elements < q)
@@ -193,20 +181,11 @@ struct PrTile {
 
 template <uint32_t V> struct PrU { static constexpr uint32_t value = V; };
 
-// T = 2 (KC = 64 only): the fused Freivalds check of gf_encode_verify_batch
-// per 64-coded-packet tile on binary
-// projection vectors r_j: the producers stage the split tables of u_ji =
-// sum_{k in tile} r_jk C[i][k] for the step's sources; after its gathers, lane
-// (word, chunk kc) multiplies the step's source kc by u_ji (selectors + 3 PRMT
-// per word) into y1_j; at write-back, y2_j ^= b_k & -(r_jk) for the lane's 16
-// coded packets; the four chunk lanes of a word XOR-reduce y1 ^ y2 and count
-// the nonzero bytes into mismatch[g].
 // TW: words per tile (384; 768 with 32 coded packets per CTA for long packets:
 // a table then serves twice the gathers, halving the build share)
-template <int F, int KC, int VT = 0, int TW = kPrTW>
+template <int F, int KC, int TW = kPrTW>
 __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p)
 {
-    static_assert(VT == 0 || (KC == 64 && TW == kPrTW), "fused verification: 64 coded packets per CTA");
     using Cf = PrCfg<KC, TW>;
     constexpr int kPrS = Cf::S, NKC = Cf::NKC;
     // mbarrier rings, object x & 3 for step x: BUILT(x) (4 producer-warp
@@ -356,22 +335,6 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
             const uint4 c = creg;
             creg = load_c();                                    // step x + 1
             build(c, kPrTab0 + (x % 3u) * 0x10000u);
-            if constexpr (VT > 0) {
-                if (pt < 4 * VT) {                               // split tables of u_{j, 4 st + ts}
-                    const int ts = pt >> 1, j = pt & 1;
-                    const uint32_t jt = x / (uint32_t)p.NS, st = x - jt * (uint32_t)p.NS;
-                    const PrTile Tt = tile_of(jt);
-                    const int i = kPrS * (int)st + ts;
-                    uint32_t u = 0;
-                    if (jt < ntj && i < p.N && j < p.t)
-                        u = __ldg(p.U + ((Tt.g * (size_t)p.k_tiles + (size_t)(Tt.k0 / KC)) * 2 + j) * p.N + i);
-                    const uint4 t0 = __ldg(reinterpret_cast<const uint4 *>(p.tabs + (size_t)u * 16u));
-                    const uint32_t t4 = __ldg(p.tabs + (size_t)u * 16u + 4u);
-                    const uint32_t ub = kPrUbuf + (x & 3u) * 256u + (uint32_t)(ts * VT + j) * 32u;
-                    sts128(ub, t0);
-                    sts128(ub + 16u, make_uint4(t4, 0u, 0u, 0u));
-                }
-            }
             __syncwarp();
             if (lane == 0) mbar_arrive(kBuilt + (x & 3u) * 8u);
         }
@@ -432,12 +395,6 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
         for (int j = 0; j < 4; j++) acc[r][j] = make_uint4(0u, 0u, 0u, 0u);
     int st_g = 0;                                              // step-in-tile of the gather step
     uint32_t j_g = 0;
-    uint32_t y1[VT > 0 ? VT : 1][R];                             // A-side projections (permuted byte order)
-#pragma unroll
-    for (int j = 0; j < (VT > 0 ? VT : 1); j++)
-#pragma unroll
-        for (int r = 0; r < R; r++) y1[j][r] = 0u;
-    uint32_t bad = 0;
 
     auto step = [&](uint32_t s, auto U) {
         constexpr uint32_t u = decltype(U)::value;             // table buffer of step s
@@ -468,56 +425,12 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
         // source loads and a tile's write-back
         __syncwarp();
         if (lane == 0) mbar_arrive(kDone + (s & 3u) * 8u);
-        uint32_t av[VT > 0 ? R : 1];                           // this lane's source word of the step (areg[r][kc])
-        (void)av;
-        if constexpr (VT > 0) {
-#pragma unroll
-            for (int r = 0; r < R; r++) {
-                av[r] = areg[r][0];                            // (select chain: no dynamic register index)
-#pragma unroll
-                for (int t = 1; t < kPrS; t++) av[r] = kc == t ? areg[r][t] : av[r];
-            }
-        }
         load_a();                                              // step s + 1
-        if constexpr (VT > 0) {                                // y1_j += u_ji a_i while the loads fly
-            // u tables of this lane's source (jw + kc) & 3 of step s: ring slot
-            // s & 3 is rewritten only for step s + 4, after DONE(s + 1), which
-            // this warp has not arrived at yet
-            PrmtTab Tu[VT];
-#pragma unroll
-            for (int j = 0; j < VT; j++) {
-                const uint32_t ub = kPrUbuf + (s & 3u) * 256u + (uint32_t)((((jw + kc) & 3) * VT + j) * 32);
-                const uint4 a0 = lds128(ub);
-                uint32_t a4;
-                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a4) : "r"(ub + 16u));
-                Tu[j].t0lo = a0.x; Tu[j].t0hi = a0.y; Tu[j].t1lo = a0.z; Tu[j].t1hi = a0.w; Tu[j].t2 = a4;
-            }
-#pragma unroll
-            for (int r = 0; r < R; r++) {                      // selectors once per word, both projections
-                if (!(gmask >> r & 1u)) continue;
-                const Sel sl = make_sel(av[r]);
-#pragma unroll
-                for (int j = 0; j < VT; j++) y1[j][r] ^= lookup_perm(Tu[j], sl);
-            }
-        }
         if (++st_g == p.NS) {
             st_g = 0;
             // ---- write back the tile: acc[r][j] word q holds B[k0 + 16 kc + 4q + e][4 wd + j]
             // (e = byte); a 4x4 byte transpose makes each word one coded packet's 4 bytes
             const PrTile T = tile_of(j_g++);
-            uint32_t rbits[VT > 0 ? VT : 1];                    // r_jk for k = k0 + 16 kc + (0 .. 15)
-            uint32_t y2[VT > 0 ? VT : 1][R];
-            (void)rbits;
-            (void)y2;
-            if constexpr (VT > 0) {
-                const int kb = T.k0 + kc * 16;
-#pragma unroll
-                for (int j = 0; j < VT; j++) {
-                    rbits[j] = (__ldg(p.RB + (T.g * 2 + j) * p.kw + (kb >> 5)) >> (kb & 31)) & 0xFFFFu;
-#pragma unroll
-                    for (int r = 0; r < R; r++) y2[j][r] = 0u;
-                }
-            }
 #pragma unroll
             for (int r = 0; r < R; r++) {
                 const uint32_t wd = T.w0 + wbase + kRW * r;
@@ -533,13 +446,6 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
 #pragma unroll
                         for (int e = 0; e < 4; e++) {
                             const int k = T.k0 + kc * 16 + q * 4 + e;
-                            if constexpr (VT > 0) {
-                                if ((p.fault >> 63) && T.g == ((p.fault >> 32) & 0x7FFFFFFFu) &&
-                                    (uint32_t)k == ((p.fault >> 20) & 0xFFFu) && wd == ((uint32_t)p.fault & 0xFFFFFu))
-                                    y[e] ^= 0x5Au;                  // harness: one wrong byte
-#pragma unroll
-                                for (int j = 0; j < VT; j++) y2[j][r] ^= y[e] & (0u - ((rbits[j] >> (q * 4 + e)) & 1u));
-                            }
                             if (k < p.K)
                                 reinterpret_cast<uint32_t *>(p.B + (T.g * (size_t)p.K + (size_t)k) * p.M)[wd] = y[e];
                         }
@@ -547,24 +453,6 @@ __global__ void __launch_bounds__(kPrThreads, 1) encode_prow_kernel(ProwParams p
                 }
 #pragma unroll
                 for (int j = 0; j < 4; j++) acc[r][j] = make_uint4(0u, 0u, 0u, 0u);
-            }
-            if constexpr (VT > 0) {
-                // the four chunk lanes of a word (lane bits 0-1) hold partial y1 / y2
-#pragma unroll
-                for (int r = 0; r < R; r++) {
-                    const uint32_t wd = T.w0 + wbase + kRW * r;
-#pragma unroll
-                    for (int j = 0; j < VT; j++) {
-                        uint32_t d = unperm(y1[j][r]) ^ y2[j][r];
-                        d ^= __shfl_xor_sync(0xffffffffu, d, 1);
-                        d ^= __shfl_xor_sync(0xffffffffu, d, 2);
-                        if (kc == 0 && wd < p.Mw) bad += nz_bytes(d);
-                        y1[j][r] = 0u;
-                    }
-                }
-                const uint32_t nb = __reduce_add_sync(0xffffffffu, bad);
-                if (lane == 0 && nb) atomicAdd(p.mismatch + T.g, (unsigned long long)nb);
-                bad = 0;
             }
             const PrTile Tn = tile_of(j_g);                     // the next gather tile's words
             gmask = 0;

@@ -251,12 +251,11 @@ static int probe_smem_base(int dev)
     return GF_OK;
 }
 
-template <int F, int KC, int T = 0, int TW = kPrTW>
+template <int F, int KC, int TW = kPrTW>
 static int launch_prow(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M,
-                       size_t batch, cudaStream_t st, const ProwParams *vp = nullptr)
+                       size_t batch, cudaStream_t st)
 {
     ProwParams p{};
-    if (vp) p = *vp;                                           // verification fields (T > 0)
     p.A = A; p.C = C; p.B = B; p.M = M; p.Mw = (uint32_t)(M / 4);
     p.N = N; p.K = K; p.NS = (N + PrCfg<KC, TW>::S - 1) / PrCfg<KC, TW>::S;
     p.tiles = (int)((p.Mw + TW - 1) / TW);
@@ -271,8 +270,8 @@ static int launch_prow(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, in
     // steps per CTA must fit 32 bits
     if ((p.ntiles + grid - 1) / grid * (size_t)p.NS > 0x7FFFFFF0u) return GF_EARG;
     const uint32_t base = g_smem_base[dev];                   // probed by gf_init (checked <= 0x400 there)
-    const size_t smem = (T > 0 ? kPrSmemEndV : kPrSmemEnd) - base;
-    encode_prow_kernel<F, KC, T, TW><<<(unsigned)grid, kPrThreads, smem, st>>>(p);
+    const size_t smem = kPrSmemEnd - base;
+    encode_prow_kernel<F, KC, TW><<<(unsigned)grid, kPrThreads, smem, st>>>(p);
     return launch_status();
 }
 
@@ -305,7 +304,7 @@ static int launch_prow_kc(int path, const uint8_t *A, const uint8_t *C, uint8_t 
                           size_t batch, cudaStream_t st)
 {
     if (path == 10) return launch_prow<F, 16>(A, C, B, N, K, M, batch, st);
-    if (path == 13) return launch_prow<F, 32, 0, 768>(A, C, B, N, K, M, batch, st);
+    if (path == 13) return launch_prow<F, 32, 768>(A, C, B, N, K, M, batch, st);
     if (path == 9) return launch_prow<F, 32>(A, C, B, N, K, M, batch, st);
     return launch_prow<F, 64>(A, C, B, N, K, M, batch, st);
 }
@@ -673,7 +672,7 @@ static int configure_field(int optin, uint32_t smem_base)
     if (rc == GF_OK) rc = allow_smem(encode_prow_kernel<F, 16>, prow);
     if (rc == GF_OK) rc = allow_smem(encode_prow_kernel<F, 32>, prow);
     if (rc == GF_OK) rc = allow_smem(encode_prow_kernel<F, 64>, prow);
-    if (rc == GF_OK) rc = allow_smem(encode_prow_kernel<F, 32, 0, 768>, prow);
+    if (rc == GF_OK) rc = allow_smem(encode_prow_kernel<F, 32, 768>, prow);
     if constexpr (F == 16)
         if (rc == GF_OK) rc = allow_smem(encode_prow16_kernel, (int)(kNbSmemEnd - smem_base));
     if constexpr (F == 2) {
@@ -690,9 +689,6 @@ static int configure_field(int optin, uint32_t smem_base)
         if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<32, true, 1>, optin);
         if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<32, false, 1>, optin);
     }
-    if constexpr (F >= 16)
-        if (rc == GF_OK) rc = allow_smem(encode_prow_kernel<F, 64, 2>, (int)(kPrSmemEndV - smem_base));
-    (void)0;
     if (rc == GF_OK) rc = allow_smem(invert_warp_kernel, optin);
     if (rc == GF_OK) rc = allow_smem(invert_kernel, optin);
     return rc;
@@ -1041,16 +1037,13 @@ int gf_encode_verify_batch(int field, const uint8_t *A, const uint8_t *C, uint8_
                                                                        field - 1);
     if ((rc = launch_status()) != GF_OK) return rc;
     const int path = encode_path(field, N, K, M, A, B);
-    if ((path == 6 || path == 12) && field >= 16) {           // fused: product-row (byte tables), 64 per CTA
-        void *tabs = nullptr;
-        if (symbol_address(0, &tabs) != GF_OK) return GF_ECUDA;
-        ProwParams vp;
-        std::memset(&vp, 0, sizeof(vp));
-        vp.tabs = reinterpret_cast<const uint32_t *>(tabs) + (size_t)fi * 256 * kTableWords;
-        vp.U = U; vp.RB = RB; vp.kw = kw; vp.t = t; vp.mismatch = mismatch; vp.fault = tls_fault;
-        return field == 256 ? launch_prow<256, 64, 2>(A, C, B, N, K, M, batch, st, &vp)
-                            : launch_prow<16, 64, 2>(A, C, B, N, K, M, batch, st, &vp);
-    }
+    // The GF(2) split engine (HBM-bound: a second pass over A and B would double
+    // its traffic) checks inside the encode.  Every other kernel -- the
+    // shared-memory-bound product-row kernels among them, which leave most of
+    // the HBM bandwidth unused -- runs the encode and then one streaming pass
+    // over A and B (verify_words_kernel; C3 GF(256): +21.5% at t = 2 against
+    // +51% for the product-row kernel with the check fused into it, which was
+    // removed).
     if (path == 11 && K <= 64) {                               // fused: GF(2) split engine
         Gf2Params vp;
         std::memset(&vp, 0, sizeof(vp));
@@ -1061,7 +1054,7 @@ int gf_encode_verify_batch(int field, const uint8_t *A, const uint8_t *C, uint8_
         return N <= 16 ? launch_gf2<16, 2>(A, C, B, N, K, M, batch, st, &vp)
                        : launch_gf2<32, 2>(A, C, B, N, K, M, batch, st, &vp);
     }
-    // every other kernel: the encode, then the same check in plain code
+    // every other kernel: the encode, then the same check in a streaming pass
     if ((rc = encode_on_stream(field, fi, A, C, B, N, K, M, batch, st)) != GF_OK) return rc;
     if (tls_fault >> 63) {
         const size_t fg = (tls_fault >> 32) & 0x7FFFFFFFu, fk = (tls_fault >> 20) & 0xFFFu, fw = tls_fault & 0xFFFFFu;
@@ -1069,6 +1062,19 @@ int gf_encode_verify_batch(int field, const uint8_t *A, const uint8_t *C, uint8_
     }
     void *tabs = nullptr;
     if (symbol_address(0, &tabs) != GF_OK) return GF_ECUDA;
+    const uint32_t *ftabs = reinterpret_cast<const uint32_t *>(tabs) + (size_t)fi * 256 * kTableWords;
+    if (M % 4 == 0 && ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 3u) == 0) {
+        const size_t units = batch * ((M / 4 + 32 * kVwW - 1) / (32 * kVwW));   // (generation, 128-word chunk)
+        const size_t blocks = (units + 7) / 8;
+        if (blocks > 0x7FFFFFFFu) return GF_EARG;
+        if (t == 1)
+            verify_words_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(A, B, U, RB, ftabs, N, K, kblocks, kw, M, batch,
+                                                                    mismatch);
+        else
+            verify_words_kernel<2><<<(unsigned)blocks, 256, 0, st>>>(A, B, U, RB, ftabs, N, K, kblocks, kw, M, batch,
+                                                                    mismatch);
+        return launch_status();
+    }
     unsigned gx = (unsigned)((M + 255) / 256);
     if (gx > 64) gx = 64;
     for (size_t g0 = 0; g0 < batch; g0 += 65535) {

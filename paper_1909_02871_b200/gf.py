@@ -298,7 +298,7 @@ def verify_workspace_bytes(N: int, K: int, batch: int) -> int:
 
 def encode_verify_batch(field: int, A: torch.Tensor, C: torch.Tensor, R: torch.Tensor,
                         B: torch.Tensor | None = None, workspace: torch.Tensor | None = None):
-    """B = A C (as encode_batch) with the fused Freivalds check on binary
+    """B = A C (as encode_batch) with the Freivalds check on binary
     projections r_j = R[g, :, j] & 1 (R: uint8 [batch, K, t], t in {1, 2});
     returns (B, mismatch) with mismatch an int64 tensor [batch] of differing
     projection bytes (0 when B == A C; include/gfrlnc.h)."""

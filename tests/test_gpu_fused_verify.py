@@ -1,10 +1,13 @@
-"""gf_encode_verify_batch: the encode with the fused
+"""gf_encode_verify_batch: the encode with the
 Freivalds check -- B bit-exact against the oracle, per-generation mismatch
 counts equal to the oracle's Freivalds projections (oracle.freivalds_gen with
 the same binary r, per block of 64 coded packets), zero on a correct encode, and
-a single corrupted byte (harness fault injection inside the kernel, before the
-store and the projection) caught in exactly its generation; for the fused
-product-row and GF(2) kernels and for the plain fallback."""
+a single corrupted byte (harness fault injection: inside the GF(2) split engine
+before the store and the projection, else in B after the encode) caught in
+exactly its generation; for the check fused into the GF(2) split engine, the
+word-parallel streaming check after every other kernel (product-row, lane-k,
+column, streaming) and the byte-wise check for packets that are not 4-byte
+aligned."""
 import numpy as np
 import pytest
 import torch
@@ -45,7 +48,10 @@ CASES = [  # (q, N, K, M, batch, expected kernel)
     (256, 64, 64, 1500, 5, "prow"), (16, 64, 64, 1500, 4, "prow-nib"), (256, 40, 100, 2000, 3, "prow"),
     (2, 32, 32, 4096, 3, "gf2-split"), (2, 17, 40, 1040, 4, "gf2-split"), (2, 5, 24, 400, 6, "gf2-split"),
     (4, 32, 32, 4096, 2, "lanek-32"), (256, 16, 8, 1500, 3, "column-words"), (16, 16, 1, 1024, 9, "stream"),
-    (2, 32, 80, 512, 2, "gf2-split")]
+    (2, 32, 80, 512, 2, "gf2-split"),
+    # packets not a multiple of 4 bytes: the byte-wise check; long packets
+    # with two coded-packet blocks and a ragged last 128-word chunk
+    (256, 20, 70, 1502, 2, "column-bytes"), (256, 64, 100, 28000, 1, "prow-32w")]
 
 
 @pytest.mark.parametrize("q,N,K,M,batch,kern", CASES)
@@ -75,8 +81,9 @@ def test_fused_verify_matches_oracle(gfm, q, N, K, M, batch, kern, t):
 
 
 def test_fused_verify_full_c3_shape_every_generation(gfm):
-    """The C3 job (65536 generations, GF(256)) through the fused product-row
-    path: B identical to the plain encode, no mismatch anywhere."""
+    """The C3 job (65536 generations, GF(256)) through the product-row encode
+    and the streaming check: B identical to the plain encode, no mismatch
+    anywhere."""
     cfg, q = si.C3, 256
     seed = si.field_seed(cfg, q)
     A = torch.empty((cfg.batch, cfg.N, cfg.M), dtype=torch.uint8, device="cuda")

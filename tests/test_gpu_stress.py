@@ -1,8 +1,9 @@
 """Race evidence without compute-sanitizer (closed on this pool): every kernel
 with an intra-CTA hand-off protocol -- the product-row kernel's producer /
-gatherer mbarrier rings (64 / 32 / 16 coded packets per CTA, plain and fused
-verify), the lane-k kernel's named FULL / EMPTY barriers, the warp-per-matrix
-and CTA-per-matrix inversions -- and the GF(2) split engine are launched many
+gatherer mbarrier rings (64 / 32 / 16 coded packets per CTA, alone and followed
+by the streaming Freivalds check), the lane-k kernel's named FULL / EMPTY
+barriers, the warp-per-matrix and CTA-per-matrix inversions -- and the GF(2)
+split engine (plain and with the fused check) are launched many
 times while a memory-bound kernel runs concurrently on a second stream (so SMs,
 L2 and DRAM are shared with a changing neighbour and warp timing varies from
 launch to launch).  Every output must be bitwise identical to the first and
