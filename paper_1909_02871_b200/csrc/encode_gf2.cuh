@@ -84,8 +84,10 @@ __device__ __forceinline__ void g2_st(uint8_t *p, uint32_t a, uint32_t b, uint32
 // u_j = C r_j from the source words already in registers; then the bytes
 // where y1_j != y2_j are counted into mismatch[g].  B == A C gives zero; a
 // wrong byte escapes one binary projection with probability <= 1/2.
-template <int NS, bool FULL, int T = 0>
-__global__ void __launch_bounds__(kG2Threads) encode_gf2_kernel(Gf2Params p, uint32_t g_base)
+// FT: the harness fault injection (gf_set_verify_fault) -- a separate
+// instantiation, so the production check carries no per-row test code.
+template <int NS, bool FULL, int T = 0, bool FT = false>
+__global__ void __launch_bounds__(kG2Threads, T > 0 ? 3 : 1) encode_gf2_kernel(Gf2Params p, uint32_t g_base)
 {
     extern __shared__ __align__(16) uint32_t cw[];              // [K][NS] (+ T: mr [K][T], mu [T][NS])
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -132,8 +134,8 @@ __global__ void __launch_bounds__(kG2Threads) encode_gf2_kernel(Gf2Params p, uin
         }
         uint32_t *Bg = reinterpret_cast<uint32_t *>(p.B) + g * (size_t)K * Mw + w0;
         // harness fault injection: the coded packet to corrupt if this lane holds the word
-        const int fk = ((p.fault >> 63) && g == ((p.fault >> 32) & 0x7FFFFFFFu) &&
-                        w0 == ((uint32_t)p.fault & 0xFFFFCu)) ? (int)((p.fault >> 20) & 0xFFFu) : -1;
+        const int fk = (FT && g == ((p.fault >> 32) & 0x7FFFFFFFu) && w0 == ((uint32_t)p.fault & 0xFFFFCu))
+                           ? (int)((p.fault >> 20) & 0xFFFu) : -1;
         (void)fk;
         uint32_t y2[T > 0 ? T : 1][4];
 #pragma unroll
@@ -142,6 +144,10 @@ __global__ void __launch_bounds__(kG2Threads) encode_gf2_kernel(Gf2Params p, uin
             for (int w = 0; w < 4; w++) y2[j][w] = 0;
 #pragma unroll 1
         for (int k = 0; k < K; k++) {
+            uint32_t mk[T > 0 ? T : 1];                // projection masks of row k, loaded with its coefficients
+#pragma unroll
+            for (int j = 0; j < T; j++) mk[j] = mr[k * T + j];
+            (void)mk;
             uint32_t c[NS];
 #pragma unroll
             for (int q = 0; q < NS / 4; q++) {
@@ -161,13 +167,12 @@ __global__ void __launch_bounds__(kG2Threads) encode_gf2_kernel(Gf2Params p, uin
                 acc[w] = x;
             }
             if constexpr (T > 0) {
-                if (k == fk) acc[p.fault & 3u] ^= 0x5Au;                // harness: one wrong byte
+                if constexpr (FT)
+                    if (k == fk) acc[p.fault & 3u] ^= 0x5Au;            // harness: one wrong byte
 #pragma unroll
-                for (int j = 0; j < T; j++) {
-                    const uint32_t m = mr[k * T + j];
+                for (int j = 0; j < T; j++)
 #pragma unroll
-                    for (int w = 0; w < 4; w++) y2[j][w] ^= acc[w] & m;
-                }
+                    for (int w = 0; w < 4; w++) y2[j][w] ^= acc[w] & mk[j];
             }
             g2_st(reinterpret_cast<uint8_t *>(Bg + (size_t)k * Mw), acc[0], acc[1], acc[2], acc[3],
                   valid ? 1u : 0u);

@@ -437,8 +437,9 @@ template <int NS, int T = 0>
 static int launch_gf2(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M, size_t batch,
                       cudaStream_t st, const Gf2Params *vp = nullptr)
 {
-    Gf2Params p;
+    Gf2Params p{};
     if (vp) p = *vp;                                           // verification fields (T > 0)
+    const bool ft = T > 0 && (p.fault >> 63);                  // harness fault injection armed
     p.A = A; p.C = C; p.B = B; p.N = N; p.K = K;
     p.Mw = (uint32_t)(M / 4);
     p.spans = (p.Mw + kG2SpanWords - 1) / kG2SpanWords;
@@ -453,7 +454,11 @@ static int launch_gf2(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int
     if (smem > 227 * 1024) return GF_EARG;
     for (size_t g0 = 0; g0 < batch; g0 += 65535) {           // grid.y <= 65535 generations per launch
         const unsigned gy = (unsigned)(batch - g0 < 65535 ? batch - g0 : 65535);
-        if (N == NS)
+        if (ft && N == NS)
+            encode_gf2_kernel<NS, true, T, true><<<dim3(bpg, gy), kG2Threads, smem, st>>>(p, (uint32_t)g0);
+        else if (ft)
+            encode_gf2_kernel<NS, false, T, true><<<dim3(bpg, gy), kG2Threads, smem, st>>>(p, (uint32_t)g0);
+        else if (N == NS)
             encode_gf2_kernel<NS, true, T><<<dim3(bpg, gy), kG2Threads, smem, st>>>(p, (uint32_t)g0);
         else
             encode_gf2_kernel<NS, false, T><<<dim3(bpg, gy), kG2Threads, smem, st>>>(p, (uint32_t)g0);
@@ -688,6 +693,14 @@ static int configure_field(int optin, uint32_t smem_base)
         if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<16, false, 1>, optin);
         if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<32, true, 1>, optin);
         if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<32, false, 1>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<16, true, 1, true>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<16, false, 1, true>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<32, true, 1, true>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<32, false, 1, true>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<16, true, 2, true>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<16, false, 2, true>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<32, true, 2, true>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<32, false, 2, true>, optin);
     }
     if (rc == GF_OK) rc = allow_smem(invert_warp_kernel, optin);
     if (rc == GF_OK) rc = allow_smem(invert_kernel, optin);
