@@ -150,7 +150,8 @@ int gf_verify_batch(int field, const uint8_t *A, const uint8_t *C, const uint8_t
  * same call, on the same stream.  dev_ws: 16-byte
  * aligned device workspace of at least
  *     round16(batch * ceil(K/64) * 2 * N) + batch * 2 * ceil(K/32) * 4 bytes.
- * Returns the codes of gf_encode_batch, or GF_EARG (t, R, mismatch, workspace). */
+ * Returns the codes of gf_encode_batch, or GF_EARG (t, R, mismatch, workspace,
+ * batch > 2^31 - 1 or K > 196608). */
 int gf_encode_verify_batch(int field, const uint8_t *A, const uint8_t *C, uint8_t *B, const uint8_t *R, int t,
                            int N, int K, size_t M, size_t batch, unsigned long long *mismatch, void *dev_ws,
                            size_t ws_bytes);

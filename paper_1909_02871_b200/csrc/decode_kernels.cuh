@@ -262,37 +262,54 @@ __global__ void __launch_bounds__(256) project_coeffs_kernel(const uint8_t *C, c
 // per block of 64 coded packets.  U[g][b][j][i] = sum_{k in block b, r_jk = 1}
 // C[g][i][k] (an element of F_q, the A-side coefficient of projection j), and
 // RB[g][j][w] = the bits r_jk, k = 32 w .. 32 w + 31.  R: [batch][K][t] bytes,
-// r_jk = R[g][k][j] & 1.  One thread per (g, b, j, i), then per (g, j, w).
-__global__ void __launch_bounds__(256) verify_prep_kernel(const uint8_t *C, const uint8_t *R, uint8_t *U,
+// r_jk = R[g][k][j] & 1.  One CTA per generation: the bits into shared memory
+// (and RB), then one thread per (b, i) reduces the block's coefficient bytes of
+// row i four at a time under the byte mask of their four r bits.
+__global__ void __launch_bounds__(128) verify_prep_kernel(const uint8_t *C, const uint8_t *R, uint8_t *U,
                                                           uint32_t *RB, int N, int K, int t, int kblocks, int kw,
                                                           size_t batch, int qmask)
 {
-    const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const size_t nu = batch * (size_t)kblocks * 2 * N;
-    if (e < nu) {
-        const size_t g = e / ((size_t)kblocks * 2 * N);
-        const int rest = (int)(e % ((size_t)kblocks * 2 * N));
-        const int b = rest / (2 * N), j = (rest / N) & 1, i = rest % N;
-        uint32_t acc = 0;
-        if (j < t) {
-            const uint8_t *Cr = C + (g * N + i) * (size_t)K;
-            const uint8_t *Rg = R + g * (size_t)K * t;
-            const int k1 = min(K, 64 * b + 64);
-            for (int k = 64 * b; k < k1; k++)
-                if (Rg[(size_t)k * t + j] & 1u) acc ^= Cr[k] & (uint32_t)qmask;
-        }
-        U[e] = (uint8_t)acc;
-        return;
+    extern __shared__ uint32_t srb[];                          // [2][kw]
+    const size_t g = blockIdx.x;
+    if (g >= batch) return;
+    for (int f = threadIdx.x; f < 2 * kw; f += blockDim.x) {
+        const int j = f / kw, w = f - j * kw;
+        uint32_t bits = 0;
+        if (j < t)
+            for (int k = 32 * w; k < min(K, 32 * w + 32); k++)
+                bits |= (uint32_t)(__ldg(R + (g * K + k) * (size_t)t + j) & 1u) << (k - 32 * w);
+        srb[f] = bits;
+        RB[g * 2 * (size_t)kw + f] = bits;
     }
-    const size_t f = e - nu;
-    if (f >= batch * 2 * (size_t)kw) return;
-    const size_t g = f / (2 * (size_t)kw);
-    const int j = (int)((f / kw) & 1), w = (int)(f % kw);
-    uint32_t bits = 0;
-    if (j < t)
-        for (int k = 32 * w; k < min(K, 32 * w + 32); k++)
-            bits |= (uint32_t)(R[(g * K + k) * (size_t)t + j] & 1u) << (k - 32 * w);
-    RB[f] = bits;
+    __syncthreads();
+    const bool cwd = K % 4 == 0 && (reinterpret_cast<uintptr_t>(C) & 3u) == 0;
+    for (int e = threadIdx.x; e < kblocks * N; e += blockDim.x) {
+        const int b = e / N, i = e - b * N;
+        const uint8_t *Cr = C + (g * N + i) * (size_t)K;
+        const int k0 = 64 * b, k1 = min(K, k0 + 64);
+        uint32_t acc[2] = {0u, 0u};
+        for (int k = k0; k < k1; k += 4) {
+            uint32_t word = 0;
+            if (cwd && k + 4 <= k1) {
+                word = __ldg(reinterpret_cast<const uint32_t *>(Cr + k));
+            } else {
+                for (int d = 0; d < 4 && k + d < k1; d++) word |= (uint32_t)__ldg(Cr + k + d) << (8 * d);
+            }
+#pragma unroll
+            for (int j = 0; j < 2; j++) {
+                const uint32_t nib = (srb[j * kw + (k >> 5)] >> (k & 31)) & 0xFu;   // k % 4 == 0
+                // bit d of nib -> 0xFF in byte d (nib * 0x00204081 puts bit d at bit 8 d, no carries)
+                acc[j] ^= word & (((nib * 0x00204081u) & 0x01010101u) * 0xFFu);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 2; j++) {
+            uint32_t a = acc[j];
+            a ^= a >> 16;
+            a ^= a >> 8;
+            U[((g * kblocks + b) * 2 + j) * (size_t)N + i] = (uint8_t)(j < t ? (a & (uint32_t)qmask) : 0u);
+        }
+    }
 }
 
 // The same check for the encode kernels without a fused form (plain code,
@@ -338,14 +355,16 @@ __global__ void __launch_bounds__(256) verify_plain_kernel(const uint8_t *A, con
 // counted per generation (same count as verify_plain_kernel).
 constexpr int kVwW = 4;                                       // words per lane
 template <int T>
-__global__ void __launch_bounds__(256) verify_words_kernel(const uint8_t *A, const uint8_t *B, const uint8_t *U,
+__global__ void __launch_bounds__(32) verify_words_kernel(const uint8_t *A, const uint8_t *B, const uint8_t *U,
                                                            const uint32_t *RB, const uint32_t *__restrict__ tabs,
                                                            int N, int K, int kblocks, int kw, size_t M, size_t batch,
                                                            unsigned long long *mismatch)
 {
     const size_t Mw = M / 4;
     const size_t chunks = (Mw + 32 * kVwW - 1) / (32 * kVwW);
-    const size_t unit = (size_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    // one warp per CTA: the unit index, the generation, the row addresses and
+    // the r_jk masks are then CTA-uniform (uniform registers, not per-lane work)
+    const size_t unit = blockIdx.x;
     if (unit >= batch * chunks) return;
     const int lane = threadIdx.x & 31;
     const size_t g = unit / chunks;

@@ -1045,16 +1045,16 @@ int gf_encode_verify_batch(int field, const uint8_t *A, const uint8_t *C, uint8_
         return GF_EOVERLAP;
     const cudaStream_t st = tls_stream;
     if (cudaMemsetAsync(mismatch, 0, batch * sizeof(unsigned long long), st) != cudaSuccess) return GF_ECUDA;
-    const size_t nprep = batch * (size_t)kblocks * 2 * N + batch * 2 * (size_t)kw;
-    verify_prep_kernel<<<(unsigned)((nprep + 255) / 256), 256, 0, st>>>(C, R, U, RB, N, K, t, kblocks, kw, batch,
-                                                                       field - 1);
+    if (batch > 0x7FFFFFFFu || 8 * (size_t)kw > 48 * 1024) return GF_EARG;
+    verify_prep_kernel<<<(unsigned)batch, 128, 8 * (size_t)kw, st>>>(C, R, U, RB, N, K, t, kblocks, kw, batch,
+                                                                      field - 1);
     if ((rc = launch_status()) != GF_OK) return rc;
     const int path = encode_path(field, N, K, M, A, B);
     // The GF(2) split engine (HBM-bound: a second pass over A and B would double
     // its traffic) checks inside the encode.  Every other kernel -- the
     // shared-memory-bound product-row kernels among them, which leave most of
     // the HBM bandwidth unused -- runs the encode and then one streaming pass
-    // over A and B (verify_words_kernel; C3 GF(256): +21.5% at t = 2 against
+    // over A and B (verify_words_kernel; C3 GF(256): +17.9% at t = 2 against
     // +51% for the product-row kernel with the check fused into it, which was
     // removed).
     if (path == 11 && K <= 64) {                               // fused: GF(2) split engine
@@ -1078,14 +1078,13 @@ int gf_encode_verify_batch(int field, const uint8_t *A, const uint8_t *C, uint8_
     const uint32_t *ftabs = reinterpret_cast<const uint32_t *>(tabs) + (size_t)fi * 256 * kTableWords;
     if (M % 4 == 0 && ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 3u) == 0) {
         const size_t units = batch * ((M / 4 + 32 * kVwW - 1) / (32 * kVwW));   // (generation, 128-word chunk)
-        const size_t blocks = (units + 7) / 8;
-        if (blocks > 0x7FFFFFFFu) return GF_EARG;
+        if (units > 0x7FFFFFFFu) return GF_EARG;
         if (t == 1)
-            verify_words_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(A, B, U, RB, ftabs, N, K, kblocks, kw, M, batch,
-                                                                    mismatch);
+            verify_words_kernel<1><<<(unsigned)units, 32, 0, st>>>(A, B, U, RB, ftabs, N, K, kblocks, kw, M, batch,
+                                                                  mismatch);
         else
-            verify_words_kernel<2><<<(unsigned)blocks, 256, 0, st>>>(A, B, U, RB, ftabs, N, K, kblocks, kw, M, batch,
-                                                                    mismatch);
+            verify_words_kernel<2><<<(unsigned)units, 32, 0, st>>>(A, B, U, RB, ftabs, N, K, kblocks, kw, M, batch,
+                                                                  mismatch);
         return launch_status();
     }
     unsigned gx = (unsigned)((M + 255) / 256);
