@@ -133,40 +133,6 @@ __device__ __forceinline__ void xor4(uint4 &a, const uint4 &b)
 {
     a.x ^= b.x; a.y ^= b.y; a.z ^= b.z; a.w ^= b.w;
 }
-__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count)
-{
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(a), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t a)
-{
-    asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" :: "r"(a) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_n(uint32_t a, uint32_t n)
-{
-    asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0], %1; }" :: "r"(a), "r"(n) : "memory");
-}
-__device__ __forceinline__ bool mbar_test(uint32_t a, uint32_t parity)
-{
-    uint32_t ok;
-    asm volatile("{ .reg .pred p;\n"
-                 "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-                 "selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(a), "r"(parity) : "memory");
-    return ok != 0;
-}
-// a waiter that is known to run ahead (the producers): poll rarely, every
-// failed poll is a shared-memory access on the pipe the gatherers are bound by
-__device__ __forceinline__ void mbar_wait_sleepy(uint32_t a, uint32_t parity)
-{
-    while (!mbar_test(a, parity)) __nanosleep(256);
-}
-__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity)
-{
-    asm volatile("{ .reg .pred p;\n"
-                 "PR_WAIT_%=:\n"
-                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
-                 "@!p bra PR_WAIT_%=;\n}" :: "r"(a), "r"(parity) : "memory");
-}
-
 __device__ __forceinline__ void nbar_sync_n(int id, int n)
 {
     asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(n) : "memory");
