@@ -80,6 +80,13 @@ struct LanekParams {
     int qmask;
     int tiles;         // word tiles per packet
     int k_tiles;       // ceil(K / (32 KG))
+    // fused Freivalds check (VT > 0 instantiations, KG <= 2: a CTA's coded
+    // packets are exactly one block of 64, or all K <= 32; gf_encode_verify_batch)
+    const uint8_t *U;      // [batch][kblocks][2][N]: u_jbi = sum_{k in block b} r_jk C[i][k]
+    const uint32_t *RB;    // [batch][2][kw]: bit k of word k / 32 = r_jk
+    int kw;
+    unsigned long long *mismatch;
+    uint64_t fault;        // harness fault injection (FT): g << 32 | k << 20 | word
 };
 
 template <int F> struct LkField;
@@ -151,10 +158,39 @@ __device__ __forceinline__ void build_word(uint32_t *q, const uint32_t (&a)[LkFi
     }
 }
 
-template <int F, int KG>
+// u * a for packed elements of F (u < q): the xtime chain of a, masked by the
+// bits of u (the A-side projection of the fused check)
+template <int F>
+__device__ __forceinline__ uint32_t lk_mul(uint32_t a, uint32_t u)
+{
+    if constexpr (F == 2) {
+        return a & (0u - (u & 1u));
+    } else if constexpr (F == 4) {
+        return (a & (0u - (u & 1u))) ^ (gf4_xtime(a) & (0u - ((u >> 1) & 1u)));
+    } else {
+        constexpr int w = F == 16 ? 4 : 8;
+        uint32_t y = 0, x = a;
+#pragma unroll
+        for (int b = 0; b < w; b++) {
+            y ^= x & (0u - ((u >> b) & 1u));
+            if (b + 1 < w) x = LkField<F>::xtime(x);
+        }
+        return y;
+    }
+}
+
+// VT > 0 (KG <= 2): the fused Freivalds check of gf_encode_verify_batch over
+// the CTA's block of coded packets: the builders accumulate y1_j = sum_i u_ji
+// a_i for their words from the source words they hold (lk_mul), the
+// epilogue accumulates y2_j = sum_k r_jk b_k while it streams the transposed
+// tile out of shared memory (one masked XOR per word and projection, shared-
+// memory XOR-atomics across warps), and the bytes where y1 != y2 are counted
+// into mismatch[g].  FT: the harness fault injection, its own instantiation.
+template <int F, int KG, int VT = 0, bool FT = false>
 __global__ void __launch_bounds__(LkGeom<KG, F == 2 && KG == 1>::THREADS, LkGeom<KG, F == 2 && KG == 1>::MINB)
 encode_lanek_kernel(LanekParams p)
 {
+    static_assert(VT == 0 || KG <= 2, "fused check: one block of coded packets per CTA");
     using L = LkField<F>;
     using G = LkGeom<KG, F == 2 && KG == 1>;
     constexpr int SG = L::kSG;
@@ -177,9 +213,18 @@ encode_lanek_kernel(LanekParams p)
     const uint32_t w0 = (uint32_t)tile * TW;                   // first word of the tile
     const uint8_t *Ag = p.A + g * (size_t)p.N * p.M;
     const int NS = (p.N + SG - 1) / SG;                        // steps
+    // fused check: y1 [VT][TW] (builders), y2 [VT][TW] (XOR-atomics), after the coefficient cache
+    uint32_t *y1s = reinterpret_cast<uint32_t *>(ccache + (((size_t)KTL * NS + 15) & ~(size_t)15));
+    uint32_t *y2s = y1s + VT * TW;
+    (void)y2s;
+    const int kblk = (p.K + 63) / 64, bk = k0 / 64;            // the CTA's block of 64 coded packets
+    (void)kblk;
+    (void)bk;
 
     // zero rows (index 0, and 16 for GF(256)) of every buffer; row indices of
     // every (step, k) from the coefficients (rows past N count as c = 0)
+    if constexpr (VT > 0)
+        for (int t = threadIdx.x; t < VT * TW; t += blockDim.x) y2s[t] = 0u;
     for (int t = threadIdx.x; t < QS; t += blockDim.x) {
 #pragma unroll
         for (int b = 0; b < kLkNQ; b++) {
@@ -202,6 +247,7 @@ encode_lanek_kernel(LanekParams p)
     __syncthreads();
 
     constexpr int BAR_FULL = 1, BAR_EMPTY = 1 + kLkNQ, BAR_EPI = 1 + 2 * kLkNQ;   // named barrier ids
+    constexpr int BAR_Y1 = 2 + 2 * kLkNQ;                      // fused check: builders' y1 written
 
     if (warp >= GW) {
         // ---------------- builders: source words straight into registers three
@@ -209,6 +255,13 @@ encode_lanek_kernel(LanekParams p)
         const int bt = threadIdx.x - 32 * GW;                  // 0 .. 127
         constexpr int D = kLkNQ;                               // prefetch distance (= NQ: one unrolled round)
         uint32_t ar[D][G::BWORDS][SG];
+        uint32_t y1[VT > 0 ? VT : 1][G::BWORDS];
+#pragma unroll
+        for (int j = 0; j < (VT > 0 ? VT : 1); j++)
+#pragma unroll
+            for (int u = 0; u < G::BWORDS; u++) y1[j][u] = 0u;
+        const uint8_t *Ub = p.U + ((g * (size_t)kblk + (size_t)bk) * 2) * (size_t)p.N;
+        (void)Ub;
         auto load = [&](int s, uint32_t (&a)[G::BWORDS][SG]) {
 #pragma unroll
             for (int j = 0; j < SG; j++) {
@@ -232,6 +285,19 @@ encode_lanek_kernel(LanekParams p)
                 if (tw < TW) build_word<F, QS>(q + tw, a[u]);
             }
             nbar_arrive(BAR_FULL + b, NT);
+            if constexpr (VT > 0) {                            // y1_j += u_ji a_i (before the loads reuse a)
+#pragma unroll
+                for (int jj = 0; jj < SG; jj++) {
+                    const int i = s * SG + jj;
+                    if (i >= p.N) break;
+#pragma unroll
+                    for (int j = 0; j < VT; j++) {
+                        const uint32_t u = __ldg(Ub + (size_t)j * p.N + i);
+#pragma unroll
+                        for (int v = 0; v < G::BWORDS; v++) y1[j][v] ^= lk_mul<F>(a[v][jj], u);
+                    }
+                }
+            }
             load(s + D, a);
         };
 #pragma unroll
@@ -243,6 +309,16 @@ encode_lanek_kernel(LanekParams p)
             bstep(s + 2, 2, ar[2]);
         }
         static_assert(D == 3, "builder loop unrolled for three Q buffers");
+        if constexpr (VT > 0) {
+#pragma unroll
+            for (int v = 0; v < G::BWORDS; v++) {
+                const int tw = bt + 128 * v;
+                if (tw < TW)
+#pragma unroll
+                    for (int j = 0; j < VT; j++) y1s[j * TW + tw] = y1[j][v];
+            }
+            nbar_arrive(BAR_Y1, NT);
+        }
         // consume the gatherers' last NQ EMPTY signals
         for (int s = max(NS, kLkNQ); s < NS + kLkNQ; s++) nbar_sync(BAR_EMPTY + s % kLkNQ, NT);
         return;
@@ -288,6 +364,14 @@ encode_lanek_kernel(LanekParams p)
         nbar_arrive(BAR_EMPTY + b, NT);
     }
 
+    if constexpr (FT) {                                        // harness: one wrong byte
+        if (g == ((p.fault >> 32) & 0x7FFFFFFFu) && k0 + kl == (int)((p.fault >> 20) & 0xFFFu)) {
+            const uint32_t fw = (uint32_t)p.fault & 0xFFFFFu;
+#pragma unroll
+            for (int w = 0; w < WT; w++)
+                if (w0 + (uint32_t)(wg * WT + w) == fw) acc[w] ^= 0x5Au;
+        }
+    }
     // ---- epilogue: transpose through shared memory so that each warp writes
     // contiguous runs of one coded packet (the Q buffers are free once every
     // gatherer passed its last step: named barrier over the gatherers only)
@@ -299,6 +383,12 @@ encode_lanek_kernel(LanekParams p)
     constexpr int kPasses = KTL / kRowsPerPass;
     static_assert(kRowsPerPass * kPasses == KTL && kRowsPerPass % 32 == 0, "epilogue passes");
     uint32_t *ot = Q;                                           // [rows per pass][OS]
+    uint32_t y2p[VT > 0 ? VT : 1][TW / 32];                     // fused check: this thread's words' partial y2
+#pragma unroll
+    for (int j = 0; j < (VT > 0 ? VT : 1); j++)
+#pragma unroll
+        for (int n = 0; n < TW / 32; n++) y2p[j][n] = 0u;
+    (void)y2p;
     const uint32_t nw = min((uint32_t)TW, p.Mw - w0);
 #pragma unroll 1
     for (int h = 0; h < kPasses; h++) {
@@ -319,17 +409,51 @@ encode_lanek_kernel(LanekParams p)
         for (int r = warp; r < kRowsPerPass; r += GW) {
             if (kbase + r >= p.K) break;
             uint32_t *row = reinterpret_cast<uint32_t *>(p.B + (g * (size_t)p.K + (size_t)(kbase + r)) * p.M) + w0;
-            for (uint32_t w = lane; w < nw; w += 32) row[w] = ot[r * OS + w];
+            if constexpr (VT > 0) {
+                const int k = kbase + r;
+                uint32_t m[VT];
+#pragma unroll
+                for (int j = 0; j < VT; j++) m[j] = 0u - ((__ldg(p.RB + (g * 2 + j) * (size_t)p.kw + (k >> 5)) >> (k & 31)) & 1u);
+#pragma unroll
+                for (int n = 0; n < TW / 32; n++) {
+                    const uint32_t w = (uint32_t)(lane + 32 * n);
+                    if (w < nw) {
+                        const uint32_t x = ot[r * OS + w];
+                        row[w] = x;
+#pragma unroll
+                        for (int j = 0; j < VT; j++) y2p[j][n] ^= x & m[j];
+                    }
+                }
+            } else {
+                for (uint32_t w = lane; w < nw; w += 32) row[w] = ot[r * OS + w];
+            }
         }
+    }
+    if constexpr (VT > 0) {
+        // combine the warps' partial y2 (shared-memory XOR-atomics), wait for the
+        // builders' y1, count the differing bytes
+#pragma unroll
+        for (int n = 0; n < TW / 32; n++)
+#pragma unroll
+            for (int j = 0; j < VT; j++)
+                if (y2p[j][n]) atomicXor(y2s + j * TW + lane + 32 * n, y2p[j][n]);
+        nbar_sync(BAR_Y1, NT);
+        uint32_t bad = 0;
+        for (int w = threadIdx.x; w < (int)nw; w += 32 * GW)
+#pragma unroll
+            for (int j = 0; j < VT; j++) bad += nz_bytes(y1s[j * TW + w] ^ y2s[j * TW + w]);
+        bad = __reduce_add_sync(0xffffffffu, bad);
+        if (lane == 0 && bad) atomicAdd(p.mismatch + g, (unsigned long long)bad);
     }
 }
 
-template <int F, int KG>
+template <int F, int KG, int VT = 0>
 __host__ __device__ constexpr size_t lk_smem_bytes(int N)
 {
     using G = LkGeom<KG, F == 2 && KG == 1>;
     return (size_t)kLkNQ * LkField<F>::kRows * G::QS * 4 +
-           (size_t)32 * KG * ((N + LkField<F>::kSG - 1) / LkField<F>::kSG);
+           (((size_t)32 * KG * ((N + LkField<F>::kSG - 1) / LkField<F>::kSG) + 15) & ~(size_t)15) +
+           (size_t)2 * VT * G::TW * 4;
 }
 
 }  // namespace gfr

@@ -211,21 +211,25 @@ static int launch_encode_field(int field, EncodeParams p, cudaStream_t st)
     }
 }
 
-template <int F, int KG>
+template <int F, int KG, int VT = 0>
 static int launch_lanek(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M,
-                        size_t batch, cudaStream_t st)
+                        size_t batch, cudaStream_t st, const LanekParams *vp = nullptr)
 {
     using G = LkGeom<KG, F == 2 && KG == 1>;
     LanekParams p{};
+    if (vp) p = *vp;                                           // verification fields (VT > 0)
     p.A = A; p.C = C; p.B = B; p.M = M; p.Mw = (uint32_t)(M / 4); p.batch = batch;
     p.N = N; p.K = K; p.qmask = F - 1;
     p.tiles = (int)((p.Mw + G::TW - 1) / G::TW);
     p.k_tiles = (K + 32 * KG - 1) / (32 * KG);
     const size_t grid = batch * (size_t)p.tiles * (size_t)p.k_tiles;
     if (grid > 0x7FFFFFFFu) return GF_EARG;
-    const size_t smem = lk_smem_bytes<F, KG>(N);
+    const size_t smem = lk_smem_bytes<F, KG, VT>(N);
     if (smem > 227 * 1024) return GF_EARG;
-    encode_lanek_kernel<F, KG><<<(unsigned)grid, G::THREADS, smem, st>>>(p);
+    if (VT > 0 && (p.fault >> 63))                             // harness fault injection armed
+        encode_lanek_kernel<F, KG, VT, true><<<(unsigned)grid, G::THREADS, smem, st>>>(p);
+    else
+        encode_lanek_kernel<F, KG, VT><<<(unsigned)grid, G::THREADS, smem, st>>>(p);
     return launch_status();
 }
 
@@ -673,6 +677,14 @@ static int configure_field(int optin, uint32_t smem_base)
     if (rc == GF_OK) rc = allow_smem(encode_lanek_kernel<F, 1>, optin);
     if (rc == GF_OK) rc = allow_smem(encode_lanek_kernel<F, 2>, optin);
     if (rc == GF_OK) rc = allow_smem(encode_lanek_kernel<F, 4>, optin);
+    if (rc == GF_OK) rc = allow_smem(encode_lanek_kernel<F, 1, 1>, optin);
+    if (rc == GF_OK) rc = allow_smem(encode_lanek_kernel<F, 1, 2>, optin);
+    if (rc == GF_OK) rc = allow_smem(encode_lanek_kernel<F, 2, 1>, optin);
+    if (rc == GF_OK) rc = allow_smem(encode_lanek_kernel<F, 2, 2>, optin);
+    if (rc == GF_OK) rc = allow_smem(encode_lanek_kernel<F, 1, 1, true>, optin);
+    if (rc == GF_OK) rc = allow_smem(encode_lanek_kernel<F, 1, 2, true>, optin);
+    if (rc == GF_OK) rc = allow_smem(encode_lanek_kernel<F, 2, 1, true>, optin);
+    if (rc == GF_OK) rc = allow_smem(encode_lanek_kernel<F, 2, 2, true>, optin);
     const int prow = (int)(kPrSmemEnd - smem_base);
     if (rc == GF_OK) rc = allow_smem(encode_prow_kernel<F, 16>, prow);
     if (rc == GF_OK) rc = allow_smem(encode_prow_kernel<F, 32>, prow);
@@ -1066,6 +1078,29 @@ int gf_encode_verify_batch(int field, const uint8_t *A, const uint8_t *C, uint8_
                            : launch_gf2<32, 1>(A, C, B, N, K, M, batch, st, &vp);
         return N <= 16 ? launch_gf2<16, 2>(A, C, B, N, K, M, batch, st, &vp)
                        : launch_gf2<32, 2>(A, C, B, N, K, M, batch, st, &vp);
+    }
+    if ((path == 2 || path == 3) && K <= 64) {                 // fused: lane-k, one block per CTA
+        LanekParams vp{};
+        vp.U = U; vp.RB = RB; vp.kw = kw; vp.mismatch = mismatch; vp.fault = tls_fault;
+        const bool kg2 = K > 32;
+        switch (field) {
+        case 256: return kg2 ? (t == 1 ? launch_lanek<256, 2, 1>(A, C, B, N, K, M, batch, st, &vp)
+                                       : launch_lanek<256, 2, 2>(A, C, B, N, K, M, batch, st, &vp))
+                             : (t == 1 ? launch_lanek<256, 1, 1>(A, C, B, N, K, M, batch, st, &vp)
+                                       : launch_lanek<256, 1, 2>(A, C, B, N, K, M, batch, st, &vp));
+        case 16: return kg2 ? (t == 1 ? launch_lanek<16, 2, 1>(A, C, B, N, K, M, batch, st, &vp)
+                                      : launch_lanek<16, 2, 2>(A, C, B, N, K, M, batch, st, &vp))
+                            : (t == 1 ? launch_lanek<16, 1, 1>(A, C, B, N, K, M, batch, st, &vp)
+                                      : launch_lanek<16, 1, 2>(A, C, B, N, K, M, batch, st, &vp));
+        case 4: return kg2 ? (t == 1 ? launch_lanek<4, 2, 1>(A, C, B, N, K, M, batch, st, &vp)
+                                     : launch_lanek<4, 2, 2>(A, C, B, N, K, M, batch, st, &vp))
+                           : (t == 1 ? launch_lanek<4, 1, 1>(A, C, B, N, K, M, batch, st, &vp)
+                                     : launch_lanek<4, 1, 2>(A, C, B, N, K, M, batch, st, &vp));
+        default: return kg2 ? (t == 1 ? launch_lanek<2, 2, 1>(A, C, B, N, K, M, batch, st, &vp)
+                                      : launch_lanek<2, 2, 2>(A, C, B, N, K, M, batch, st, &vp))
+                            : (t == 1 ? launch_lanek<2, 1, 1>(A, C, B, N, K, M, batch, st, &vp)
+                                      : launch_lanek<2, 1, 2>(A, C, B, N, K, M, batch, st, &vp));
+        }
     }
     // every other kernel: the encode, then the same check in a streaming pass
     if ((rc = encode_on_stream(field, fi, A, C, B, N, K, M, batch, st)) != GF_OK) return rc;

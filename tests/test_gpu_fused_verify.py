@@ -51,7 +51,11 @@ CASES = [  # (q, N, K, M, batch, expected kernel)
     (2, 32, 80, 512, 2, "gf2-split"),
     # packets not a multiple of 4 bytes: the byte-wise check; long packets
     # with two coded-packet blocks and a ragged last 128-word chunk
-    (256, 20, 70, 1502, 2, "column-bytes"), (256, 64, 100, 28000, 1, "prow-32w")]
+    (256, 20, 70, 1502, 2, "column-bytes"), (256, 64, 100, 28000, 1, "prow-32w"),
+    # lane-k with the check fused: 32 and 64 coded packets per CTA (GF(2) with
+    # N > 32, where the split engine does not apply); 128 per CTA (K > 64) runs
+    # the streaming check
+    (4, 64, 64, 4096, 2, "lanek-64"), (2, 40, 48, 2048, 3, "lanek-64"), (4, 24, 70, 1024, 2, "lanek-64")]
 
 
 @pytest.mark.parametrize("q,N,K,M,batch,kern", CASES)
@@ -78,6 +82,33 @@ def test_fused_verify_matches_oracle(gfm, q, N, K, M, batch, kern, t):
     rsel = R[batch // 2, K - 1, :t] & 1
     assert (got[batch // 2] > 0) == bool(rsel.any())       # caught iff some r_j selects coded packet K-1
     assert got.sum() == got[batch // 2]
+
+
+@pytest.mark.parametrize("q", (16, 256))
+def test_fused_verify_forced_lanek(gfm, q):
+    """The lane-k kernel's fused check for GF(16) / GF(256) (forced: the router
+    sends these fields to the product-row kernels), 32 and 64 coded packets per
+    CTA, with and without an injected fault."""
+    gfm.set_encode_path("lanek")
+    try:
+        for N, K, M, batch in ((20, 30, 1540, 3), (20, 40, 1540, 3)):
+            assert gfm.encode_path(q, N, K, M).startswith("lanek")
+            A = si.random_bytes(600 + N, si.STREAM_A, 0, batch * N * M).reshape(batch, N, M)
+            C = si.uniform_coeffs(q, 601 + K, si.STREAM_C, 0, batch * N * K).reshape(batch, N, K)
+            R = si.random_bytes(602, si.STREAM_FREIVALDS, 0, batch * K * 2).reshape(batch, K, 2)
+            B, mism = gfm.encode_verify_batch(q, *(torch.from_numpy(x).cuda() for x in (A, C, R)))
+            Bh = B.cpu().numpy()
+            assert np.array_equal(Bh, oracle.encode_batch(q, A, C)) and int(mism.sum()) == 0
+            gfm.set_verify_fault(1, K - 2, 100)
+            try:
+                B2, mism2 = gfm.encode_verify_batch(q, *(torch.from_numpy(x).cuda() for x in (A, C, R)))
+            finally:
+                gfm.set_verify_fault(-1)
+            B2h = B2.cpu().numpy()
+            assert int((B2h != Bh).sum()) == 1
+            assert np.array_equal(mism2.cpu().numpy(), oracle_counts(q, A, C, B2h, R))
+    finally:
+        gfm.set_encode_path("auto")
 
 
 def test_fused_verify_full_c3_shape_every_generation(gfm):

@@ -1,6 +1,7 @@
 """Cost of the Freivalds check (gf_encode_verify_batch, t = 2 and t = 1) against
-the plain encode on the bench shapes: C3 GF(256) / GF(16) (65536 generations)
-and a C5 GF(2) launch (256 generations)."""
+the plain encode on the bench shapes: C3 GF(256) / GF(16) (65536 generations),
+a C5 GF(2) and GF(4) launch (256 generations) and a C4 launch (16 generations).
+    python tools/time_verify.py [C3 | C4 | C5 | C5-4 ...]"""
 import os
 import sys
 
@@ -24,7 +25,10 @@ def timeit(fn, reps=10):
 
 
 def main():
-    for cfg, q, G in ((si.C3, 256, 65536), (si.C3, 16, 65536), (si.C5, 2, 256)):
+    only = sys.argv[1:]                                        # optional config names, e.g. C4 C5-4
+    for cfg, q, G in ((si.C3, 256, 65536), (si.C3, 16, 65536), (si.C5, 2, 256), (si.C5, 4, 256), (si.C4, 256, 16)):
+        if only and f"{cfg.name}-{q}" not in only and cfg.name not in only:
+            continue
         gf.init(q)
         A = torch.empty((G, cfg.N, cfg.M), dtype=torch.uint8, device="cuda")
         C = torch.empty((G, cfg.N, cfg.K), dtype=torch.uint8, device="cuda")
