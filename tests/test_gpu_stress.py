@@ -66,8 +66,10 @@ def test_encode_kernels_deterministic_under_perturbation(gfm, q, N, K, M, G, ker
         assert np.array_equal(outs[0][g].cpu().numpy(), oracle.encode_batch(q, Ah, Ch)[0]), (kern, g)
 
 
-@pytest.mark.parametrize("q", (2, 256))
+@pytest.mark.parametrize("q", (2, 4, 256))
 def test_fused_verify_deterministic_under_perturbation(gfm, q):
+    """GF(2) split engine and lane-k (GF(4)) with the check fused in, the
+    product-row encode followed by the streaming check (GF(256))."""
     N, K, M, G = (64, 64, 1500, 2048) if q == 256 else (32, 32, 65536, 24)
     A = torch.empty((G, N, M), dtype=torch.uint8, device="cuda")
     C = torch.empty((G, N, K), dtype=torch.uint8, device="cuda")
