@@ -354,7 +354,9 @@ __global__ void __launch_bounds__(256) verify_plain_kernel(const uint8_t *A, con
 // warp-uniform, so y2 is a masked XOR per coded row.  Bytes where y1 != y2 are
 // counted per generation (same count as verify_plain_kernel).
 constexpr int kVwW = 4;                                       // words per lane
-template <int T>
+// KB blocks of 64 coded packets per pass over A (C4: K = 256, four blocks in one
+// pass): the selectors of a source word are made once for all KB blocks.
+template <int T, int KB>
 __global__ void __launch_bounds__(32) verify_words_kernel(const uint8_t *A, const uint8_t *B, const uint8_t *U,
                                                            const uint32_t *RB, const uint32_t *__restrict__ tabs,
                                                            int N, int K, int kblocks, int kw, size_t M, size_t batch,
@@ -375,13 +377,16 @@ __global__ void __launch_bounds__(32) verify_words_kernel(const uint8_t *A, cons
 #pragma unroll
     for (int v = 0; v < kVwW; v++) ok[v] = w0 + 32 * v < Mw;
     uint32_t bad = 0;
-    for (int b = 0; b < kblocks; b++) {
-        uint32_t y1[T][kVwW], y2[T][kVwW];
+    for (int b0 = 0; b0 < kblocks; b0 += KB) {
+        const int nb = min(KB, kblocks - b0);                  // blocks of this pass
+        uint32_t y1[KB][T][kVwW];
 #pragma unroll
-        for (int j = 0; j < T; j++)
+        for (int bb = 0; bb < KB; bb++)
 #pragma unroll
-            for (int v = 0; v < kVwW; v++) y1[j][v] = y2[j][v] = 0u;
-        const uint8_t *Ub = U + (g * kblocks + b) * 2 * (size_t)N;
+            for (int j = 0; j < T; j++)
+#pragma unroll
+                for (int v = 0; v < kVwW; v++) y1[bb][j][v] = 0u;
+        const uint8_t *Ub = U + (g * kblocks + b0) * 2 * (size_t)N;   // block b0 + bb at Ub + 2 N bb
         // source words of four sources in flight while two are multiplied
         // (HBM latency, not issue, bounds a warp that waits per source)
         auto load2 = [&](int i, uint32_t (&a)[2][kVwW]) {
@@ -401,19 +406,22 @@ __global__ void __launch_bounds__(32) verify_words_kernel(const uint8_t *A, cons
 #pragma unroll
             for (int h = 0; h < 2; h++) {
                 if (i + h >= N) break;
-                PrmtTab Tj[T];
+                Sel sv[kVwW];
 #pragma unroll
-                for (int j = 0; j < T; j++) {
-                    const uint32_t *tp = tabs + (size_t)__ldg(Ub + (size_t)j * N + i + h) * 16u;
-                    const uint4 t0 = __ldg(reinterpret_cast<const uint4 *>(tp));
-                    Tj[j].t0lo = t0.x; Tj[j].t0hi = t0.y; Tj[j].t1lo = t0.z; Tj[j].t1hi = t0.w;
-                    Tj[j].t2 = __ldg(tp + 4);
-                }
+                for (int v = 0; v < kVwW; v++) sv[v] = make_sel(acur[h][v]);
 #pragma unroll
-                for (int v = 0; v < kVwW; v++) {
-                    const Sel s = make_sel(acur[h][v]);
+                for (int bb = 0; bb < KB; bb++) {
+                    if (bb >= nb) break;
 #pragma unroll
-                    for (int j = 0; j < T; j++) y1[j][v] ^= lookup_perm(Tj[j], s);
+                    for (int j = 0; j < T; j++) {
+                        const uint32_t *tp = tabs + (size_t)__ldg(Ub + (size_t)(2 * bb + j) * N + i + h) * 16u;
+                        const uint4 t0 = __ldg(reinterpret_cast<const uint4 *>(tp));
+                        PrmtTab Tt;
+                        Tt.t0lo = t0.x; Tt.t0hi = t0.y; Tt.t1lo = t0.z; Tt.t1hi = t0.w;
+                        Tt.t2 = __ldg(tp + 4);
+#pragma unroll
+                        for (int v = 0; v < kVwW; v++) y1[bb][j][v] ^= lookup_perm(Tt, sv[v]);
+                    }
                 }
             }
 #pragma unroll
@@ -424,40 +432,50 @@ __global__ void __launch_bounds__(32) verify_words_kernel(const uint8_t *A, cons
                     anext[h][v] = afar[h][v];
                 }
         }
-        // coded rows eight at a time; a row in no projection is not read
-        const int k1 = min(K, 64 * b + 64);
+        // each block's coded rows eight at a time; a row in no projection is not read
+#pragma unroll
+        for (int bb = 0; bb < KB; bb++) {
+            if (bb >= nb) break;
+            const int b = b0 + bb;
+            uint32_t y2[T][kVwW];
+#pragma unroll
+            for (int j = 0; j < T; j++)
+#pragma unroll
+                for (int v = 0; v < kVwW; v++) y2[j][v] = 0u;
+            const int k1 = min(K, 64 * b + 64);
 #pragma unroll 1
-        for (int k0 = 64 * b; k0 < k1; k0 += 8) {
-            uint32_t rb[T];
+            for (int k0 = 64 * b; k0 < k1; k0 += 8) {
+                uint32_t rb[T];
 #pragma unroll
-            for (int j = 0; j < T; j++) rb[j] = __ldg(RB + (g * 2 + j) * kw + (k0 >> 5)) >> (k0 & 31);   // 8 | 32
-            uint32_t x[8][kVwW];
+                for (int j = 0; j < T; j++) rb[j] = __ldg(RB + (g * 2 + j) * kw + (k0 >> 5)) >> (k0 & 31);   // 8 | 32
+                uint32_t x[8][kVwW];
 #pragma unroll
-            for (int e = 0; e < 8; e++) {
-                uint32_t sel = 0u;
+                for (int e = 0; e < 8; e++) {
+                    uint32_t sel = 0u;
 #pragma unroll
-                for (int j = 0; j < T; j++) sel |= rb[j] >> e;
-                const bool need = (sel & 1u) && k0 + e < k1;
+                    for (int j = 0; j < T; j++) sel |= rb[j] >> e;
+                    const bool need = (sel & 1u) && k0 + e < k1;
 #pragma unroll
-                for (int v = 0; v < kVwW; v++)
-                    x[e][v] = (need && ok[v]) ? __ldg(Bg + (size_t)(k0 + e) * Mw + 32 * v) : 0u;
+                    for (int v = 0; v < kVwW; v++)
+                        x[e][v] = (need && ok[v]) ? __ldg(Bg + (size_t)(k0 + e) * Mw + 32 * v) : 0u;
+                }
+#pragma unroll
+                for (int e = 0; e < 8; e++)
+#pragma unroll
+                    for (int j = 0; j < T; j++) {
+                        const uint32_t m = 0u - ((rb[j] >> e) & 1u);
+#pragma unroll
+                        for (int v = 0; v < kVwW; v++) y2[j][v] ^= x[e][v] & m;
+                    }
             }
 #pragma unroll
-            for (int e = 0; e < 8; e++)
+            for (int j = 0; j < T; j++)
 #pragma unroll
-                for (int j = 0; j < T; j++) {
-                    const uint32_t m = 0u - ((rb[j] >> e) & 1u);
-#pragma unroll
-                    for (int v = 0; v < kVwW; v++) y2[j][v] ^= x[e][v] & m;
-                }
+                for (int v = 0; v < kVwW; v++) bad += nz_bytes(unperm(y1[bb][j][v]) ^ y2[j][v]);
         }
-#pragma unroll
-        for (int j = 0; j < T; j++)
-#pragma unroll
-            for (int v = 0; v < kVwW; v++) bad += nz_bytes(unperm(y1[j][v]) ^ y2[j][v]);
     }
-    const uint32_t nb = __reduce_add_sync(0xffffffffu, bad);
-    if (lane == 0 && nb) atomicAdd(mismatch + g, (unsigned long long)nb);
+    const uint32_t nbad = __reduce_add_sync(0xffffffffu, bad);
+    if (lane == 0 && nbad) atomicAdd(mismatch + g, (unsigned long long)nbad);
 }
 
 // mismatch[g] += #{ positions where Y1[g] and Y2[g] differ }, Y: [batch][len]

@@ -1114,12 +1114,22 @@ int gf_encode_verify_batch(int field, const uint8_t *A, const uint8_t *C, uint8_
     if (M % 4 == 0 && ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 3u) == 0) {
         const size_t units = batch * ((M / 4 + 32 * kVwW - 1) / (32 * kVwW));   // (generation, 128-word chunk)
         if (units > 0x7FFFFFFFu) return GF_EARG;
-        if (t == 1)
-            verify_words_kernel<1><<<(unsigned)units, 32, 0, st>>>(A, B, U, RB, ftabs, N, K, kblocks, kw, M, batch,
-                                                                  mismatch);
-        else
-            verify_words_kernel<2><<<(unsigned)units, 32, 0, st>>>(A, B, U, RB, ftabs, N, K, kblocks, kw, M, batch,
-                                                                  mismatch);
+        // blocks of 64 coded packets per pass over A: all of them up to four
+        const int kb = kblocks >= 4 ? 4 : kblocks;
+        auto go = [&](auto kern) {
+            kern<<<(unsigned)units, 32, 0, st>>>(A, B, U, RB, ftabs, N, K, kblocks, kw, M, batch, mismatch);
+        };
+        if (t == 1) {
+            if (kb == 1) go(verify_words_kernel<1, 1>);
+            else if (kb == 2) go(verify_words_kernel<1, 2>);
+            else if (kb == 3) go(verify_words_kernel<1, 3>);
+            else go(verify_words_kernel<1, 4>);
+        } else {
+            if (kb == 1) go(verify_words_kernel<2, 1>);
+            else if (kb == 2) go(verify_words_kernel<2, 2>);
+            else if (kb == 3) go(verify_words_kernel<2, 3>);
+            else go(verify_words_kernel<2, 4>);
+        }
         return launch_status();
     }
     unsigned gx = (unsigned)((M + 255) / 256);
