@@ -108,3 +108,18 @@ def test_job_plan_for_a_rank_without_work():
     assert sorted(gens) == [0] * 7 + [1]
     r, h = bench.dominant_roofline(256, 16, 1, 1500, 0, "stream", 1e-9, PEAKS)
     assert r["byte_madds_per_launch"] == 0
+
+
+def test_ncu_traffic_matches_the_headline_kernel_source():
+    """roofline.traffic comes from a committed ncu --set full capture, valid only
+    for the kernel source it measured: the headline (C3 GF(256), product-row)
+    entry must carry the current source hash, and its DRAM bytes must agree with
+    the algorithmic A + B bytes of the launch to within 1% (no re-reads)."""
+    import json
+    import os
+    import bench
+    d = json.load(open(os.path.join(bench.ROOT, "profiles", "ncu_traffic.json")))
+    e = d["C3/GF256/65536/1500"]
+    assert e["kernel_sha"] == bench.kernel_sha("prow"), "re-capture the C3 kernel with ncu (profiles/ncu_traffic.json)"
+    algorithmic = 65536 * (64 * 1500 + 64 * 64 + 64 * 1500)
+    assert abs(e["bytes"] / algorithmic - 1) < 0.01
