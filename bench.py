@@ -417,6 +417,7 @@ def main():
     path = gf.encode_path(q, N, K, job.Ms)
     roof, hbm = dominant_roofline(q, N, K, job.Ms, job.chunk, path, avg_kernel_s, peaks)
     roof["traffic"] = lookup_traffic(q, cfg, job.chunk, job.Ms, path)
+    alu = lookup_pipes(q, cfg, job.chunk, job.Ms, path)
     roof["kernel_ms"] = round(statistics.mean(kern_ms), 4) if kern_ms else None
 
     # the oracle's sample compared with the GPU's bytes (rank 0, N = 1): the
@@ -492,6 +493,7 @@ def main():
             "per_field": per_field,
             "roofline": roof,
             "hbm": hbm,
+            "alu": alu,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clocks,
@@ -522,6 +524,9 @@ def field_entry(value, cfg, q, path, ms_per_step, total_ms, kern_ms, job_src, st
         e["launches_per_step"] = nchunks
         e["gens_per_launch"] = chunk
         e["timing"] = "sum of encode-launch event durations (inputs of each chunk generated between launches)"
+    alu = lookup_pipes(q, cfg, chunk if chunk else cfg.batch, sh.columns, path)
+    if alu:
+        e["alu"] = alu
     return e
 
 
@@ -608,6 +613,24 @@ def kernel_sha(path):
     if not f:
         return None
     return hashlib.sha256(open(os.path.join(ROOT, "paper_1909_02871_b200", "csrc", f), "rb").read()).hexdigest()[:16]
+
+
+def lookup_pipes(q, cfg, gens, Ms, path):
+    """The integer-ALU (and FMA) pipe activity of the encode launch, as fractions
+    of peak, from the same committed ncu capture as `traffic` (None when the
+    kernel source changed since).  The method's binding resource and its
+    roofline fraction are in `roofline`; this is the integer-ALU side the
+    north star asks for next to HBM."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        e = json.load(open(p)).get(f"{cfg.name}/GF{q}/{gens}/{Ms}")
+        if e and e.get("kernel_sha") == kernel_sha(path) and "pipes" in e:
+            return {"alu_pipe_active": e["pipes"]["alu"], "fma_pipe_active": e["pipes"]["fma"],
+                    "issue_active": e["pipes"]["issue"], "unit": "fraction of peak (ncu, active cycles)",
+                    "source": e["source"]}
+    except Exception:
+        pass
+    return None
 
 
 def lookup_traffic(q, cfg, gens, Ms, path):
