@@ -152,3 +152,36 @@ def test_encode_verify_argument_errors(gfm):
     assert L.gf_encode_verify_batch(256, A.data_ptr(), C.data_ptr(), B.data_ptr(), R.data_ptr(), 2, N, K, M, 0,
                                     mism.data_ptr(), ws.data_ptr(), need) == gfm.GF_OK   # empty batch
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_verify_random_shapes(gfm, seed):
+    """Seeded random shapes through gf_encode_verify_batch (whatever kernel the
+    router picks: lane-k with the check fused, the GF(2) split engine, product
+    rows, column, streaming, each followed by the matching check): B bit-exact
+    and the per-generation counts equal to the oracle's, with and without one
+    injected wrong byte."""
+    rng = np.random.default_rng(9000 + seed)
+    q = int(rng.choice([2, 4, 16, 256]))
+    N = int(rng.integers(1, 70))
+    K = int(rng.integers(1, 140))
+    M = 4 * int(rng.integers(1, 700)) + (0 if seed % 6 else int(rng.integers(1, 4)))
+    batch = int(rng.integers(1, 5))
+    t = 1 + seed % 2
+    A = si.random_bytes(9100 + seed, si.STREAM_A, 0, batch * N * M).reshape(batch, N, M)
+    C = si.uniform_coeffs(q, 9200 + seed, si.STREAM_C, 0, batch * N * K).reshape(batch, N, K)
+    R = si.random_bytes(9300 + seed, si.STREAM_FREIVALDS, 0, batch * K * t).reshape(batch, K, t)
+    B, mism = gfm.encode_verify_batch(q, *(torch.from_numpy(x).cuda() for x in (A, C, R)))
+    Bh = B.cpu().numpy()
+    path = gfm.encode_path(q, N, K, M)
+    assert np.array_equal(Bh, oracle.encode_batch(q, A, C)), (q, N, K, M, batch, path)
+    assert int(mism.sum()) == 0, (q, N, K, M, batch, path)
+    g, k, w = int(rng.integers(0, batch)), int(rng.integers(0, K)), int(rng.integers(0, M // 4)) if M >= 4 else 0
+    gfm.set_verify_fault(g, k, w)
+    try:
+        B2, mism2 = gfm.encode_verify_batch(q, *(torch.from_numpy(x).cuda() for x in (A, C, R)))
+    finally:
+        gfm.set_verify_fault(-1)
+    B2h = B2.cpu().numpy()
+    assert int((B2h != Bh).sum()) == (1 if 4 * w < M else 0), (q, N, K, M, batch, path, g, k, w)
+    assert np.array_equal(mism2.cpu().numpy(), oracle_counts(q, A, C, B2h, R)), (q, N, K, M, batch, path)
