@@ -181,17 +181,25 @@ __global__ void __launch_bounds__(kG2Threads, T > 0 ? 3 : 1) encode_gf2_kernel(G
             const uint32_t mus = (uint32_t)__cvta_generic_to_shared(mu);
 #pragma unroll
             for (int j = 0; j < T; j++) {
-                uint32_t x[4] = {y2[j][0], y2[j][1], y2[j][2], y2[j][3]};
+                // two independent XOR chains per word (even / odd source groups),
+                // joined at the end: half the dependent-LOP3 depth
+                uint32_t x[4] = {y2[j][0], y2[j][1], y2[j][2], y2[j][3]}, xo[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
                 for (int q = 0; q < NS / 4; q++) {
                     uint4 m;                          // volatile: read here, not hoisted across the k loop
                     asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                                  : "=r"(m.x), "=r"(m.y), "=r"(m.z), "=r"(m.w) : "r"(mus + (uint32_t)(j * NS + 4 * q) * 4u));
 #pragma unroll
-                    for (int w = 0; w < 4; w++)
-                        x[w] ^= (a[4 * q][w] & m.x) ^ (a[4 * q + 1][w] & m.y) ^ (a[4 * q + 2][w] & m.z) ^
-                                (a[4 * q + 3][w] & m.w);
+                    for (int w = 0; w < 4; w++) {
+                        uint32_t &xx = (q & 1) ? xo[w] : x[w];
+                        xx ^= a[4 * q][w] & m.x;
+                        xx ^= a[4 * q + 1][w] & m.y;
+                        xx ^= a[4 * q + 2][w] & m.z;
+                        xx ^= a[4 * q + 3][w] & m.w;
+                    }
                 }
+#pragma unroll
+                for (int w = 0; w < 4; w++) x[w] ^= xo[w];
                 if (valid)
 #pragma unroll
                     for (int w = 0; w < 4; w++) bad += nz_bytes(x[w]);
