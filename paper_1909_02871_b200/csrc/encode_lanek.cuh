@@ -158,24 +158,18 @@ __device__ __forceinline__ void build_word(uint32_t *q, const uint32_t (&a)[LkFi
     }
 }
 
-// u * a for packed elements of F (u < q): the xtime chain of a, masked by the
-// bits of u (the A-side projection of the fused check)
+// bits per element; the xtime chain x^b a (b < bits) of a packed word -- u * a
+// is the XOR of the chain values selected by the bits of u (the A-side
+// projection of the fused check, with u's bits as precomputed masks)
+template <int F> __host__ __device__ constexpr int lk_bits() { return F == 2 ? 1 : F == 4 ? 2 : F == 16 ? 4 : 8; }
 template <int F>
-__device__ __forceinline__ uint32_t lk_mul(uint32_t a, uint32_t u)
+__device__ __forceinline__ void lk_chain(uint32_t a, uint32_t (&x)[lk_bits<F>()])
 {
-    if constexpr (F == 2) {
-        return a & (0u - (u & 1u));
-    } else if constexpr (F == 4) {
-        return (a & (0u - (u & 1u))) ^ (gf4_xtime(a) & (0u - ((u >> 1) & 1u)));
-    } else {
-        constexpr int w = F == 16 ? 4 : 8;
-        uint32_t y = 0, x = a;
+    x[0] = a;
 #pragma unroll
-        for (int b = 0; b < w; b++) {
-            y ^= x & (0u - ((u >> b) & 1u));
-            if (b + 1 < w) x = LkField<F>::xtime(x);
-        }
-        return y;
+    for (int b = 1; b < lk_bits<F>(); b++) {
+        if constexpr (F == 4) x[b] = gf4_xtime(x[b - 1]);
+        else if constexpr (F != 2) x[b] = LkField<F>::xtime(x[b - 1]);
     }
 }
 
@@ -217,14 +211,26 @@ encode_lanek_kernel(LanekParams p)
     uint32_t *y1s = reinterpret_cast<uint32_t *>(ccache + (((size_t)KTL * NS + 15) & ~(size_t)15));
     uint32_t *y2s = y1s + VT * TW;
     (void)y2s;
+    // fused check: masks -(bit b of u_ji) per (step, source of the step, projection, b)
+    constexpr int WB = lk_bits<F>(), kMaskStep = SG * VT * WB;   // words per step (a multiple of 4)
+    static_assert(VT == 0 || kMaskStep % 4 == 0, "mask words per step");
+    uint32_t *umask = y2s + VT * TW;
+    (void)umask;
     const int kblk = (p.K + 63) / 64, bk = k0 / 64;            // the CTA's block of 64 coded packets
     (void)kblk;
     (void)bk;
 
     // zero rows (index 0, and 16 for GF(256)) of every buffer; row indices of
     // every (step, k) from the coefficients (rows past N count as c = 0)
-    if constexpr (VT > 0)
+    if constexpr (VT > 0) {
         for (int t = threadIdx.x; t < VT * TW; t += blockDim.x) y2s[t] = 0u;
+        const uint8_t *Ub = p.U + ((g * (size_t)kblk + (size_t)bk) * 2) * (size_t)p.N;
+        for (int e = threadIdx.x; e < NS * kMaskStep; e += blockDim.x) {
+            const int b = e % WB, rest = e / WB, j = rest % VT, i = rest / VT;   // i = SG s + source of the step
+            const uint32_t u = i < p.N ? __ldg(Ub + (size_t)j * p.N + i) : 0u;
+            umask[e] = 0u - ((u >> b) & 1u);
+        }
+    }
     for (int t = threadIdx.x; t < QS; t += blockDim.x) {
 #pragma unroll
         for (int b = 0; b < kLkNQ; b++) {
@@ -260,8 +266,7 @@ encode_lanek_kernel(LanekParams p)
         for (int j = 0; j < (VT > 0 ? VT : 1); j++)
 #pragma unroll
             for (int u = 0; u < G::BWORDS; u++) y1[j][u] = 0u;
-        const uint8_t *Ub = p.U + ((g * (size_t)kblk + (size_t)bk) * 2) * (size_t)p.N;
-        (void)Ub;
+
         auto load = [&](int s, uint32_t (&a)[G::BWORDS][SG]) {
 #pragma unroll
             for (int j = 0; j < SG; j++) {
@@ -286,17 +291,23 @@ encode_lanek_kernel(LanekParams p)
             }
             nbar_arrive(BAR_FULL + b, NT);
             if constexpr (VT > 0) {                            // y1_j += u_ji a_i (before the loads reuse a)
+                uint32_t m[kMaskStep];                          // this step's masks (broadcast loads)
 #pragma unroll
-                for (int jj = 0; jj < SG; jj++) {
-                    const int i = s * SG + jj;
-                    if (i >= p.N) break;
-#pragma unroll
-                    for (int j = 0; j < VT; j++) {
-                        const uint32_t u = __ldg(Ub + (size_t)j * p.N + i);
-#pragma unroll
-                        for (int v = 0; v < G::BWORDS; v++) y1[j][v] ^= lk_mul<F>(a[v][jj], u);
-                    }
+                for (int c = 0; c < kMaskStep; c += 4) {
+                    const uint4 mv = *reinterpret_cast<const uint4 *>(umask + s * kMaskStep + c);
+                    m[c] = mv.x; m[c + 1] = mv.y; m[c + 2] = mv.z; m[c + 3] = mv.w;
                 }
+#pragma unroll
+                for (int jj = 0; jj < SG; jj++)
+#pragma unroll
+                    for (int v = 0; v < G::BWORDS; v++) {
+                        uint32_t x[WB];                             // x^b a, shared by the projections
+                        lk_chain<F>(a[v][jj], x);
+#pragma unroll
+                        for (int j = 0; j < VT; j++)
+#pragma unroll
+                            for (int b = 0; b < WB; b++) y1[j][v] ^= x[b] & m[(jj * VT + j) * WB + b];
+                    }
             }
             load(s + D, a);
         };
@@ -453,7 +464,8 @@ __host__ __device__ constexpr size_t lk_smem_bytes(int N)
     using G = LkGeom<KG, F == 2 && KG == 1>;
     return (size_t)kLkNQ * LkField<F>::kRows * G::QS * 4 +
            (((size_t)32 * KG * ((N + LkField<F>::kSG - 1) / LkField<F>::kSG) + 15) & ~(size_t)15) +
-           (size_t)2 * VT * G::TW * 4;
+           (size_t)2 * VT * G::TW * 4 +
+           (size_t)VT * ((N + LkField<F>::kSG - 1) / LkField<F>::kSG) * LkField<F>::kSG * lk_bits<F>() * 4;
 }
 
 }  // namespace gfr
