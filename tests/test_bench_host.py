@@ -123,3 +123,17 @@ def test_ncu_traffic_matches_the_headline_kernel_source():
     assert e["kernel_sha"] == bench.kernel_sha("prow"), "re-capture the C3 kernel with ncu (profiles/ncu_traffic.json)"
     algorithmic = 65536 * (64 * 1500 + 64 * 64 + 64 * 1500)
     assert abs(e["bytes"] / algorithmic - 1) < 0.01
+
+
+def test_alu_pipes_from_the_committed_capture():
+    """The bench line's `alu` object: the integer-ALU / FMA pipe activity and
+    issue activity of the headline launch, fractions of peak in (0, 1), from
+    the same capture (and source hash) as `traffic`; None for a launch that
+    was never captured."""
+    import bench
+    import seeded_inputs as si
+    a = bench.lookup_pipes(256, si.C3, 65536, 1500, "prow")
+    assert a is not None and a["source"].startswith("profiles/")
+    for k in ("alu_pipe_active", "fma_pipe_active", "issue_active"):
+        assert 0.0 < a[k] < 1.0
+    assert bench.lookup_pipes(256, si.C3, 12345, 1500, "prow") is None
