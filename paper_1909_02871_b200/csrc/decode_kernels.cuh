@@ -234,6 +234,82 @@ __global__ void __launch_bounds__(32 * kInvWarps) invert_warp_kernel(InvertParam
     if (lane == 0 && p.rank) p.rank[g] = rank;
 }
 
+// ---- GF(2), N <= 64: bit-sliced Gauss-Jordan, one warp per matrix --------
+// Over GF(2) an entry is one bit, so a row of [C | I] is 128 bits: lane l
+// holds rows l and l + 32 as (C bits, I bits) pairs of 64-bit words.  Per
+// column: a ballot over the rows not yet used whose bit is set picks the
+// pivot, four shuffles broadcast it, and every other row with the bit set
+// XORs it in -- the byte-packed kernels' row operation on 64 entries per
+// instruction pair.  No row swaps: the pivot row remembers its column and
+// becomes that row of D.
+constexpr int kInvG2Warps = 8;
+
+__global__ void __launch_bounds__(32 * kInvG2Warps) invert_gf2_kernel(InvertParams p)
+{
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const size_t g = (size_t)blockIdx.x * kInvG2Warps + warp;
+    if (g >= p.batch) return;
+    const int N = p.N;
+    const uint8_t *Cg = p.C + g * (size_t)N * N;
+    const bool words = (N % 4) == 0 && (reinterpret_cast<uintptr_t>(p.C) & 3u) == 0;
+    auto load_row = [&](int r, uint64_t &c, uint64_t &d) {
+        c = 0;
+        d = 0;
+        if (r >= N) return;
+        const uint8_t *row = Cg + (size_t)r * N;
+        if (words) {
+            for (int q = 0; q < N / 4; q++) {
+                const uint32_t x = __ldg(reinterpret_cast<const uint32_t *>(row) + q) & 0x01010101u;
+                const uint32_t nib = (x & 1u) | ((x >> 7) & 2u) | ((x >> 14) & 4u) | ((x >> 21) & 8u);
+                c |= (uint64_t)nib << (4 * q);
+            }
+        } else {
+            for (int k = 0; k < N; k++) c |= (uint64_t)(__ldg(row + k) & 1u) << k;
+        }
+        d = 1ull << r;
+    };
+    uint64_t ca, da, cb, db;
+    load_row(lane, ca, da);
+    load_row(lane + 32, cb, db);
+    int pa = -1, pb = -1;                             // column this row became the pivot of
+    int rank = 0;
+    for (int col = 0; col < N; col++) {
+        const bool sa = (ca >> col) & 1u, sb = (cb >> col) & 1u;
+        const uint32_t ba = __ballot_sync(0xffffffffu, sa && pa < 0);
+        const uint32_t bb = __ballot_sync(0xffffffffu, sb && pb < 0);
+        if ((ba | bb) == 0u) continue;                // no pivot: rank deficient column
+        const bool inA = ba != 0u;
+        const int pl = inA ? __ffs(ba) - 1 : __ffs(bb) - 1;
+        const uint64_t pc = __shfl_sync(0xffffffffu, inA ? ca : cb, pl);
+        const uint64_t pd = __shfl_sync(0xffffffffu, inA ? da : db, pl);
+        const bool pivA = inA && lane == pl, pivB = !inA && lane == pl;
+        if (sa && !pivA) { ca ^= pc; da ^= pd; }
+        if (sb && !pivB) { cb ^= pc; db ^= pd; }
+        if (pivA) pa = col;
+        if (pivB) pb = col;
+        rank++;
+    }
+    // row pcol of D = the I bits of the row that pivoted on pcol, one byte per entry
+    uint8_t *Dg = p.D + g * (size_t)N * N;
+    const bool dwords = (N % 4) == 0 && (reinterpret_cast<uintptr_t>(p.D) & 3u) == 0;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const int pc = h ? pb : pa;
+        if (pc < 0) continue;
+        const uint64_t d = h ? db : da;
+        uint8_t *drow = Dg + (size_t)pc * N;
+        if (dwords) {
+            for (int q = 0; q < N / 4; q++) {
+                const uint32_t nib = (uint32_t)(d >> (4 * q)) & 0xFu;
+                reinterpret_cast<uint32_t *>(drow)[q] = (nib * 0x00204081u) & 0x01010101u;   // bit e -> byte e
+            }
+        } else {
+            for (int k = 0; k < N; k++) drow[k] = (uint8_t)((d >> k) & 1u);
+        }
+    }
+    if (lane == 0 && p.rank) p.rank[g] = rank;
+}
+
 }  // namespace gfr
 
 namespace gfr {

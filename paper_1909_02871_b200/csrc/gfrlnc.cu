@@ -957,6 +957,11 @@ int gf_invert_batch(int field, const uint8_t *C, uint8_t *D, int *rank, int N, s
     p.tabs = reinterpret_cast<const uint32_t *>(tabs) + (size_t)fi * 256 * kTableWords;
     p.inv = reinterpret_cast<const uint8_t *>(inv) + (size_t)fi * 256;
     const size_t rw = (2 * (size_t)N + 3) / 4;
+    if (field == 2 && N <= 64) {                              // bit-sliced, warp per matrix
+        invert_gf2_kernel<<<(unsigned)((batch + kInvG2Warps - 1) / kInvG2Warps), 32 * kInvG2Warps, 0,
+                            tls_stream>>>(p);
+        return launch_status();
+    }
     if (N <= 64) {                                            // warp per matrix (no CTA barriers)
         const size_t smem_w = (256 * 5 + 64 + kInvWarps * 32 * 4) * 4 + (size_t)kInvWarps * N * (rw + 1) * 4;
         invert_warp_kernel<<<(unsigned)((batch + kInvWarps - 1) / kInvWarps), 32 * kInvWarps, smem_w,

@@ -83,7 +83,7 @@ def test_fused_verify_deterministic_under_perturbation(gfm, q):
         assert torch.equal(B, ref) and int(mism.sum()) == 0
 
 
-@pytest.mark.parametrize("q,N", [(256, 64), (16, 33), (256, 80), (2, 130)])
+@pytest.mark.parametrize("q,N", [(256, 64), (16, 33), (256, 80), (2, 130), (2, 64), (2, 37)])
 def test_inversion_deterministic_under_perturbation(gfm, q, N):
     G = 4096 if N <= 64 else 256
     C = torch.empty((G, N, N), dtype=torch.uint8, device="cuda")
