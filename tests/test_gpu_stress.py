@@ -18,7 +18,9 @@ import seeded_inputs as si
 
 pytestmark = pytest.mark.gpu
 
-REPS = 25
+import os
+
+REPS = int(os.environ.get("GF_STRESS_REPS", "25"))   # 25 in the suite; longer one-off runs: profiles/r02_stress_*.log
 
 
 @pytest.fixture(scope="module")
