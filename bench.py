@@ -48,6 +48,7 @@ ALU_LANES_PER_SM_CLK = 64     # B300_MICROARCH.md: alu pipe rt_SMSP = 2 -> 16 la
 ISSUE_LANES_PER_SM_CLK = 128  # 4 SMSPs x 1 warp-instruction / clk x 32 lanes
 N_SM = 148
 SMEM_BYTES_PER_SM_CLK = 128   # shared-memory pipe (tools/ubench_smem.cu, profiles/r01_ubench_smem.txt)
+TMEM_X2_BYTES_PER_SM_CLK = 132.8   # tcgen05.ld.32x32b.x2 from 32 warps (tools/ubench_tmem2.cu, profiles/r02_ubench_tmem2.txt)
 # algorithmic ALU ops per byte-madd of the column kernel's inner loop:
 # GF(256)/GF(16) 3 PRMT + 2 LOP3 per 4 byte-madds; GF(4) 2 LOP3; GF(2) 1 LOP3
 OPS_PER_BYTE_MADD = {256: 5 / 4, 16: 5 / 4, 4: 2 / 4, 2: 1 / 4}
@@ -576,6 +577,21 @@ def dominant_roofline(q, N, K, Ms, gens, path, kernel_s, peaks):
         roof = {"bound": "smem", "achieved": round(ach / 1e12, 3), "peak": round(smem_peak / 1e12, 3),
                 "unit": "TB/s", "frac": round(ach / smem_peak, 4), "peak_source": smem_src,
                 "smem_bytes_per_launch": smem_bytes}
+    elif path == "tmem":
+        # TMEM lookup-table engine: HBM-bound design; its lookups read 8 B per
+        # lane from tensor memory (tcgen05.ld.32x32b.x2), one per (4-bit group,
+        # coded packet, 2-word lane slot), against the measured x2-load rate
+        w = {2: 1, 4: 2, 16: 4, 256: 8}[q]
+        ng = -(-(-(-N * w // 4)) // 4) * 4
+        spans = -(-(Ms // 4) // 64)
+        kp = -(-K // 32) * 32
+        tm_bytes = gens * spans * 32 * ng * kp * 8
+        tm_peak = N_SM * TMEM_X2_BYTES_PER_SM_CLK * clk
+        roof = dict(hbm, bound="hbm")
+        roof["tmem_read_bytes_per_launch"] = tm_bytes
+        roof["tmem_read_frac"] = round(tm_bytes / kernel_s / tm_peak, 4)
+        roof["tmem_peak_source"] = (f"{N_SM} SMs x {TMEM_X2_BYTES_PER_SM_CLK} B/clk (tcgen05.ld.32x32b.x2, "
+                                    f"profiles/r02_ubench_tmem2.txt) x {peaks['sm_max_mhz']:.0f} MHz")
     elif path == "gf2-split":
         issue_peak = N_SM * ISSUE_LANES_PER_SM_CLK * clk
         roof = dict(hbm, bound="hbm")
@@ -602,7 +618,7 @@ def dominant_roofline(q, N, K, Ms, gens, path, kernel_s, peaks):
 KERNEL_SOURCES = {"prow": "encode_prow.cuh", "prow-32": "encode_prow.cuh", "prow-16": "encode_prow.cuh",
                   "prow-nib": "encode_prow16.cuh", "prow-32w": "encode_prow.cuh",
                   "lanek-32": "encode_lanek.cuh", "lanek-64": "encode_lanek.cuh", "stream": "encode_stream.cuh",
-                  "column-words": "encode_kernels.cuh", "gf2-split": "encode_gf2.cuh"}
+                  "column-words": "encode_kernels.cuh", "gf2-split": "encode_gf2.cuh", "tmem": "encode_tmem.cuh"}
 
 
 def kernel_sha(path):

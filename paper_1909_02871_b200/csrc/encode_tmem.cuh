@@ -1,0 +1,340 @@
+// encode_tmem.cuh -- batched RLNC encode with the multiples of the source words
+// held as lookup tables in tensor memory (TMEM), indexed by the coefficients.
+//
+//   B[g][k][m] = XOR_{i < N} C[g][i][k] * A[g][i][m]          (Eq. 2)
+//
+// Over F_q, q = 2^w, multiplication by c is linear over GF(2):
+//   c * a = XOR_{j < w} c_j * (x^j a)        (c_j = bit j of c; §II)
+// so a coded word b_k is the XOR of the basis words e_t = x^j a_i (t = i w + j)
+// selected by the coefficient bits.  The basis words of a span are cut into
+// groups of four; a group's 16 XOR-subsets form a table T[0..15], and the
+// contribution of the group to coded packet k is ONE lookup T[idx(k)], idx(k)
+// = the four coefficient bits that select the group's basis words.  This is the
+// paper's split-table idea (Alg. 1: precompute the products
+// of a 4-bit part once, look them up, XOR the parts) turned around: the
+// tables hold products of the DATA with every 4-bit coefficient part, so the
+// table index depends only on C and is the same for all 32 lanes of a warp.
+//   GF(2):   group = 4 sources,                   idx = c_i c_i+1 c_i+2 c_i+3
+//   GF(4):   group = 2 sources {a, xa, b, xb},    idx = c_i | c_i+1 << 2
+//   GF(16):  group = 1 source {a, xa, x^2a, x^3a}, idx = c_i
+//   GF(256): 2 groups per source (x^0..3 a, x^4..7 a), idx = low / high nibble
+// A warp-uniform index is what TMEM serves: tcgen05.ld reads one column (a
+// uniform address) for all 32 lanes of the warp's lane quarter, on the tensor
+// memory datapath beside the shared-memory pipe (~200-270 B/clk
+// per SM from ordinary warps, tools/ubench_tmem.cu).
+//
+// Layout: warp wid owns TMEM lanes 32 (wid % 4) .. +31 and 64 columns
+// (2 groups x 16 combos x 2 words).  Lane l holds words 2l, 2l+1 of a 64-word
+// (256-byte) span of every packet; a work unit is (generation, span), and
+// each warp walks a contiguous range of units.  A unit is processed in passes
+// of 32 coded packets (accumulators acc[32][2] in registers) and steps of 2
+// groups: per step the lane builds the 2 x 16 combos of its two words
+// (11 XORs per group and word, plus the field's x-multiples), stores them with
+// one tcgen05.st.32x32b.x32 per group, and each coded packet XORs two
+// tcgen05.ld.32x32b.x2 results into its accumulator (one LOP3 per word).
+// The TMEM column addresses of every (pass, group, k) are precomputed per
+// warp and generation in shared memory and read with broadcast LDS.128.
+// Source words stream through a per-warp ring of kTmRing steps with cp.async
+// (each lane copies exactly the words it later reads, so no warp barrier).
+// HBM traffic is the algorithmic N*M + K*M (+ N*K) per generation (each
+// pass > 0 re-reads the span's sources, from L2).
+//
+// Requirements (checked by the router): M % 4 == 0 and 4-byte aligned A / B
+// (AL8: M % 8 == 0 and 8-byte aligned, 8-byte copies and stores).
+#pragma once
+#include <cstdint>
+
+#include "gf_device.cuh"
+
+namespace gfr {
+
+constexpr int kTmW = 2;                         // words per lane per span
+constexpr int kTmSpanWords = 32 * kTmW;         // 64 words = 256 bytes per warp and packet
+constexpr int kTmKB = 32;                       // coded packets per pass
+constexpr int kTmGPB = 4;                       // groups per step
+constexpr int kTmRing = 4;                      // steps of source words in flight per warp
+constexpr int kTmColsPerWarp = kTmGPB * 16 * kTmW;   // 128
+
+struct TmParams {
+    const uint8_t *A;      // [batch][N][M]
+    const uint8_t *C;      // [batch][N][K]
+    uint8_t *B;            // [batch][K][M]
+    uint32_t Mw;           // 32-bit words per packet
+    uint32_t spans;        // ceil(Mw / 64)
+    int N, K;
+    int NG;                // groups, ceil(N w / 4) rounded up to kTmGPB
+    int passes;            // ceil(K / 32)
+    uint64_t units;        // batch * spans
+    uint64_t upw;          // units per warp
+};
+
+// sources per step (kTmGPB groups of 4 basis words, w basis words per source)
+__host__ __device__ constexpr int tm_sps(int logw) { return (4 * kTmGPB) >> logw; }
+
+// per-warp shared memory: TMEM addresses [passes][steps][kTmKB / 4][kTmGPB][4]
+// (one word per (pass, group, k)), then the source ring
+__host__ __device__ constexpr size_t tm_tab_bytes(int NG, int passes) { return (size_t)passes * NG * kTmKB * 4; }
+__host__ __device__ constexpr size_t tm_warp_bytes(int logw, int NG, int passes)
+{
+    return tm_tab_bytes(NG, passes) + (size_t)kTmRing * tm_sps(logw) * kTmSpanWords * 4;
+}
+
+// x * a on packed w-bit elements (bit j of an element = coefficient of x^j)
+template <int LOGW>
+__device__ __forceinline__ uint32_t tm_xtime(uint32_t a)
+{
+    if constexpr (LOGW == 1) {
+        return gf4_xtime(a);
+    } else if constexpr (LOGW == 2) {                         // x^4 + x + 1
+        const uint32_t h = (a >> 3) & 0x11111111u;
+        return ((a << 1) & 0xEEEEEEEEu) ^ (h * 3u);
+    } else {                                                  // x^8 + x^4 + x^3 + x + 1
+        const uint32_t h = (a >> 7) & 0x01010101u;
+        return ((a << 1) & 0xFEFEFEFEu) ^ (h * 0x1Bu);
+    }
+}
+
+#define TM_R8(v, o) "r"(v[o]), "r"(v[o + 1]), "r"(v[o + 2]), "r"(v[o + 3]), "r"(v[o + 4]), "r"(v[o + 5]), "r"(v[o + 6]), "r"(v[o + 7])
+__device__ __forceinline__ void tm_st32(uint32_t taddr, const uint32_t (&v)[32])
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+                 "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+                 :: "r"(taddr), TM_R8(v, 0), TM_R8(v, 8), TM_R8(v, 16), TM_R8(v, 24) : "memory");
+}
+#undef TM_R8
+
+__device__ __forceinline__ void tm_ld2(uint32_t taddr, uint32_t &x, uint32_t &y)
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(x), "=r"(y) : "r"(taddr));
+}
+
+// wait for this thread's outstanding tcgen05.ld; the loaded registers pass
+// through the asm so that no use of them is scheduled above the wait
+#define TM_P8(v, o) "+r"(v[o]), "+r"(v[o + 1]), "+r"(v[o + 2]), "+r"(v[o + 3]), "+r"(v[o + 4]), "+r"(v[o + 5]), "+r"(v[o + 6]), "+r"(v[o + 7])
+__device__ __forceinline__ void tm_wait_ld32(uint32_t (&v)[32])
+{
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : TM_P8(v, 0), TM_P8(v, 8), TM_P8(v, 16), TM_P8(v, 24) :: "memory");
+}
+#undef TM_P8
+
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+template <int BYTES>
+__device__ __forceinline__ void tm_cp_async(uint32_t sdst, const void *gsrc)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" :: "r"(sdst), "l"(gsrc), "n"(BYTES) : "memory");
+}
+__device__ __forceinline__ void tm_cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void tm_cp_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(kTmRing - 1) : "memory"); }
+
+// Grid: 1-D, WPC warps per block, one block per SM (TMEM: WPC / 4 x 128 columns).
+template <int LOGW, int WPC, bool AL8>
+__global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p)
+{
+    constexpr int w = 1 << LOGW;
+    constexpr int SPS = tm_sps(LOGW);
+    constexpr int SPG = SPS / kTmGPB > 0 ? SPS / kTmGPB : 1;      // sources per group (GF(256): 2 groups per source)
+    static_assert((WPC / 4) * kTmColsPerWarp <= 512, "TMEM columns");
+    constexpr uint32_t kCols = (WPC / 4) * kTmColsPerWarp <= 128 ? 128 : (WPC / 4) * kTmColsPerWarp <= 256 ? 256 : 512;
+    extern __shared__ __align__(16) uint8_t smem8[];
+    __shared__ uint32_t s_tbase;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (wid == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     :: "r"((uint32_t)__cvta_generic_to_shared(&s_tbase)), "n"(kCols) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // this warp's TMEM: lanes 32 (wid % 4) .., columns (wid / 4) * 128 ..
+    const uint32_t tb = s_tbase + ((uint32_t)(32 * (wid & 3)) << 16) + (uint32_t)(wid >> 2) * kTmColsPerWarp;
+
+    const int N = p.N, K = p.K, NG = p.NG, passes = p.passes, steps = NG / kTmGPB;
+    const uint32_t Mw = p.Mw, spans = p.spans;
+    const size_t tabb = tm_tab_bytes(NG, passes);
+    uint32_t *tab = reinterpret_cast<uint32_t *>(smem8 + (size_t)wid * tm_warp_bytes(LOGW, NG, passes));
+    const uint32_t *ring = reinterpret_cast<const uint32_t *>(smem8 + (size_t)wid * tm_warp_bytes(LOGW, NG, passes) + tabb);
+    const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+
+    const uint64_t u0 = ((uint64_t)blockIdx.x * WPC + wid) * p.upw;
+    const uint64_t u1 = u0 + p.upw < p.units ? u0 + p.upw : p.units;
+    const int64_t T = u0 < u1 ? (int64_t)(u1 - u0) * passes * steps : 0;
+
+    // Step cursors (no divisions in the loop): a step is (unit, pass, group
+    // step gs); unit = (generation g, span sp).  The producer runs
+    // kTmRing - 1 steps ahead of the consumer.
+    struct Cur {
+        uint64_t g; uint32_t sp; int pass, gs; int64_t t;
+    };
+    auto advance = [&](Cur &c) {
+        c.t++;
+        if (++c.gs == steps) {
+            c.gs = 0;
+            if (++c.pass == passes) {
+                c.pass = 0;
+                if (++c.sp == spans) { c.sp = 0; c.g++; }
+            }
+        }
+    };
+    Cur pc{u0 / spans, (uint32_t)(u0 % spans), 0, 0, 0};
+    Cur cc = pc;
+    // producer: row pointer of the step's first source at this lane's words
+    // (lanes past the packet end read word 0 and never store)
+    const uint32_t *A32 = reinterpret_cast<const uint32_t *>(p.A);
+    auto row0 = [&](const Cur &c) -> const uint32_t * {
+        const uint32_t wi = c.sp * kTmSpanWords + 2 * lane;
+        return A32 + c.g * (uint64_t)N * Mw + (wi < Mw ? wi : 0u);
+    };
+    const uint32_t *prow = row0(pc);
+    const bool full_steps = (N % SPS) == 0;
+    auto issue = [&]() {
+        if (pc.t < T) {
+            const uint32_t d0 = ring_s + ((uint32_t)(pc.t % kTmRing) * SPS * kTmSpanWords + 2 * lane) * 4u;
+            const bool odd_ok = AL8 || pc.sp * kTmSpanWords + 2 * lane + 1 < Mw;
+#pragma unroll
+            for (int s = 0; s < SPS; s++) {
+                // sources >= N (a partial last step) re-read the step's first
+                // row: their coefficients are zero, any value gives zero terms
+                const uint32_t *r = (full_steps || pc.gs * SPS + s < N) ? prow + (size_t)s * Mw : prow;
+                if constexpr (AL8) {
+                    tm_cp_async<8>(d0 + s * kTmSpanWords * 4, r);
+                } else {
+                    tm_cp_async<4>(d0 + s * kTmSpanWords * 4, r);
+                    tm_cp_async<4>(d0 + s * kTmSpanWords * 4 + 4, odd_ok ? r + 1 : r);
+                }
+            }
+            const int gs0 = pc.gs;
+            advance(pc);
+            if (pc.gs == 0 || gs0 + 1 != pc.gs) prow = row0(pc);
+            else prow += (size_t)SPS * Mw;
+        }
+        tm_cp_commit();
+    };
+
+#pragma unroll 1
+    for (int t = 0; t < kTmRing - 1; t++) issue();
+
+    uint64_t cur_g = ~0ull;
+    uint32_t acc[kTmKB][2];
+#pragma unroll
+    for (int k = 0; k < kTmKB; k++) acc[k][0] = acc[k][1] = 0u;
+
+#pragma unroll 1
+    for (int64_t t = 0; t < T; t++) {
+        issue();
+        const uint64_t g = cc.g;
+        const int pass = cc.pass, gs = cc.gs;
+        if (g != cur_g) {                            // this warp's TMEM lookup addresses for generation g
+            cur_g = g;
+            const uint8_t *Cg = p.C + g * (size_t)N * K;
+            __syncwarp();
+            for (int e = lane; e < (int)(tabb / 4); e += 32) {
+                // e = (((ps * steps + st) * 8 + kq) * kTmGPB + sl) * 4 + kk
+                const int kk = e & 3, sl = (e >> 2) & (kTmGPB - 1), kq = (e >> 4) & 7;
+                const int pst = e >> 7, st = pst % steps, ps = pst / steps;
+                const int k = ps * kTmKB + kq * 4 + kk, grp = st * kTmGPB + sl;
+                uint32_t idx = 0;
+                if (k < K) {
+#pragma unroll
+                    for (int b = 0; b < 4; b++) {
+                        const int tt = 4 * grp + b, i = tt >> LOGW, j = tt & (w - 1);
+                        if (i < N) idx |= ((__ldg(Cg + (size_t)i * K + k) >> j) & 1u) << b;
+                    }
+                }
+                tab[e] = tb + (uint32_t)sl * (16 * kTmW) + idx * kTmW;
+            }
+            __syncwarp();
+        }
+        tm_cp_wait();                                // stage t has landed (this lane's own copies)
+        const uint32_t *rs = ring + (size_t)(t % kTmRing) * SPS * kTmSpanWords + 2 * lane;
+        uint32_t hi4[SPG][2];                        // GF(256): x^4 a of the step's sources
+        (void)hi4;
+#pragma unroll
+        for (int sl = 0; sl < kTmGPB; sl++) {
+            uint32_t e[4][2];
+#pragma unroll
+            for (int wd = 0; wd < 2; wd++) {
+                if constexpr (LOGW == 0) {
+#pragma unroll
+                    for (int b = 0; b < 4; b++) e[b][wd] = rs[(sl * 4 + b) * kTmSpanWords + wd];
+                } else if constexpr (LOGW == 1) {
+                    const uint32_t a = rs[(sl * 2) * kTmSpanWords + wd], c = rs[(sl * 2 + 1) * kTmSpanWords + wd];
+                    e[0][wd] = a; e[1][wd] = tm_xtime<1>(a); e[2][wd] = c; e[3][wd] = tm_xtime<1>(c);
+                } else if constexpr (LOGW == 2) {
+                    const uint32_t a = rs[sl * kTmSpanWords + wd];
+                    e[0][wd] = a; e[1][wd] = tm_xtime<2>(a); e[2][wd] = tm_xtime<2>(e[1][wd]);
+                    e[3][wd] = tm_xtime<2>(e[2][wd]);
+                } else {
+                    const uint32_t a = (sl & 1) ? tm_xtime<3>(hi4[0][wd]) : rs[(sl >> 1) * kTmSpanWords + wd];
+                    e[0][wd] = a; e[1][wd] = tm_xtime<3>(a); e[2][wd] = tm_xtime<3>(e[1][wd]);
+                    e[3][wd] = tm_xtime<3>(e[2][wd]);
+                    if (!(sl & 1)) hi4[0][wd] = e[3][wd];     // x^3 a; x^4 a = x * that
+                }
+            }
+            uint32_t v[32];
+#pragma unroll
+            for (int wd = 0; wd < 2; wd++) {
+                v[0 + wd] = 0u;
+                v[2 + wd] = e[0][wd];
+                v[4 + wd] = e[1][wd];
+                v[6 + wd] = e[0][wd] ^ e[1][wd];
+#pragma unroll
+                for (int c = 4; c < 8; c++) v[2 * c + wd] = e[2][wd] ^ v[2 * (c - 4) + wd];
+#pragma unroll
+                for (int c = 8; c < 16; c++) v[2 * c + wd] = e[3][wd] ^ v[2 * (c - 8) + wd];
+            }
+            tm_st32(tb + (uint32_t)sl * (16 * kTmW), v);
+        }
+        tm_wait_st();
+        const uint4 *ta = reinterpret_cast<const uint4 *>(tab + ((size_t)pass * steps + gs) * (kTmKB * kTmGPB));
+#pragma unroll
+        for (int kq = 0; kq < kTmKB / 4; kq++) {
+            uint32_t r[32];
+#pragma unroll
+            for (int sl = 0; sl < kTmGPB; sl++) {
+                const uint4 a = ta[kq * kTmGPB + sl];     // addresses of k = 4 kq .. 4 kq + 3
+                const uint32_t aw[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+                for (int kk = 0; kk < 4; kk++) tm_ld2(aw[kk], r[(kk * 4 + sl) * 2], r[(kk * 4 + sl) * 2 + 1]);
+            }
+            tm_wait_ld32(r);
+#pragma unroll
+            for (int kk = 0; kk < 4; kk++)
+#pragma unroll
+                for (int wd = 0; wd < 2; wd++) {
+                    const uint32_t x = acc[kq * 4 + kk][wd] ^ r[(kk * 4) * 2 + wd] ^ r[(kk * 4 + 1) * 2 + wd];
+                    acc[kq * 4 + kk][wd] = x ^ r[(kk * 4 + 2) * 2 + wd] ^ r[(kk * 4 + 3) * 2 + wd];
+                }
+        }
+        if (gs == steps - 1) {                       // the pass is complete: store and reset
+            const uint32_t wi = cc.sp * kTmSpanWords + 2 * lane;
+            uint32_t *Bg = reinterpret_cast<uint32_t *>(p.B) + (g * K + (size_t)pass * kTmKB) * Mw + wi;
+            const int kn = K - pass * kTmKB;
+#pragma unroll
+            for (int k = 0; k < kTmKB; k++) {
+                if (k < kn) {
+                    if constexpr (AL8) {
+                        if (wi < Mw)
+                            asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};"
+                                         :: "l"(Bg + (size_t)k * Mw), "r"(acc[k][0]), "r"(acc[k][1]) : "memory");
+                    } else {
+                        if (wi < Mw) Bg[(size_t)k * Mw] = acc[k][0];
+                        if (wi + 1 < Mw) Bg[(size_t)k * Mw + 1] = acc[k][1];
+                    }
+                }
+                acc[k][0] = acc[k][1] = 0u;
+            }
+        }
+        advance(cc);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (wid == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(s_tbase), "n"(kCols) : "memory");
+}
+
+}  // namespace gfr

@@ -16,6 +16,7 @@
 #include "encode_prow16.cuh"
 #include "encode_stream.cuh"
 #include "encode_gf2.cuh"
+#include "encode_tmem.cuh"
 #include "decode_kernels.cuh"
 #include "region_kernels.cuh"
 #include "rng_kernels.cuh"
@@ -24,7 +25,7 @@
 namespace gfr {
 
 constexpr int kMaxDevices = 64;
-constexpr int kVersion = 200;   // 0.2.00: GF(2) split engine, kernels configured in gf_init
+constexpr int kVersion = 201;   // 0.2.01: TMEM lookup-table engine for GF(2) / GF(4)
 
 __device__ uint32_t g_dev_tabs[4][256 * kTableWords];
 __device__ uint8_t g_dev_inv[4][256];
@@ -472,6 +473,51 @@ static int launch_gf2(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int
     return GF_OK;
 }
 
+// TMEM lookup-table engine (encode_tmem.cuh): 4-bit groups of the basis words
+// x^j a_i, their 16 XOR-subsets in tensor memory, one lookup per (group, k).
+// Warps per CTA: 12 for GF(4) (C5: 1.75 vs 1.57 TB/s at 8), 8 otherwise
+// (GF(2) C5: 2.60 vs 2.43 at 12; tools/exp_tmem.cu, profiles/r02_exp_tmem_v3.txt).
+template <int LOGW>
+constexpr int tm_wpc() { return LOGW == 1 ? 12 : 8; }
+
+static int tm_groups(int logw, int N) { return ((((N << logw) + 3) / 4) + kTmGPB - 1) / kTmGPB * kTmGPB; }
+
+static size_t tm_smem(int logw, int N, int K)
+{
+    const int wpc = logw == 1 ? tm_wpc<1>() : tm_wpc<0>();
+    return (size_t)wpc * tm_warp_bytes(logw, tm_groups(logw, N), (K + kTmKB - 1) / kTmKB);
+}
+
+static constexpr int log2_field(int field) { return field == 2 ? 0 : field == 4 ? 1 : field == 16 ? 2 : 3; }
+
+static bool tmem_ok(int field, int N, int K, size_t M, const void *A, const void *B)
+{
+    return M % 8 == 0 && M / 4 < 0xFFFFFFFFull && ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 7u) == 0 &&
+           tm_smem(log2_field(field), N, K) <= 226 * 1024;
+}
+
+template <int LOGW>
+static int launch_tmem(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M, size_t batch,
+                       cudaStream_t st)
+{
+    constexpr int WPC = tm_wpc<LOGW>();
+    int dev;
+    if (current_device(&dev) != GF_OK) return GF_ECUDA;
+    TmParams p{};
+    p.A = A; p.C = C; p.B = B; p.N = N; p.K = K;
+    p.Mw = (uint32_t)(M / 4);
+    p.spans = (p.Mw + kTmSpanWords - 1) / kTmSpanWords;
+    p.NG = tm_groups(LOGW, N);
+    p.passes = (K + kTmKB - 1) / kTmKB;
+    p.units = (uint64_t)batch * p.spans;
+    const uint64_t warps = (uint64_t)(g_sm_count[dev] > 0 ? g_sm_count[dev] : 148) * WPC;
+    p.upw = (p.units + warps - 1) / warps;
+    const uint64_t blocks = (p.units + WPC * p.upw - 1) / (WPC * p.upw);
+    const size_t smem = tm_smem(LOGW, N, K);
+    encode_tmem_kernel<LOGW, WPC, true><<<(unsigned)blocks, WPC * 32, smem, st>>>(p);
+    return launch_status();
+}
+
 // Harness override of the encode kernel (gf_set_encode_path, thread-local).
 // Stream sub-layout codes force the streaming kernel.
 static int encode_path_override()
@@ -485,20 +531,26 @@ static int encode_path_override()
 // product-row with 64 / 32 / 16 coded packets per CTA, 8 streaming (K <= 4),
 // 11 GF(2) split engine (N <= 32, 16-byte aligned packets, K >= 24; any K when forced),
 // 12 GF(16) product-row with nibble-indexed tables (K > 32), 13 GF(256)
-// product-row with 32 coded packets per CTA on 768-word tiles (K > 32, long packets)
+// product-row with 32 coded packets per CTA on 768-word tiles (K > 32, long packets),
+// 14 TMEM lookup-table engine (GF(2) / GF(4), K >= 24, packets >= 4 KiB, 8-byte aligned)
 static bool gf2_split_ok(int field, int N, int K, size_t M, const void *A, const void *B)
 {
     return field == 2 && N <= 32 && K >= 1 && M % 16 == 0 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0 &&
            (reinterpret_cast<uintptr_t>(B) & 15u) == 0 && gf2_smem_bytes(K, 32) <= 227 * 1024;
 }
 
-static int encode_path(int field, int N, int K, size_t M, const void *A, const void *B)
+static int encode_path(int field, int N, int K, size_t M, const void *A, const void *B, bool tmem = true)
 {
     const bool aligned = M % 4 == 0 && (reinterpret_cast<uintptr_t>(A) & 3u) == 0 &&
                          (reinterpret_cast<uintptr_t>(B) & 3u) == 0 && M / 4 < 0xFFFFFFFFull;
     const int ov = encode_path_override();
     if (!aligned) return 1;
     if (K <= 4 && (ov == GF_PATH_STREAM || ov == 0)) return 8;  // streaming (16- or 4-byte chunks)
+    // GF(2) / GF(4), K >= 24, long packets: the TMEM lookup-table engine
+    // (C5: GF(2) 2.29 -> 2.60 TB/s against the split engine, GF(4) 1.13 -> 1.75
+    // against lane-k; forced: any field and shape it takes)
+    if (tmem && ov == GF_PATH_TMEM && tmem_ok(field, N, K, M, A, B)) return 14;
+    if (tmem && ov == 0 && field <= 4 && K >= 24 && M >= 4096 && tmem_ok(field, N, K, M, A, B)) return 14;
     // GF(2): the split engine (encode_gf2.cuh) where the lane-k kernel ran
     // before, K >= 24 (C5 N = K = 32, 1 MiB: 2.21 vs 1.66 TB/s)
     if (ov == GF_PATH_GF2 && gf2_split_ok(field, N, K, M, A, B)) return 11;
@@ -530,6 +582,14 @@ static int encode_on_stream(int field, int fi, const uint8_t *A, const uint8_t *
         const int path = encode_path(field, N, K, M, A, B);
         if (path == 8) return launch_stream(field, fi, A, C, B, N, K, M, batch, st);
         if (path == 12) return launch_prow16(A, C, B, N, K, M, batch, st);
+        if (path == 14) {
+            switch (field) {
+            case 2: return launch_tmem<0>(A, C, B, N, K, M, batch, st);
+            case 4: return launch_tmem<1>(A, C, B, N, K, M, batch, st);
+            case 16: return launch_tmem<2>(A, C, B, N, K, M, batch, st);
+            default: return launch_tmem<3>(A, C, B, N, K, M, batch, st);
+            }
+        }
         if (path == 11) return N <= 16 ? launch_gf2<16>(A, C, B, N, K, M, batch, st)
                                        : launch_gf2<32>(A, C, B, N, K, M, batch, st);
         if (path == 6 || path == 9 || path == 10 || path == 13) {
@@ -714,6 +774,7 @@ static int configure_field(int optin, uint32_t smem_base)
         if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<32, true, 2, true>, optin);
         if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<32, false, 2, true>, optin);
     }
+    if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<log2_field(F), tm_wpc<log2_field(F)>(), true>, optin);
     if (rc == GF_OK) rc = allow_smem(invert_warp_kernel, optin);
     if (rc == GF_OK) rc = allow_smem(invert_kernel, optin);
     return rc;
@@ -766,7 +827,7 @@ const char *gf_strerror(int status)
 
 int gf_set_encode_path(int path)
 {
-    if (path < 0 || path > GF_PATH_STREAM_WIDE4 || path == 3 || path == 5) return GF_EARG;
+    if (path < 0 || path > GF_PATH_TMEM || path == 3 || path == 5) return GF_EARG;
     tls_path = path;
     return GF_OK;
 }
@@ -1066,7 +1127,8 @@ int gf_encode_verify_batch(int field, const uint8_t *A, const uint8_t *C, uint8_
     verify_prep_kernel<<<(unsigned)batch, 128, 8 * (size_t)kw, st>>>(C, R, U, RB, N, K, t, kblocks, kw, batch,
                                                                       field - 1);
     if ((rc = launch_status()) != GF_OK) return rc;
-    const int path = encode_path(field, N, K, M, A, B);
+    // (the TMEM engine has no fused check: its shapes take the fused kernels below)
+    const int path = encode_path(field, N, K, M, A, B, false);
     // The GF(2) split engine (HBM-bound: a second pass over A and B would double
     // its traffic) checks inside the encode.  Every other kernel -- the
     // shared-memory-bound product-row kernels among them, which leave most of

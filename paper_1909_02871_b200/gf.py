@@ -89,13 +89,13 @@ def version() -> int:
 
 ENCODE_PATHS = {0: "column-words", 1: "column-bytes", 2: "lanek-32", 3: "lanek-64", 6: "prow", 8: "stream",
                 9: "prow-32", 10: "prow-16", 11: "gf2-split", 12: "prow-nib",
-                13: "prow-32w"}
+                13: "prow-32w", 14: "tmem"}
 
 
 # gf_set_encode_path codes (include/gfrlnc.h GF_PATH_*)
 FORCE_PATHS = {"auto": 0, "column": 1, "lanek": 2, "prow": 4, "stream": 6, "gf2": 7,
                "stream-strided4": 8, "stream-strided8": 9, "stream-strided12": 10,
-               "stream-wide2": 11, "stream-wide4": 12}
+               "stream-wide2": 11, "stream-wide4": 12, "tmem": 13}
 
 
 def set_encode_path(name: str) -> None:

@@ -238,12 +238,19 @@ def test_encode_path_query():
     assert gf.encode_path(4, 32, 12, 1500) == "column-words"
     assert gf.encode_path(2, 32, 20, 4096) == "column-words"
     assert gf.encode_path(4, 64, 64, 1500) == "lanek-64"
-    assert gf.encode_path(2, 32, 32, 1 << 20) == "gf2-split"    # C5 GF(2)
-    assert gf.encode_path(4, 32, 32, 1 << 20) == "lanek-32"     # C5 GF(4)
-    assert gf.encode_path(2, 33, 32, 1 << 20) == "lanek-32"     # GF(2), N > 32
+    assert gf.encode_path(2, 32, 32, 1 << 20) == "tmem"         # C5 GF(2): TMEM lookup tables
+    assert gf.encode_path(4, 32, 32, 1 << 20) == "tmem"         # C5 GF(4)
+    assert gf.encode_path(2, 33, 32, 1 << 20) == "tmem"         # GF(2), N > 32
+    assert gf.encode_path(4, 32, 32, 1 << 20, a_align=4) == "lanek-32"   # TMEM engine: 8-byte aligned
+    assert gf.encode_path(4, 32, 32, 4096 + 4) == "lanek-32"    # ... and M % 8 == 0
+    assert gf.encode_path(2, 32, 32, 2048) == "gf2-split"       # M < 4096: the split engine
+    assert gf.encode_path(2, 33, 32, 2048) == "lanek-32"        # GF(2), N > 32, short packets
+    assert gf.encode_path(4, 32, 16, 1 << 20) == "prow-16"      # K < 24
+    assert gf.encode_path(16, 32, 32, 1 << 20) == "prow-32"     # GF(16)/GF(256) keep the product rows
     assert gf.encode_path(2, 32, 32, 1500) == "lanek-32"        # GF(2), M % 16 != 0
     assert gf.encode_path(2, 32, 32, 4096, a_align=4) == "lanek-32"
-    assert gf.encode_path(2, 16, 24, 4096) == "gf2-split"
+    assert gf.encode_path(2, 16, 24, 2048) == "gf2-split"
+    assert gf.encode_path(2, 16, 24, 4096) == "tmem"
     assert gf.encode_path(256, 16, 1, 1024) == "stream"         # NEXT-2 (paper: N = 16, K = 1)
     assert gf.encode_path(2, 16, 4, 65536) == "stream"
     assert gf.encode_path(256, 16, 1, 1024, a_align=4) == "stream"    # 4-byte chunks
