@@ -203,8 +203,8 @@ int gf_host_tables(int field, uint32_t *out, size_t cap_words);
  * 12 = GF(16) product-row kernel with nibble-indexed tables (K > 32: C3 GF(16)),
  * 13 = GF(256) product-row kernel with 32 coded packets per CTA on 768-word
  * tiles (K > 32, packets of >= 6144 words tiled >= 90%: C4)
- * 14 = TMEM lookup-table engine (GF(2) / GF(4), K >= 24, M >= 4096, M % 8 == 0,
- * 8-byte aligned A and B: C5)
+ * 14 = TMEM lookup-table engine (GF(2) / GF(4), K >= 24, M >= 4096, M % 16 == 0,
+ * 16-byte aligned A and B: C5)
  * (DESIGN.md section 6), or GF_EFIELD / GF_EARG. */
 int gf_encode_path(int field, int N, int K, size_t M, size_t a_align, size_t b_align);
 
@@ -225,7 +225,7 @@ enum {
     GF_PATH_STREAM_STRIDED12 = 10,   /* ... 12-word blocks                      */
     GF_PATH_STREAM_WIDE2 = 11,       /* streaming, two 16-byte chunks per thread at any packet size */
     GF_PATH_STREAM_WIDE4 = 12,       /* streaming, four 16-byte chunks per thread                   */
-    GF_PATH_TMEM = 13                /* TMEM lookup-table engine (any field; M % 8 == 0, 8-byte aligned) */
+    GF_PATH_TMEM = 13                /* TMEM lookup-table engine (any field; M % 16 == 0, 16-byte aligned) */
 };
 int gf_set_encode_path(int path);
 

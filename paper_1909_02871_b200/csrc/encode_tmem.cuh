@@ -34,14 +34,19 @@
 // tcgen05.ld.32x32b.x2 results into its accumulator (one LOP3 per word).
 // The TMEM column addresses of every (pass, group, k) are precomputed per
 // warp and generation in shared memory and read with broadcast LDS.128.
-// Source words stream through a per-warp ring of kTmRing steps with cp.async
-// (each lane copies exactly the words it later reads, so no warp barrier).
+// Source words stream through a per-warp ring of kTmRing steps: one lane
+// issues one TMA tile load per step (2-D tensor map over A viewed as
+// [batch N rows][M bytes], box SPS rows x 256 bytes), completing on the
+// stage's mbarrier; rows and bytes past the end of A are zero-filled.
 // HBM traffic is the algorithmic N*M + K*M (+ N*K) per generation (each
 // pass > 0 re-reads the span's sources, from L2).
 //
-// Requirements (checked by the router): M % 4 == 0 and 4-byte aligned A / B
-// (AL8: M % 8 == 0 and 8-byte aligned, 8-byte copies and stores).
+// Requirements (checked by the router): M % 16 == 0, 16-byte aligned A and B.
 #pragma once
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
 #include <cstdint>
 
 #include "gf_device.cuh"
@@ -72,11 +77,13 @@ struct TmParams {
 __host__ __device__ constexpr int tm_sps(int logw) { return (4 * kTmGPB) >> logw; }
 
 // per-warp shared memory: TMEM addresses [passes][steps][kTmKB / 4][kTmGPB][4]
-// (one word per (pass, group, k)), then the source ring
+// (one word per (pass, group, k)), then the source ring, then one mbarrier
+// per ring stage
 __host__ __device__ constexpr size_t tm_tab_bytes(int NG, int passes) { return (size_t)passes * NG * kTmKB * 4; }
 __host__ __device__ constexpr size_t tm_warp_bytes(int logw, int NG, int passes)
 {
-    return tm_tab_bytes(NG, passes) + (size_t)kTmRing * tm_sps(logw) * kTmSpanWords * 4;
+    // (a multiple of 128 bytes: TMA destinations are 128-byte aligned)
+    return (tm_tab_bytes(NG, passes) + (size_t)kTmRing * tm_sps(logw) * kTmSpanWords * 4 + kTmRing * 8 + 127) / 128 * 128;
 }
 
 // x * a on packed w-bit elements (bit j of an element = coefficient of x^j)
@@ -120,24 +127,52 @@ __device__ __forceinline__ void tm_wait_ld32(uint32_t (&v)[32])
 
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-template <int BYTES>
-__device__ __forceinline__ void tm_cp_async(uint32_t sdst, const void *gsrc)
+// one TMA tile load (box SPS rows x 256 bytes at byte x, row y of A) into
+// shared memory, completing its bytes on an mbarrier
+__device__ __forceinline__ void tm_tma_load(uint32_t sdst, const CUtensorMap *map, uint32_t x, uint32_t y, uint32_t bar)
 {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" :: "r"(sdst), "l"(gsrc), "n"(BYTES) : "memory");
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                 :: "r"(sdst), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar) : "memory");
 }
-__device__ __forceinline__ void tm_cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void tm_cp_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(kTmRing - 1) : "memory"); }
+
+// Host: the tensor map of A for the kernel's source ring (2-D: M bytes per
+// row, batch * N rows of stride M; box 256 bytes x SPS rows).  M % 16 == 0
+// and 16-byte aligned A (TMA's stride / address rules).  Returns false when
+// the driver entry point is missing or the encode fails.
+static inline bool tm_make_map(CUtensorMap *map, const void *A, uint64_t rows, uint64_t M, int logw)
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !f)
+            return false;
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }
+    const cuuint64_t dims[2] = {M, rows};
+    const cuuint64_t strides[1] = {M};
+    const cuuint32_t box[2] = {(cuuint32_t)(kTmSpanWords * 4), (cuuint32_t)tm_sps(logw)};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(A), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+__device__ __forceinline__ void tm_expect_tx(uint32_t bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
+}
 
 // Grid: 1-D, WPC warps per block, one block per SM (TMEM: WPC / 4 x 128 columns).
-template <int LOGW, int WPC, bool AL8>
-__global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p)
+template <int LOGW, int WPC>
+__global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, const __grid_constant__ CUtensorMap tmA)
 {
     constexpr int w = 1 << LOGW;
     constexpr int SPS = tm_sps(LOGW);
     constexpr int SPG = SPS / kTmGPB > 0 ? SPS / kTmGPB : 1;      // sources per group (GF(256): 2 groups per source)
     static_assert((WPC / 4) * kTmColsPerWarp <= 512, "TMEM columns");
     constexpr uint32_t kCols = (WPC / 4) * kTmColsPerWarp <= 128 ? 128 : (WPC / 4) * kTmColsPerWarp <= 256 ? 256 : 512;
-    extern __shared__ __align__(16) uint8_t smem8[];
+    extern __shared__ __align__(1024) uint8_t smem8[];
     __shared__ uint32_t s_tbase;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (wid == 0) {
@@ -157,6 +192,10 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p)
     uint32_t *tab = reinterpret_cast<uint32_t *>(smem8 + (size_t)wid * tm_warp_bytes(LOGW, NG, passes));
     const uint32_t *ring = reinterpret_cast<const uint32_t *>(smem8 + (size_t)wid * tm_warp_bytes(LOGW, NG, passes) + tabb);
     const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+    const uint32_t bar_s = ring_s + kTmRing * SPS * kTmSpanWords * 4;
+    if (lane < kTmRing) mbar_init(bar_s + 8 * lane, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
 
     const uint64_t u0 = ((uint64_t)blockIdx.x * WPC + wid) * p.upw;
     const uint64_t u1 = u0 + p.upw < p.units ? u0 + p.upw : p.units;
@@ -180,37 +219,20 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p)
     };
     Cur pc{u0 / spans, (uint32_t)(u0 % spans), 0, 0, 0};
     Cur cc = pc;
-    // producer: row pointer of the step's first source at this lane's words
-    // (lanes past the packet end read word 0 and never store)
-    const uint32_t *A32 = reinterpret_cast<const uint32_t *>(p.A);
-    auto row0 = [&](const Cur &c) -> const uint32_t * {
-        const uint32_t wi = c.sp * kTmSpanWords + 2 * lane;
-        return A32 + c.g * (uint64_t)N * Mw + (wi < Mw ? wi : 0u);
-    };
-    const uint32_t *prow = row0(pc);
-    const bool full_steps = (N % SPS) == 0;
+    // producer: one TMA tile load per step, rows g N + gs SPS .. + SPS - 1,
+    // bytes sp * 256 .. + 255 (rows past the generation's N belong to the next
+    // one or lie past the end of A, and only meet zero coefficients; bytes past
+    // the packet end belong to lanes that never store)
     auto issue = [&]() {
         if (pc.t < T) {
-            const uint32_t d0 = ring_s + ((uint32_t)(pc.t % kTmRing) * SPS * kTmSpanWords + 2 * lane) * 4u;
-            const bool odd_ok = AL8 || pc.sp * kTmSpanWords + 2 * lane + 1 < Mw;
-#pragma unroll
-            for (int s = 0; s < SPS; s++) {
-                // sources >= N (a partial last step) re-read the step's first
-                // row: their coefficients are zero, any value gives zero terms
-                const uint32_t *r = (full_steps || pc.gs * SPS + s < N) ? prow + (size_t)s * Mw : prow;
-                if constexpr (AL8) {
-                    tm_cp_async<8>(d0 + s * kTmSpanWords * 4, r);
-                } else {
-                    tm_cp_async<4>(d0 + s * kTmSpanWords * 4, r);
-                    tm_cp_async<4>(d0 + s * kTmSpanWords * 4 + 4, odd_ok ? r + 1 : r);
-                }
+            if (lane == 0) {
+                const uint32_t st = (uint32_t)(pc.t % kTmRing);
+                tm_expect_tx(bar_s + 8 * st, SPS * kTmSpanWords * 4u);
+                tm_tma_load(ring_s + st * (SPS * kTmSpanWords * 4u), &tmA, pc.sp * (kTmSpanWords * 4u),
+                            (uint32_t)(pc.g * N) + (uint32_t)(pc.gs * SPS), bar_s + 8 * st);
             }
-            const int gs0 = pc.gs;
             advance(pc);
-            if (pc.gs == 0 || gs0 + 1 != pc.gs) prow = row0(pc);
-            else prow += (size_t)SPS * Mw;
         }
-        tm_cp_commit();
     };
 
 #pragma unroll 1
@@ -223,6 +245,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p)
 
 #pragma unroll 1
     for (int64_t t = 0; t < T; t++) {
+        __syncwarp();                                // every lane is done with the stage issue() refills
         issue();
         const uint64_t g = cc.g;
         const int pass = cc.pass, gs = cc.gs;
@@ -247,7 +270,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p)
             }
             __syncwarp();
         }
-        tm_cp_wait();                                // stage t has landed (this lane's own copies)
+        mbar_wait(bar_s + 8 * (uint32_t)(t % kTmRing), (uint32_t)(t / kTmRing) & 1u);   // stage t has landed
         const uint32_t *rs = ring + (size_t)(t % kTmRing) * SPS * kTmSpanWords + 2 * lane;
         uint32_t hi4[SPG][2];                        // GF(256): x^4 a of the step's sources
         (void)hi4;
@@ -315,21 +338,15 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p)
 #pragma unroll
             for (int k = 0; k < kTmKB; k++) {
                 if (k < kn) {
-                    if constexpr (AL8) {
-                        if (wi < Mw)
-                            asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};"
-                                         :: "l"(Bg + (size_t)k * Mw), "r"(acc[k][0]), "r"(acc[k][1]) : "memory");
-                    } else {
-                        if (wi < Mw) Bg[(size_t)k * Mw] = acc[k][0];
-                        if (wi + 1 < Mw) Bg[(size_t)k * Mw + 1] = acc[k][1];
-                    }
+                    if (wi < Mw)
+                        asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};"
+                                     :: "l"(Bg + (size_t)k * Mw), "r"(acc[k][0]), "r"(acc[k][1]) : "memory");
                 }
                 acc[k][0] = acc[k][1] = 0u;
             }
         }
         advance(cc);
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");

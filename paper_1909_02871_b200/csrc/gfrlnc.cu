@@ -475,10 +475,10 @@ static int launch_gf2(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int
 
 // TMEM lookup-table engine (encode_tmem.cuh): 4-bit groups of the basis words
 // x^j a_i, their 16 XOR-subsets in tensor memory, one lookup per (group, k).
-// Warps per CTA: 12 for GF(4) (C5: 1.75 vs 1.57 TB/s at 8), 8 otherwise
-// (GF(2) C5: 2.60 vs 2.43 at 12; tools/exp_tmem.cu, profiles/r02_exp_tmem_v3.txt).
+// Warps per CTA: 16 for GF(4) (C5: 1.83 vs 1.77 TB/s at 12, 1.50 at 8), 8 otherwise
+// (GF(2) C5: 2.71 TB/s at 8 and 12; tools/exp_tmem.cu, profiles/r02_exp_tmem_v5.txt).
 template <int LOGW>
-constexpr int tm_wpc() { return LOGW == 1 ? 12 : 8; }
+constexpr int tm_wpc() { return LOGW == 1 ? 16 : 8; }
 
 static int tm_groups(int logw, int N) { return ((((N << logw) + 3) / 4) + kTmGPB - 1) / kTmGPB * kTmGPB; }
 
@@ -492,7 +492,7 @@ static constexpr int log2_field(int field) { return field == 2 ? 0 : field == 4 
 
 static bool tmem_ok(int field, int N, int K, size_t M, const void *A, const void *B)
 {
-    return M % 8 == 0 && M / 4 < 0xFFFFFFFFull && ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 7u) == 0 &&
+    return M % 16 == 0 && M / 4 < 0xFFFFFFFFull && N * K > 0 && ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15u) == 0 &&
            tm_smem(log2_field(field), N, K) <= 226 * 1024;
 }
 
@@ -503,19 +503,28 @@ static int launch_tmem(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, in
     constexpr int WPC = tm_wpc<LOGW>();
     int dev;
     if (current_device(&dev) != GF_OK) return GF_ECUDA;
-    TmParams p{};
-    p.A = A; p.C = C; p.B = B; p.N = N; p.K = K;
-    p.Mw = (uint32_t)(M / 4);
-    p.spans = (p.Mw + kTmSpanWords - 1) / kTmSpanWords;
-    p.NG = tm_groups(LOGW, N);
-    p.passes = (K + kTmKB - 1) / kTmKB;
-    p.units = (uint64_t)batch * p.spans;
-    const uint64_t warps = (uint64_t)(g_sm_count[dev] > 0 ? g_sm_count[dev] : 148) * WPC;
-    p.upw = (p.units + warps - 1) / warps;
-    const uint64_t blocks = (p.units + WPC * p.upw - 1) / (WPC * p.upw);
-    const size_t smem = tm_smem(LOGW, N, K);
-    encode_tmem_kernel<LOGW, WPC, true><<<(unsigned)blocks, WPC * 32, smem, st>>>(p);
-    return launch_status();
+    // TMA row coordinates are 32-bit signed: at most 2^31 - 1 rows of A per launch
+    const size_t gmax = (size_t)0x7FFFFFFF / (size_t)N;
+    for (size_t g0 = 0; g0 < batch; g0 += gmax) {
+        const size_t nb = batch - g0 < gmax ? batch - g0 : gmax;
+        TmParams p{};
+        p.A = A + g0 * N * M; p.C = C + g0 * N * K; p.B = B + g0 * K * M; p.N = N; p.K = K;
+        p.Mw = (uint32_t)(M / 4);
+        p.spans = (p.Mw + kTmSpanWords - 1) / kTmSpanWords;
+        p.NG = tm_groups(LOGW, N);
+        p.passes = (K + kTmKB - 1) / kTmKB;
+        p.units = (uint64_t)nb * p.spans;
+        const uint64_t warps = (uint64_t)(g_sm_count[dev] > 0 ? g_sm_count[dev] : 148) * WPC;
+        p.upw = (p.units + warps - 1) / warps;
+        const uint64_t blocks = (p.units + WPC * p.upw - 1) / (WPC * p.upw);
+        const size_t smem = tm_smem(LOGW, N, K);
+        CUtensorMap map;
+        if (!tm_make_map(&map, p.A, (uint64_t)nb * N, M, LOGW)) return GF_ECUDA;
+        encode_tmem_kernel<LOGW, WPC><<<(unsigned)blocks, WPC * 32, smem, st>>>(p, map);
+        const int rc = launch_status();
+        if (rc != GF_OK) return rc;
+    }
+    return GF_OK;
 }
 
 // Harness override of the encode kernel (gf_set_encode_path, thread-local).
@@ -523,7 +532,7 @@ static int launch_tmem(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, in
 static int encode_path_override()
 {
     const int t = tls_path;
-    return t >= GF_PATH_STREAM_STRIDED4 ? GF_PATH_STREAM : t;
+    return t >= GF_PATH_STREAM_STRIDED4 && t <= GF_PATH_STREAM_WIDE4 ? GF_PATH_STREAM : t;
 }
 
 // returned codes (include/gfrlnc.h, gf_encode_path): 0 column (words), 1 column
@@ -532,7 +541,7 @@ static int encode_path_override()
 // 11 GF(2) split engine (N <= 32, 16-byte aligned packets, K >= 24; any K when forced),
 // 12 GF(16) product-row with nibble-indexed tables (K > 32), 13 GF(256)
 // product-row with 32 coded packets per CTA on 768-word tiles (K > 32, long packets),
-// 14 TMEM lookup-table engine (GF(2) / GF(4), K >= 24, packets >= 4 KiB, 8-byte aligned)
+// 14 TMEM lookup-table engine (GF(2) / GF(4), K >= 24, packets >= 4 KiB, 16-byte aligned)
 static bool gf2_split_ok(int field, int N, int K, size_t M, const void *A, const void *B)
 {
     return field == 2 && N <= 32 && K >= 1 && M % 16 == 0 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0 &&
@@ -774,7 +783,7 @@ static int configure_field(int optin, uint32_t smem_base)
         if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<32, true, 2, true>, optin);
         if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<32, false, 2, true>, optin);
     }
-    if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<log2_field(F), tm_wpc<log2_field(F)>(), true>, optin);
+    if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<log2_field(F), tm_wpc<log2_field(F)>()>, optin);
     if (rc == GF_OK) rc = allow_smem(invert_warp_kernel, optin);
     if (rc == GF_OK) rc = allow_smem(invert_kernel, optin);
     return rc;

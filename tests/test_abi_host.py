@@ -241,8 +241,8 @@ def test_encode_path_query():
     assert gf.encode_path(2, 32, 32, 1 << 20) == "tmem"         # C5 GF(2): TMEM lookup tables
     assert gf.encode_path(4, 32, 32, 1 << 20) == "tmem"         # C5 GF(4)
     assert gf.encode_path(2, 33, 32, 1 << 20) == "tmem"         # GF(2), N > 32
-    assert gf.encode_path(4, 32, 32, 1 << 20, a_align=4) == "lanek-32"   # TMEM engine: 8-byte aligned
-    assert gf.encode_path(4, 32, 32, 4096 + 4) == "lanek-32"    # ... and M % 8 == 0
+    assert gf.encode_path(4, 32, 32, 1 << 20, a_align=8) == "lanek-32"   # TMEM engine: 16-byte aligned
+    assert gf.encode_path(4, 32, 32, 4096 + 8) == "lanek-32"    # ... and M % 16 == 0
     assert gf.encode_path(2, 32, 32, 2048) == "gf2-split"       # M < 4096: the split engine
     assert gf.encode_path(2, 33, 32, 2048) == "lanek-32"        # GF(2), N > 32, short packets
     assert gf.encode_path(4, 32, 16, 1 << 20) == "prow-16"      # K < 24

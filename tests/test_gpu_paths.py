@@ -28,13 +28,13 @@ CASES = {
     "gf2": [(2, s) for s in ((32, 32, 4096, 3), (17, 33, 1504, 3), (5, 24, 400, 3), (32, 1, 512, 4),
                              (1, 9, 16, 5), (16, 16, 2064, 2), (31, 96, 1040, 2), (32, 32, 65536, 2),
                              (12, 40, 528, 6))],
-    # TMEM lookup-table engine (any field; M % 8 == 0): ragged last span
+    # TMEM lookup-table engine (any field; M % 16 == 0): ragged last span
     # (M % 256 != 0), partial last 4-bit group (N w % 16 != 0), one to three
-    # passes of 32 coded packets, K % 32 != 0, single-word packets
-    "tmem": [(q, s) for q in ALL for s in ((32, 32, 4096, 3), (17, 33, 1504, 3), (5, 24, 400, 3), (1, 1, 8, 5),
-                                           (3, 70, 2056, 2), (33, 64, 65544, 1), (8, 40, 264, 7),
-                                           (32, 96, 1000, 2), (2, 5, 16, 9))] +
-            [(q, s) for q in (2, 4, 16) for s in ((64, 96, 1000, 2), (64, 64, 1504, 4))],
+    # passes of 32 coded packets, K % 32 != 0, four-word packets
+    "tmem": [(q, s) for q in ALL for s in ((32, 32, 4096, 3), (17, 33, 1504, 3), (5, 24, 400, 3), (1, 1, 16, 5),
+                                           (3, 70, 2064, 2), (33, 64, 65552, 1), (8, 40, 272, 7),
+                                           (32, 96, 1008, 2), (2, 5, 16, 9))] +
+            [(q, s) for q in (2, 4, 16) for s in ((64, 96, 1008, 2), (64, 64, 1504, 4))],
 }
 for name in ("stream", "stream-strided4", "stream-strided8", "stream-strided12", "stream-wide2",
              "stream-wide4"):
