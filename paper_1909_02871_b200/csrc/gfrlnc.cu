@@ -475,32 +475,42 @@ static int launch_gf2(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int
 
 // TMEM lookup-table engine (encode_tmem.cuh): 4-bit groups of the basis words
 // x^j a_i, their 16 XOR-subsets in tensor memory, one lookup per (group, k).
-// Warps per CTA: 16 for GF(4) (C5: 1.83 vs 1.77 TB/s at 12, 1.50 at 8), 8 otherwise
-// (GF(2) C5: 2.71 TB/s at 8 and 12; tools/exp_tmem.cu, profiles/r02_exp_tmem_v5.txt).
+// Warps per CTA: 16 for GF(4) (C5: 1.83 vs 1.77 TB/s at 12, 1.50 at 8), 8
+// otherwise (GF(2) C5: 2.71 TB/s at 8 and 12; tools/exp_tmem.cu,
+// profiles/r02_exp_tmem_v5.txt); half of that when the per-warp shared
+// memory (coefficient-address table + source ring) does not fit.
 template <int LOGW>
 constexpr int tm_wpc() { return LOGW == 1 ? 16 : 8; }
 
 static int tm_groups(int logw, int N) { return ((((N << logw) + 3) / 4) + kTmGPB - 1) / kTmGPB * kTmGPB; }
 
-static size_t tm_smem(int logw, int N, int K)
+static size_t tm_smem_w(int logw, int N, int K, int wpc)
 {
-    const int wpc = logw == 1 ? tm_wpc<1>() : tm_wpc<0>();
     return (size_t)wpc * tm_warp_bytes(logw, tm_groups(logw, N), (K + kTmKB - 1) / kTmKB);
 }
 
 static constexpr int log2_field(int field) { return field == 2 ? 0 : field == 4 ? 1 : field == 16 ? 2 : 3; }
 
-static bool tmem_ok(int field, int N, int K, size_t M, const void *A, const void *B)
+// warps per CTA for this shape: the preferred count or half of it, 0 if neither fits
+static int tm_pick_wpc(int logw, int N, int K)
 {
-    return M % 16 == 0 && M / 4 < 0xFFFFFFFFull && N * K > 0 && ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15u) == 0 &&
-           tm_smem(log2_field(field), N, K) <= 226 * 1024;
+    const int w0 = logw == 1 ? tm_wpc<1>() : tm_wpc<0>();
+    if (tm_smem_w(logw, N, K, w0) <= 226 * 1024) return w0;
+    if (tm_smem_w(logw, N, K, w0 / 2) <= 226 * 1024) return w0 / 2;
+    return 0;
 }
 
-template <int LOGW>
-static int launch_tmem(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M, size_t batch,
-                       cudaStream_t st)
+static bool tmem_ok(int field, int N, int K, size_t M, const void *A, const void *B)
 {
-    constexpr int WPC = tm_wpc<LOGW>();
+    return M % 16 == 0 && M / 4 < 0xFFFFFFFFull && N * K > 0 &&
+           ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15u) == 0 &&
+           tm_pick_wpc(log2_field(field), N, K) > 0;
+}
+
+template <int LOGW, int WPC>
+static int launch_tmem_w(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M, size_t batch,
+                         cudaStream_t st)
+{
     int dev;
     if (current_device(&dev) != GF_OK) return GF_ECUDA;
     // TMA row coordinates are 32-bit signed: at most 2^31 - 1 rows of A per launch
@@ -517,7 +527,7 @@ static int launch_tmem(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, in
         const uint64_t warps = (uint64_t)(g_sm_count[dev] > 0 ? g_sm_count[dev] : 148) * WPC;
         p.upw = (p.units + warps - 1) / warps;
         const uint64_t blocks = (p.units + WPC * p.upw - 1) / (WPC * p.upw);
-        const size_t smem = tm_smem(LOGW, N, K);
+        const size_t smem = tm_smem_w(LOGW, N, K, WPC);
         CUtensorMap map;
         if (!tm_make_map(&map, p.A, (uint64_t)nb * N, M, LOGW)) return GF_ECUDA;
         encode_tmem_kernel<LOGW, WPC><<<(unsigned)blocks, WPC * 32, smem, st>>>(p, map);
@@ -525,6 +535,17 @@ static int launch_tmem(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, in
         if (rc != GF_OK) return rc;
     }
     return GF_OK;
+}
+
+template <int LOGW>
+static int launch_tmem(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M, size_t batch,
+                       cudaStream_t st)
+{
+    constexpr int W0 = tm_wpc<LOGW>();
+    const int wpc = tm_pick_wpc(LOGW, N, K);
+    if (wpc == W0) return launch_tmem_w<LOGW, W0>(A, C, B, N, K, M, batch, st);
+    if (wpc == W0 / 2) return launch_tmem_w<LOGW, W0 / 2>(A, C, B, N, K, M, batch, st);
+    return GF_EARG;
 }
 
 // Harness override of the encode kernel (gf_set_encode_path, thread-local).
@@ -784,6 +805,7 @@ static int configure_field(int optin, uint32_t smem_base)
         if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<32, false, 2, true>, optin);
     }
     if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<log2_field(F), tm_wpc<log2_field(F)>()>, optin);
+    if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<log2_field(F), tm_wpc<log2_field(F)>() / 2>, optin);
     if (rc == GF_OK) rc = allow_smem(invert_warp_kernel, optin);
     if (rc == GF_OK) rc = allow_smem(invert_kernel, optin);
     return rc;
