@@ -71,19 +71,25 @@ struct TmParams {
     int passes;            // ceil(K / 32)
     uint64_t units;        // batch * spans
     uint64_t upw;          // units per warp
+    // fused Freivalds check (T > 0 instantiations; gf_encode_verify_batch, K <= 64)
+    const uint8_t *U;      // [batch][1][2][N]: u_j = C r_j over F_q
+    const uint32_t *RB;    // [batch][2][kw]: bit k of word k / 32 = r_jk
+    int kw;
+    unsigned long long *mismatch;   // [batch] += differing bytes
+    uint64_t fault;        // harness fault injection (FT): g << 32 | k << 20 | word
 };
 
 // sources per step (kTmGPB groups of 4 basis words, w basis words per source)
 __host__ __device__ constexpr int tm_sps(int logw) { return (4 * kTmGPB) >> logw; }
 
 // per-warp shared memory: TMEM addresses [passes][steps][kTmKB / 4][kTmGPB][4]
-// (one word per (pass, group, k)), then the source ring, then one mbarrier
-// per ring stage
+// (one word per (pass, group, k)), the check's addresses [NG][T] (T > 0),
+// then the source ring, then one mbarrier per ring stage
 __host__ __device__ constexpr size_t tm_tab_bytes(int NG, int passes) { return (size_t)passes * NG * kTmKB * 4; }
-__host__ __device__ constexpr size_t tm_warp_bytes(int logw, int NG, int passes)
+__host__ __device__ constexpr size_t tm_warp_bytes(int logw, int NG, int passes, int T = 0)
 {
     // (a multiple of 128 bytes: TMA destinations are 128-byte aligned)
-    return (tm_tab_bytes(NG, passes) + (size_t)kTmRing * tm_sps(logw) * kTmSpanWords * 4 + kTmRing * 8 + 127) / 128 * 128;
+    return (tm_tab_bytes(NG, passes) + (size_t)NG * T * 4 + (size_t)kTmRing * tm_sps(logw) * kTmSpanWords * 4 + kTmRing * 8 + 127) / 128 * 128;
 }
 
 // x * a on packed w-bit elements (bit j of an element = coefficient of x^j)
@@ -164,7 +170,17 @@ __device__ __forceinline__ void tm_expect_tx(uint32_t bar, uint32_t bytes)
 }
 
 // Grid: 1-D, WPC warps per block, one block per SM (TMEM: WPC / 4 x 128 columns).
-template <int LOGW, int WPC>
+//
+// T > 0: the fused Freivalds check of gf_encode_verify_batch (SURVEY 8(c) step
+// 7, 8(f) NEXT-4) with T binary projections r_j (K <= 64): B == A C iff
+// sum_k r_jk b_k == sum_i u_ji a_i with u_j = C r_j.  The A side is one more
+// lookup per group and projection in the first pass (u_j restricted to the
+// group's basis words is a 4-bit index into the same table); the B side XORs
+// every finished coded word into y2_j where r_jk = 1, before its store.  At the
+// end of a unit the differing bytes of y1_j and y2_j are counted into
+// mismatch[g].  FT: the harness fault injection (gf_set_verify_fault), a
+// separate instantiation.
+template <int LOGW, int WPC, int T = 0, bool FT = false>
 __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, const __grid_constant__ CUtensorMap tmA)
 {
     constexpr int w = 1 << LOGW;
@@ -189,8 +205,10 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, co
     const int N = p.N, K = p.K, NG = p.NG, passes = p.passes, steps = NG / kTmGPB;
     const uint32_t Mw = p.Mw, spans = p.spans;
     const size_t tabb = tm_tab_bytes(NG, passes);
-    uint32_t *tab = reinterpret_cast<uint32_t *>(smem8 + (size_t)wid * tm_warp_bytes(LOGW, NG, passes));
-    const uint32_t *ring = reinterpret_cast<const uint32_t *>(smem8 + (size_t)wid * tm_warp_bytes(LOGW, NG, passes) + tabb);
+    uint8_t *wbase = smem8 + (size_t)wid * tm_warp_bytes(LOGW, NG, passes, T);
+    uint32_t *tab = reinterpret_cast<uint32_t *>(wbase);
+    uint32_t *tabu = reinterpret_cast<uint32_t *>(wbase + tabb);               // [NG][T]
+    const uint32_t *ring = reinterpret_cast<const uint32_t *>(wbase + tabb + (size_t)NG * T * 4);
     const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
     const uint32_t bar_s = ring_s + kTmRing * SPS * kTmSpanWords * 4;
     if (lane < kTmRing) mbar_init(bar_s + 8 * lane, 1);
@@ -199,7 +217,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, co
 
     const uint64_t u0 = ((uint64_t)blockIdx.x * WPC + wid) * p.upw;
     const uint64_t u1 = u0 + p.upw < p.units ? u0 + p.upw : p.units;
-    const int64_t T = u0 < u1 ? (int64_t)(u1 - u0) * passes * steps : 0;
+    const int64_t nsteps = u0 < u1 ? (int64_t)(u1 - u0) * passes * steps : 0;
 
     // Step cursors (no divisions in the loop): a step is (unit, pass, group
     // step gs); unit = (generation g, span sp).  The producer runs
@@ -224,7 +242,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, co
     // one or lie past the end of A, and only meet zero coefficients; bytes past
     // the packet end belong to lanes that never store)
     auto issue = [&]() {
-        if (pc.t < T) {
+        if (pc.t < nsteps) {
             if (lane == 0) {
                 const uint32_t st = (uint32_t)(pc.t % kTmRing);
                 tm_expect_tx(bar_s + 8 * st, SPS * kTmSpanWords * 4u);
@@ -239,17 +257,30 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, co
     for (int t = 0; t < kTmRing - 1; t++) issue();
 
     uint64_t cur_g = ~0ull;
+    uint32_t bad = 0;                                // check: differing bytes of this warp's current generation
+    int fk = -1;                                     // FT: coded packet to corrupt in this generation
+    uint32_t y1[T > 0 ? T : 1][2], y2[T > 0 ? T : 1][2], rw[T > 0 ? T : 1];
+#pragma unroll
+    for (int j = 0; j < (T > 0 ? T : 1); j++) y1[j][0] = y1[j][1] = y2[j][0] = y2[j][1] = rw[j] = 0u;
+    (void)fk; (void)y1; (void)y2; (void)rw;
     uint32_t acc[kTmKB][2];
 #pragma unroll
     for (int k = 0; k < kTmKB; k++) acc[k][0] = acc[k][1] = 0u;
 
 #pragma unroll 1
-    for (int64_t t = 0; t < T; t++) {
+    for (int64_t t = 0; t < nsteps; t++) {
         __syncwarp();                                // every lane is done with the stage issue() refills
         issue();
         const uint64_t g = cc.g;
         const int pass = cc.pass, gs = cc.gs;
         if (g != cur_g) {                            // this warp's TMEM lookup addresses for generation g
+            if constexpr (T > 0) {
+                bad = __reduce_add_sync(0xffffffffu, bad);
+                if (lane == 0 && bad && cur_g != ~0ull) atomicAdd(p.mismatch + cur_g, (unsigned long long)bad);
+                bad = 0;
+                if constexpr (FT)
+                    fk = (g == ((p.fault >> 32) & 0x7FFFFFFFu)) ? (int)((p.fault >> 20) & 0xFFFu) : -1;
+            }
             cur_g = g;
             const uint8_t *Cg = p.C + g * (size_t)N * K;
             __syncwarp();
@@ -267,6 +298,19 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, co
                     }
                 }
                 tab[e] = tb + (uint32_t)sl * (16 * kTmW) + idx * kTmW;
+            }
+            if constexpr (T > 0) {
+                const uint8_t *Ug = p.U + g * 2 * (size_t)N;
+                for (int e = lane; e < NG * T; e += 32) {
+                    const int grp = e / T, j = e - grp * T;
+                    uint32_t idx = 0;
+#pragma unroll
+                    for (int b = 0; b < 4; b++) {
+                        const int tt = 4 * grp + b, i = tt >> LOGW, jj = tt & (w - 1);
+                        if (i < N) idx |= ((__ldg(Ug + (size_t)j * N + i) >> jj) & 1u) << b;
+                    }
+                    tabu[e] = tb + (uint32_t)(grp % kTmGPB) * (16 * kTmW) + idx * kTmW;
+                }
             }
             __syncwarp();
         }
@@ -331,12 +375,41 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, co
                     acc[kq * 4 + kk][wd] = x ^ r[(kk * 4 + 2) * 2 + wd] ^ r[(kk * 4 + 3) * 2 + wd];
                 }
         }
+        if constexpr (T > 0) {
+            if (gs == 0)
+#pragma unroll
+                for (int j = 0; j < T; j++) rw[j] = __ldg(p.RB + (g * 2 + j) * (size_t)p.kw + pass);
+            if (pass == 0) {                         // A side: u_j's 4-bit index per group, same tables
+                uint32_t r[32];
+#pragma unroll
+                for (int e = 0; e < 32; e++) r[e] = 0u;
+                const uint32_t *tu = tabu + (size_t)gs * kTmGPB * T;
+#pragma unroll
+                for (int e = 0; e < kTmGPB * T; e++) tm_ld2(tu[e], r[2 * e], r[2 * e + 1]);
+                tm_wait_ld32(r);
+#pragma unroll
+                for (int e = 0; e < kTmGPB * T; e++) {
+                    y1[e % T][0] ^= r[2 * e];
+                    y1[e % T][1] ^= r[2 * e + 1];
+                }
+            }
+        }
         if (gs == steps - 1) {                       // the pass is complete: store and reset
             const uint32_t wi = cc.sp * kTmSpanWords + 2 * lane;
             uint32_t *Bg = reinterpret_cast<uint32_t *>(p.B) + (g * K + (size_t)pass * kTmKB) * Mw + wi;
             const int kn = K - pass * kTmKB;
 #pragma unroll
             for (int k = 0; k < kTmKB; k++) {
+                if constexpr (T > 0) {
+                    if constexpr (FT)
+                        if (pass * kTmKB + k == fk && wi == ((uint32_t)p.fault & 0xFFFFEu)) {
+                            if (p.fault & 1u) acc[k][1] ^= 0x5Au;      // harness: one wrong byte
+                            else acc[k][0] ^= 0x5Au;
+                        }
+#pragma unroll
+                    for (int j = 0; j < T; j++)
+                        if ((rw[j] >> k) & 1u) { y2[j][0] ^= acc[k][0]; y2[j][1] ^= acc[k][1]; }
+                }
                 if (k < kn) {
                     if (wi < Mw)
                         asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};"
@@ -344,8 +417,21 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, co
                 }
                 acc[k][0] = acc[k][1] = 0u;
             }
+            if constexpr (T > 0) {
+                if (pass == passes - 1) {            // the unit is complete: compare the projections
+#pragma unroll
+                    for (int j = 0; j < T; j++) {
+                        if (wi < Mw) bad += nz_bytes(y1[j][0] ^ y2[j][0]) + nz_bytes(y1[j][1] ^ y2[j][1]);
+                        y1[j][0] = y1[j][1] = y2[j][0] = y2[j][1] = 0u;
+                    }
+                }
+            }
         }
         advance(cc);
+    }
+    if constexpr (T > 0) {
+        bad = __reduce_add_sync(0xffffffffu, bad);
+        if (lane == 0 && bad && cur_g != ~0ull) atomicAdd(p.mismatch + cur_g, (unsigned long long)bad);
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();

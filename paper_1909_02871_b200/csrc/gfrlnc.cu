@@ -484,9 +484,9 @@ constexpr int tm_wpc() { return LOGW == 1 ? 16 : 8; }
 
 static int tm_groups(int logw, int N) { return ((((N << logw) + 3) / 4) + kTmGPB - 1) / kTmGPB * kTmGPB; }
 
-static size_t tm_smem_w(int logw, int N, int K, int wpc)
+static size_t tm_smem_w(int logw, int N, int K, int wpc, int T = 0)
 {
-    return (size_t)wpc * tm_warp_bytes(logw, tm_groups(logw, N), (K + kTmKB - 1) / kTmKB);
+    return (size_t)wpc * tm_warp_bytes(logw, tm_groups(logw, N), (K + kTmKB - 1) / kTmKB, T);
 }
 
 static constexpr int log2_field(int field) { return field == 2 ? 0 : field == 4 ? 1 : field == 16 ? 2 : 3; }
@@ -507,9 +507,9 @@ static bool tmem_ok(int field, int N, int K, size_t M, const void *A, const void
            tm_pick_wpc(log2_field(field), N, K) > 0;
 }
 
-template <int LOGW, int WPC>
+template <int LOGW, int WPC, int T = 0, bool FT = false>
 static int launch_tmem_w(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M, size_t batch,
-                         cudaStream_t st)
+                         cudaStream_t st, const TmParams *vp = nullptr)
 {
     int dev;
     if (current_device(&dev) != GF_OK) return GF_ECUDA;
@@ -518,6 +518,15 @@ static int launch_tmem_w(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, 
     for (size_t g0 = 0; g0 < batch; g0 += gmax) {
         const size_t nb = batch - g0 < gmax ? batch - g0 : gmax;
         TmParams p{};
+        if (vp) {                                              // check fields (T > 0)
+            p = *vp;
+            p.U = vp->U + g0 * 2 * (size_t)N;
+            p.RB = vp->RB + g0 * 2 * (size_t)vp->kw;
+            p.mismatch = vp->mismatch + g0;
+            const uint64_t fg = (vp->fault >> 32) & 0x7FFFFFFFu;
+            p.fault = (fg >= g0 && fg < g0 + nb) ? (vp->fault & 0xFFFFFFFFull) | ((fg - g0) << 32)
+                                                 : 0x7FFFFFFFull << 32;           // (no generation matches)
+        }
         p.A = A + g0 * N * M; p.C = C + g0 * N * K; p.B = B + g0 * K * M; p.N = N; p.K = K;
         p.Mw = (uint32_t)(M / 4);
         p.spans = (p.Mw + kTmSpanWords - 1) / kTmSpanWords;
@@ -527,10 +536,10 @@ static int launch_tmem_w(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, 
         const uint64_t warps = (uint64_t)(g_sm_count[dev] > 0 ? g_sm_count[dev] : 148) * WPC;
         p.upw = (p.units + warps - 1) / warps;
         const uint64_t blocks = (p.units + WPC * p.upw - 1) / (WPC * p.upw);
-        const size_t smem = tm_smem_w(LOGW, N, K, WPC);
+        const size_t smem = tm_smem_w(LOGW, N, K, WPC, T);
         CUtensorMap map;
         if (!tm_make_map(&map, p.A, (uint64_t)nb * N, M, LOGW)) return GF_ECUDA;
-        encode_tmem_kernel<LOGW, WPC><<<(unsigned)blocks, WPC * 32, smem, st>>>(p, map);
+        encode_tmem_kernel<LOGW, WPC, T, FT><<<(unsigned)blocks, WPC * 32, smem, st>>>(p, map);
         const int rc = launch_status();
         if (rc != GF_OK) return rc;
     }
@@ -545,6 +554,24 @@ static int launch_tmem(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, in
     const int wpc = tm_pick_wpc(LOGW, N, K);
     if (wpc == W0) return launch_tmem_w<LOGW, W0>(A, C, B, N, K, M, batch, st);
     if (wpc == W0 / 2) return launch_tmem_w<LOGW, W0 / 2>(A, C, B, N, K, M, batch, st);
+    return GF_EARG;
+}
+
+// the TMEM engine with the check fused (GF(2) / GF(4), K <= 64): 12 warps per
+// CTA for GF(4) (the check's registers), 8 for GF(2); 8 / 4 when the per-warp
+// shared memory does not fit
+template <int LOGW, int T>
+static int launch_tmem_check(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M, size_t batch,
+                             cudaStream_t st, const TmParams *vp)
+{
+    constexpr int W0 = LOGW == 1 ? 12 : 8, W1 = LOGW == 1 ? 8 : 4;
+    const bool ft = (vp->fault >> 63) != 0;
+    if (tm_smem_w(LOGW, N, K, W0, T) <= 226 * 1024)
+        return ft ? launch_tmem_w<LOGW, W0, T, true>(A, C, B, N, K, M, batch, st, vp)
+                  : launch_tmem_w<LOGW, W0, T>(A, C, B, N, K, M, batch, st, vp);
+    if (tm_smem_w(LOGW, N, K, W1, T) <= 226 * 1024)
+        return ft ? launch_tmem_w<LOGW, W1, T, true>(A, C, B, N, K, M, batch, st, vp)
+                  : launch_tmem_w<LOGW, W1, T>(A, C, B, N, K, M, batch, st, vp);
     return GF_EARG;
 }
 
@@ -806,6 +833,17 @@ static int configure_field(int optin, uint32_t smem_base)
     }
     if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<log2_field(F), tm_wpc<log2_field(F)>()>, optin);
     if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<log2_field(F), tm_wpc<log2_field(F)>() / 2>, optin);
+    if constexpr (F <= 4) {
+        constexpr int L = log2_field(F), W0 = L == 1 ? 12 : 8, W1 = L == 1 ? 8 : 4;
+        if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<L, W0, 1>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<L, W0, 2>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<L, W0, 1, true>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<L, W0, 2, true>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<L, W1, 1>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<L, W1, 2>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<L, W1, 1, true>, optin);
+        if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<L, W1, 2, true>, optin);
+    }
     if (rc == GF_OK) rc = allow_smem(invert_warp_kernel, optin);
     if (rc == GF_OK) rc = allow_smem(invert_kernel, optin);
     return rc;
@@ -1158,8 +1196,16 @@ int gf_encode_verify_batch(int field, const uint8_t *A, const uint8_t *C, uint8_
     verify_prep_kernel<<<(unsigned)batch, 128, 8 * (size_t)kw, st>>>(C, R, U, RB, N, K, t, kblocks, kw, batch,
                                                                       field - 1);
     if ((rc = launch_status()) != GF_OK) return rc;
-    // (the TMEM engine has no fused check: its shapes take the fused kernels below)
-    const int path = encode_path(field, N, K, M, A, B, false);
+    const int path = encode_path(field, N, K, M, A, B);
+    if (path == 14 && field <= 4 && K <= 64) {                 // fused: the TMEM engine
+        TmParams vp{};
+        vp.U = U; vp.RB = RB; vp.kw = kw; vp.mismatch = mismatch; vp.fault = tls_fault;
+        if (field == 2)
+            return t == 1 ? launch_tmem_check<0, 1>(A, C, B, N, K, M, batch, st, &vp)
+                          : launch_tmem_check<0, 2>(A, C, B, N, K, M, batch, st, &vp);
+        return t == 1 ? launch_tmem_check<1, 1>(A, C, B, N, K, M, batch, st, &vp)
+                      : launch_tmem_check<1, 2>(A, C, B, N, K, M, batch, st, &vp);
+    }
     // The GF(2) split engine (HBM-bound: a second pass over A and B would double
     // its traffic) checks inside the encode.  Every other kernel -- the
     // shared-memory-bound product-row kernels among them, which leave most of

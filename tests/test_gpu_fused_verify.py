@@ -55,7 +55,12 @@ CASES = [  # (q, N, K, M, batch, expected kernel)
     # lane-k with the check fused: 32 and 64 coded packets per CTA (GF(2) with
     # N > 32, where the split engine does not apply); 128 per CTA (K > 64) runs
     # the streaming check
-    (4, 64, 64, 4096, 2, "lanek-64"), (2, 40, 48, 2048, 3, "lanek-64"), (4, 24, 70, 1024, 2, "lanek-64")]
+    (4, 64, 64, 2048, 2, "lanek-64"), (2, 40, 48, 2048, 3, "lanek-64"), (4, 24, 70, 1024, 2, "lanek-64"),
+    # the TMEM engine with the check fused: two passes of 32 coded packets,
+    # a partial last group (N = 33), a ragged last span, several generations
+    # per warp; K > 64 runs the streaming check after it
+    (4, 33, 64, 4112, 3, "tmem"), (2, 64, 64, 8192, 2, "tmem"), (4, 32, 40, 20480, 2, "tmem"),
+    (2, 7, 24, 4096, 40, "tmem"), (4, 32, 70, 4096, 2, "tmem")]
 
 
 @pytest.mark.parametrize("q,N,K,M,batch,kern", CASES)
@@ -84,6 +89,34 @@ def test_fused_verify_matches_oracle(gfm, q, N, K, M, batch, kern, t):
     rsel = R[batch // 2, K - 1, :t] & 1
     assert (got[batch // 2] > 0) == bool(rsel.any())       # caught iff some r_j selects coded packet K-1
     assert got.sum() == got[batch // 2]
+
+
+@pytest.mark.parametrize("q", (2, 4))
+def test_fused_verify_forced_tmem(gfm, q):
+    """The TMEM engine's fused check on short packets (forced: the router sends
+    packets below 4 KiB elsewhere), one and two projections, with and without
+    an injected fault."""
+    gfm.set_encode_path("tmem")
+    try:
+        for N, K, M, batch, t in ((5, 24, 400, 6, 2), (17, 33, 1040, 3, 1), (3, 1, 16, 9, 2), (32, 64, 272, 4, 2)):
+            assert gfm.encode_path(q, N, K, M) == "tmem"
+            A = si.random_bytes(700 + N, si.STREAM_A, 0, batch * N * M).reshape(batch, N, M)
+            C = si.uniform_coeffs(q, 701 + K, si.STREAM_C, 0, batch * N * K).reshape(batch, N, K)
+            R = si.random_bytes(702, si.STREAM_FREIVALDS, 0, batch * K * t).reshape(batch, K, t)
+            B, mism = gfm.encode_verify_batch(q, *(torch.from_numpy(x).cuda() for x in (A, C, R)))
+            Bh = B.cpu().numpy()
+            assert np.array_equal(Bh, oracle.encode_batch(q, A, C)), (q, N, K, M)
+            assert (mism.cpu().numpy() == 0).all()
+            gfm.set_verify_fault(batch - 1, K - 1, (M // 4) - 1)
+            try:
+                B2, mism2 = gfm.encode_verify_batch(q, *(torch.from_numpy(x).cuda() for x in (A, C, R)))
+            finally:
+                gfm.set_verify_fault(-1)
+            B2h, got = B2.cpu().numpy(), mism2.cpu().numpy()
+            assert int((B2h != Bh).sum()) == 1
+            assert np.array_equal(got, oracle_counts(q, A, C, B2h, R)), (got, q, N, K, M)
+    finally:
+        gfm.set_encode_path("auto")
 
 
 @pytest.mark.parametrize("q", (16, 256))

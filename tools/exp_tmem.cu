@@ -70,7 +70,7 @@ static void run(int N, int K, size_t M, size_t G, int reps)
     p.units = (uint64_t)G * p.spans;
     const uint64_t warps = (uint64_t)sms * WPC;
     p.upw = (p.units + warps - 1) / warps;
-    const size_t smem = (size_t)WPC * tm_warp_bytes(LOGW, NG, p.passes);
+    const size_t smem = (size_t)WPC * tm_warp_bytes(LOGW, NG, p.passes, 0);
     auto kern = encode_tmem_kernel<LOGW, WPC>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int blocks = (int)((p.units + (uint64_t)WPC * p.upw - 1) / ((uint64_t)WPC * p.upw));
