@@ -86,10 +86,11 @@ __host__ __device__ constexpr int tm_sps(int logw) { return (4 * kTmGPB) >> logw
 // (one word per (pass, group, k)), the check's addresses [NG][T] (T > 0),
 // then the source ring, then one mbarrier per ring stage
 __host__ __device__ constexpr size_t tm_tab_bytes(int NG, int passes) { return (size_t)passes * NG * kTmKB * 4; }
+__host__ __device__ constexpr size_t tm_tabu_bytes(int NG, int T) { return ((size_t)NG * T * 4 + 127) / 128 * 128; }
 __host__ __device__ constexpr size_t tm_warp_bytes(int logw, int NG, int passes, int T = 0)
 {
     // (a multiple of 128 bytes: TMA destinations are 128-byte aligned)
-    return (tm_tab_bytes(NG, passes) + (size_t)NG * T * 4 + (size_t)kTmRing * tm_sps(logw) * kTmSpanWords * 4 + kTmRing * 8 + 127) / 128 * 128;
+    return (tm_tab_bytes(NG, passes) + tm_tabu_bytes(NG, T) + (size_t)kTmRing * tm_sps(logw) * kTmSpanWords * 4 + kTmRing * 8 + 127) / 128 * 128;
 }
 
 // x * a on packed w-bit elements (bit j of an element = coefficient of x^j)
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, co
     uint8_t *wbase = smem8 + (size_t)wid * tm_warp_bytes(LOGW, NG, passes, T);
     uint32_t *tab = reinterpret_cast<uint32_t *>(wbase);
     uint32_t *tabu = reinterpret_cast<uint32_t *>(wbase + tabb);               // [NG][T]
-    const uint32_t *ring = reinterpret_cast<const uint32_t *>(wbase + tabb + (size_t)NG * T * 4);
+    const uint32_t *ring = reinterpret_cast<const uint32_t *>(wbase + tabb + tm_tabu_bytes(NG, T));
     const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
     const uint32_t bar_s = ring_s + kTmRing * SPS * kTmSpanWords * 4;
     if (lane < kTmRing) mbar_init(bar_s + 8 * lane, 1);
