@@ -98,7 +98,10 @@ template <int LOGW>
 __device__ __forceinline__ uint32_t tm_xtime(uint32_t a)
 {
     if constexpr (LOGW == 1) {
-        return gf4_xtime(a);
+        // x (a1 x + a0) = (a0 + a1) x + a1: with t = a >> 1, new a0 = t & 0x55..,
+        // new a1 = ((a ^ t) & 0x55..) << 1 (two LOP3, one SHF, one IMAD)
+        const uint32_t t = a >> 1, u = (a ^ t) & 0x55555555u;
+        return (t & 0x55555555u) | (u + u);
     } else if constexpr (LOGW == 2) {                         // x^4 + x + 1
         const uint32_t h = (a >> 3) & 0x11111111u;
         return ((a << 1) & 0xEEEEEEEEu) ^ (h * 3u);
@@ -131,6 +134,13 @@ __device__ __forceinline__ void tm_wait_ld32(uint32_t (&v)[32])
                  : TM_P8(v, 0), TM_P8(v, 8), TM_P8(v, 16), TM_P8(v, 24) :: "memory");
 }
 #undef TM_P8
+
+#define TM_Q8(v, o) "+r"(v[o]), "+r"(v[o + 1]), "+r"(v[o + 2]), "+r"(v[o + 3]), "+r"(v[o + 4]), "+r"(v[o + 5]), "+r"(v[o + 6]), "+r"(v[o + 7])
+__device__ __forceinline__ void tm_wait_ld16(uint32_t (&v)[16])
+{
+    asm volatile("tcgen05.wait::ld.sync.aligned;" : TM_Q8(v, 0), TM_Q8(v, 8) :: "memory");
+}
+#undef TM_Q8
 
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -359,22 +369,29 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, co
         const uint4 *ta = reinterpret_cast<const uint4 *>(tab + ((size_t)pass * steps + gs) * (kTmKB * kTmGPB));
 #pragma unroll
         for (int kq = 0; kq < kTmKB / 4; kq++) {
-            uint32_t r[32];
+            uint4 a4[kTmGPB];                       // addresses of k = 4 kq .. 4 kq + 3, per group
 #pragma unroll
-            for (int sl = 0; sl < kTmGPB; sl++) {
-                const uint4 a = ta[kq * kTmGPB + sl];     // addresses of k = 4 kq .. 4 kq + 3
-                const uint32_t aw[4] = {a.x, a.y, a.z, a.w};
+            for (int sl = 0; sl < kTmGPB; sl++) a4[sl] = ta[kq * kTmGPB + sl];
+            // two half-batches of 2 coded packets x 4 groups (8 loads in flight
+            // per wait: fewer registers than 16, so 16 warps fit without spills)
 #pragma unroll
-                for (int kk = 0; kk < 4; kk++) tm_ld2(aw[kk], r[(kk * 4 + sl) * 2], r[(kk * 4 + sl) * 2 + 1]);
-            }
-            tm_wait_ld32(r);
+            for (int h = 0; h < 2; h++) {
+                uint32_t r[16];
 #pragma unroll
-            for (int kk = 0; kk < 4; kk++)
-#pragma unroll
-                for (int wd = 0; wd < 2; wd++) {
-                    const uint32_t x = acc[kq * 4 + kk][wd] ^ r[(kk * 4) * 2 + wd] ^ r[(kk * 4 + 1) * 2 + wd];
-                    acc[kq * 4 + kk][wd] = x ^ r[(kk * 4 + 2) * 2 + wd] ^ r[(kk * 4 + 3) * 2 + wd];
+                for (int sl = 0; sl < kTmGPB; sl++) {
+                    tm_ld2(h ? a4[sl].z : a4[sl].x, r[sl * 2], r[sl * 2 + 1]);
+                    tm_ld2(h ? a4[sl].w : a4[sl].y, r[8 + sl * 2], r[8 + sl * 2 + 1]);
                 }
+                tm_wait_ld16(r);
+#pragma unroll
+                for (int kk = 0; kk < 2; kk++)
+#pragma unroll
+                    for (int wd = 0; wd < 2; wd++) {
+                        uint32_t &y = acc[kq * 4 + 2 * h + kk][wd];
+                        const uint32_t x = y ^ r[kk * 8 + wd] ^ r[kk * 8 + 2 + wd];
+                        y = x ^ r[kk * 8 + 4 + wd] ^ r[kk * 8 + 6 + wd];
+                    }
+            }
         }
         if constexpr (T > 0) {
             if (gs == 0)
@@ -399,9 +416,9 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, co
             const uint32_t wi = cc.sp * kTmSpanWords + 2 * lane;
             uint32_t *Bg = reinterpret_cast<uint32_t *>(p.B) + (g * K + (size_t)pass * kTmKB) * Mw + wi;
             const int kn = K - pass * kTmKB;
+            if constexpr (T > 0) {
 #pragma unroll
-            for (int k = 0; k < kTmKB; k++) {
-                if constexpr (T > 0) {
+                for (int k = 0; k < kTmKB; k++) {
                     if constexpr (FT)
                         if (pass * kTmKB + k == fk && wi == ((uint32_t)p.fault & 0xFFFFEu)) {
                             if (p.fault & 1u) acc[k][1] ^= 0x5Au;      // harness: one wrong byte
@@ -411,13 +428,19 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, co
                     for (int j = 0; j < T; j++)
                         if ((rw[j] >> k) & 1u) { y2[j][0] ^= acc[k][0]; y2[j][1] ^= acc[k][1]; }
                 }
-                if (k < kn) {
-                    if (wi < Mw)
-                        asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};"
-                                     :: "l"(Bg + (size_t)k * Mw), "r"(acc[k][0]), "r"(acc[k][1]) : "memory");
-                }
-                acc[k][0] = acc[k][1] = 0u;
             }
+            if (wi < Mw) {                           // row k of the pass: one pointer step of Mw words
+                uint32_t *q = Bg;
+#pragma unroll
+                for (int k = 0; k < kTmKB; k++) {
+                    if (k < kn)
+                        asm volatile("st.global.v2.u32 [%0], {%1,%2};" :: "l"(q), "r"(acc[k][0]), "r"(acc[k][1])
+                                     : "memory");
+                    q += Mw;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < kTmKB; k++) acc[k][0] = acc[k][1] = 0u;
             if constexpr (T > 0) {
                 if (pass == passes - 1) {            // the unit is complete: compare the projections
 #pragma unroll

@@ -475,12 +475,15 @@ static int launch_gf2(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int
 
 // TMEM lookup-table engine (encode_tmem.cuh): 4-bit groups of the basis words
 // x^j a_i, their 16 XOR-subsets in tensor memory, one lookup per (group, k).
-// Warps per CTA: 16 for GF(4) (C5: 1.83 vs 1.77 TB/s at 12, 1.50 at 8), 8
-// otherwise (GF(2) C5: 2.71 TB/s at 8 and 12; tools/exp_tmem.cu,
-// profiles/r02_exp_tmem_v5.txt); half of that when the per-warp shared
-// memory (coefficient-address table + source ring) does not fit.
+// Warps per CTA: 12 for GF(4) (C5: 1.85 TB/s against 1.46 at 16 -- register
+// spills at 128 per thread -- and 1.66 at 8), 8 otherwise (GF(2) C5: 2.81
+// TB/s against 2.69 at 12; tools/exp_tmem.cu, profiles/r02_exp_tmem_v7.txt);
+// tm_wpc2 when the per-warp shared memory (coefficient-address table +
+// source ring) does not fit.
 template <int LOGW>
-constexpr int tm_wpc() { return LOGW == 1 ? 16 : 8; }
+constexpr int tm_wpc() { return LOGW == 1 ? 12 : 8; }
+template <int LOGW>
+constexpr int tm_wpc2() { return LOGW == 1 ? 8 : 4; }
 
 static int tm_groups(int logw, int N) { return ((((N << logw) + 3) / 4) + kTmGPB - 1) / kTmGPB * kTmGPB; }
 
@@ -494,9 +497,9 @@ static constexpr int log2_field(int field) { return field == 2 ? 0 : field == 4 
 // warps per CTA for this shape: the preferred count or half of it, 0 if neither fits
 static int tm_pick_wpc(int logw, int N, int K)
 {
-    const int w0 = logw == 1 ? tm_wpc<1>() : tm_wpc<0>();
+    const int w0 = logw == 1 ? tm_wpc<1>() : tm_wpc<0>(), w1 = logw == 1 ? tm_wpc2<1>() : tm_wpc2<0>();
     if (tm_smem_w(logw, N, K, w0) <= 226 * 1024) return w0;
-    if (tm_smem_w(logw, N, K, w0 / 2) <= 226 * 1024) return w0 / 2;
+    if (tm_smem_w(logw, N, K, w1) <= 226 * 1024) return w1;
     return 0;
 }
 
@@ -550,10 +553,10 @@ template <int LOGW>
 static int launch_tmem(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M, size_t batch,
                        cudaStream_t st)
 {
-    constexpr int W0 = tm_wpc<LOGW>();
+    constexpr int W0 = tm_wpc<LOGW>(), W1 = tm_wpc2<LOGW>();
     const int wpc = tm_pick_wpc(LOGW, N, K);
     if (wpc == W0) return launch_tmem_w<LOGW, W0>(A, C, B, N, K, M, batch, st);
-    if (wpc == W0 / 2) return launch_tmem_w<LOGW, W0 / 2>(A, C, B, N, K, M, batch, st);
+    if (wpc == W1) return launch_tmem_w<LOGW, W1>(A, C, B, N, K, M, batch, st);
     return GF_EARG;
 }
 
@@ -832,7 +835,7 @@ static int configure_field(int optin, uint32_t smem_base)
         if (rc == GF_OK) rc = allow_smem(encode_gf2_kernel<32, false, 2, true>, optin);
     }
     if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<log2_field(F), tm_wpc<log2_field(F)>()>, optin);
-    if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<log2_field(F), tm_wpc<log2_field(F)>() / 2>, optin);
+    if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<log2_field(F), tm_wpc2<log2_field(F)>()>, optin);
     if constexpr (F <= 4) {
         constexpr int L = log2_field(F), W0 = L == 1 ? 12 : 8, W1 = L == 1 ? 8 : 4;
         if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<L, W0, 1>, optin);
