@@ -48,6 +48,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "gf_device.cuh"
 
@@ -143,6 +144,18 @@ __device__ __forceinline__ void tm_wait_ld16(uint32_t (&v)[16])
 #undef TM_Q8
 
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// f(integral_constant<int, i>) for i = 0 .. NI-1, unrolled at compile time
+template <int I, int NI, class F>
+__device__ __forceinline__ void tm_unroll_i(F &&f)
+{
+    if constexpr (I < NI) {
+        f(std::integral_constant<int, I>{});
+        tm_unroll_i<I + 1, NI>(f);
+    }
+}
+template <int NI, class F>
+__device__ __forceinline__ void tm_unroll(F &&f) { tm_unroll_i<0, NI>(f); }
 
 // one TMA tile load (box SPS rows x 256 bytes at byte x, row y of A) into
 // shared memory, completing its bytes on an mbarrier
@@ -367,13 +380,15 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, co
         }
         tm_wait_st();
         const uint4 *ta = reinterpret_cast<const uint4 *>(tab + ((size_t)pass * steps + gs) * (kTmKB * kTmGPB));
-#pragma unroll
-        for (int kq = 0; kq < kTmKB / 4; kq++) {
+        const int kpass = K - pass * kTmKB;          // coded packets of this pass (warp-uniform)
+        // one kq step: lookups of coded packets 4 kq .. 4 kq + 3
+        auto kstep = [&](auto kqc) {
+            constexpr int kq = decltype(kqc)::value;
             uint4 a4[kTmGPB];                       // addresses of k = 4 kq .. 4 kq + 3, per group
 #pragma unroll
             for (int sl = 0; sl < kTmGPB; sl++) a4[sl] = ta[kq * kTmGPB + sl];
             // two half-batches of 2 coded packets x 4 groups (8 loads in flight
-            // per wait: fewer registers than 16, so 16 warps fit without spills)
+            // per wait: fewer live registers than 16)
 #pragma unroll
             for (int h = 0; h < 2; h++) {
                 uint32_t r[16];
@@ -392,6 +407,11 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, co
                         y = x ^ r[kk * 8 + 4 + wd] ^ r[kk * 8 + 6 + wd];
                     }
             }
+        };
+        if (kpass >= kTmKB) {
+            tm_unroll<kTmKB / 4>([&](auto kqc) { kstep(kqc); });
+        } else {                                     // K < 32: no lookups for absent coded packets
+            tm_unroll<kTmKB / 4>([&](auto kqc) { if (decltype(kqc)::value * 4 < kpass) kstep(kqc); });
         }
         if constexpr (T > 0) {
             if (gs == 0)

@@ -592,7 +592,8 @@ static int encode_path_override()
 // 11 GF(2) split engine (N <= 32, 16-byte aligned packets, K >= 24; any K when forced),
 // 12 GF(16) product-row with nibble-indexed tables (K > 32), 13 GF(256)
 // product-row with 32 coded packets per CTA on 768-word tiles (K > 32, long packets),
-// 14 TMEM lookup-table engine (GF(2) / GF(4), K >= 24, packets >= 4 KiB, 16-byte aligned)
+// 14 TMEM lookup-table engine (GF(2) / GF(4) K >= 9, GF(16) 24 <= K <= 32 or K > 32 with
+// N <= 32; packets >= 256 B, M % 16 == 0, 16-byte aligned)
 static bool gf2_split_ok(int field, int N, int K, size_t M, const void *A, const void *B)
 {
     return field == 2 && N <= 32 && K >= 1 && M % 16 == 0 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0 &&
@@ -606,11 +607,18 @@ static int encode_path(int field, int N, int K, size_t M, const void *A, const v
     const int ov = encode_path_override();
     if (!aligned) return 1;
     if (K <= 4 && (ov == GF_PATH_STREAM || ov == 0)) return 8;  // streaming (16- or 4-byte chunks)
-    // GF(2) / GF(4), K >= 24, long packets: the TMEM lookup-table engine
-    // (C5: GF(2) 2.29 -> 2.60 TB/s against the split engine, GF(4) 1.13 -> 1.75
-    // against lane-k; forced: any field and shape it takes)
+    // The TMEM lookup-table engine on 16-byte aligned packets of >= 256 bytes:
+    // GF(2) / GF(4) with K >= 9 (C5: GF(2) 2.29 -> 2.8-2.95 TB/s against the
+    // split engine, GF(4) 1.13 -> 1.8 against lane-k; K = 12-20: 1.3-2.4x the
+    // column / product-row kernels; K = 8: the column kernel is 0-10% faster),
+    // GF(16) with 24 <= K <= 32, or K > 32 and N <= 32 (1.1-2.3x the
+    // product-row kernels; at K = 16 they are 1.8x faster, at N = K = 64
+    // 5%); profiles/r02_exp_tmem_route_v4.txt.  Forced: any field and shape it takes.
     if (tmem && ov == GF_PATH_TMEM && tmem_ok(field, N, K, M, A, B)) return 14;
-    if (tmem && ov == 0 && field <= 4 && K >= 24 && M >= 4096 && tmem_ok(field, N, K, M, A, B)) return 14;
+    if (tmem && ov == 0 && M >= 256 &&
+        ((field <= 4 && K >= 9) || (field == 16 && ((K >= 24 && K <= 32) || (K > 32 && N <= 32)))) &&
+        tmem_ok(field, N, K, M, A, B))
+        return 14;
     // GF(2): the split engine (encode_gf2.cuh) where the lane-k kernel ran
     // before, K >= 24 (C5 N = K = 32, 1 MiB: 2.21 vs 1.66 TB/s)
     if (ov == GF_PATH_GF2 && gf2_split_ok(field, N, K, M, A, B)) return 11;

@@ -233,23 +233,30 @@ def test_encode_path_query():
     assert gf.encode_path(4, 32, 32, 1500) == "lanek-32"
     # GF(4), 9 <= K < 24: product rows when tiles cover >= 85% and (K > 16 or M >= 4 KiB)
     assert gf.encode_path(4, 32, 20, 1500) == "prow-32"
-    assert gf.encode_path(4, 32, 20, 2048) == "column-words"      # 2 tiles for 512 words: 67%
-    assert gf.encode_path(4, 32, 12, 4096) == "prow-16"
+    assert gf.encode_path(4, 32, 20, 2052) == "column-words"      # 2 tiles for 513 words: 67%
+    assert gf.encode_path(4, 32, 12, 4100) == "prow-16"
     assert gf.encode_path(4, 32, 12, 1500) == "column-words"
-    assert gf.encode_path(2, 32, 20, 4096) == "column-words"
+    assert gf.encode_path(2, 32, 20, 4100) == "column-words"
+    assert gf.encode_path(2, 32, 20, 4096) == "tmem"
+    assert gf.encode_path(2, 32, 8, 4096) == "column-words"     # K = 8: the column kernel
     assert gf.encode_path(4, 64, 64, 1500) == "lanek-64"
+    assert gf.encode_path(4, 64, 64, 4096) == "tmem"
     assert gf.encode_path(2, 32, 32, 1 << 20) == "tmem"         # C5 GF(2): TMEM lookup tables
     assert gf.encode_path(4, 32, 32, 1 << 20) == "tmem"         # C5 GF(4)
     assert gf.encode_path(2, 33, 32, 1 << 20) == "tmem"         # GF(2), N > 32
     assert gf.encode_path(4, 32, 32, 1 << 20, a_align=8) == "lanek-32"   # TMEM engine: 16-byte aligned
     assert gf.encode_path(4, 32, 32, 4096 + 8) == "lanek-32"    # ... and M % 16 == 0
-    assert gf.encode_path(2, 32, 32, 2048) == "gf2-split"       # M < 4096: the split engine
-    assert gf.encode_path(2, 33, 32, 2048) == "lanek-32"        # GF(2), N > 32, short packets
-    assert gf.encode_path(4, 32, 16, 1 << 20) == "prow-16"      # K < 24
-    assert gf.encode_path(16, 32, 32, 1 << 20) == "prow-32"     # GF(16)/GF(256) keep the product rows
+    assert gf.encode_path(2, 32, 32, 240) == "gf2-split"        # M < 256: the split engine
+    assert gf.encode_path(2, 33, 32, 240) == "lanek-32"         # GF(2), N > 32, short packets
+    assert gf.encode_path(4, 32, 16, 1 << 20) == "tmem"
+    assert gf.encode_path(16, 32, 32, 1 << 20) == "tmem"        # GF(16), 24 <= K <= 32
+    assert gf.encode_path(16, 32, 16, 1 << 20) == "prow-16"
+    assert gf.encode_path(16, 32, 64, 1 << 20) == "tmem"        # K > 32, N <= 32
+    assert gf.encode_path(16, 64, 64, 1 << 20) == "prow-nib"
+    assert gf.encode_path(256, 32, 32, 1 << 20) == "prow-32"    # GF(256) keeps the product rows
     assert gf.encode_path(2, 32, 32, 1500) == "lanek-32"        # GF(2), M % 16 != 0
     assert gf.encode_path(2, 32, 32, 4096, a_align=4) == "lanek-32"
-    assert gf.encode_path(2, 16, 24, 2048) == "gf2-split"
+    assert gf.encode_path(2, 16, 24, 128) == "gf2-split"
     assert gf.encode_path(2, 16, 24, 4096) == "tmem"
     assert gf.encode_path(256, 16, 1, 1024) == "stream"         # NEXT-2 (paper: N = 16, K = 1)
     assert gf.encode_path(2, 16, 4, 65536) == "stream"

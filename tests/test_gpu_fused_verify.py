@@ -119,11 +119,12 @@ def test_fused_verify_forced_tmem(gfm, q):
         gfm.set_encode_path("auto")
 
 
-@pytest.mark.parametrize("q", (16, 256))
+@pytest.mark.parametrize("q", (2, 4, 16, 256))
 def test_fused_verify_forced_lanek(gfm, q):
-    """The lane-k kernel's fused check for GF(16) / GF(256) (forced: the router
-    sends these fields to the product-row kernels), 32 and 64 coded packets per
-    CTA, with and without an injected fault."""
+    """The lane-k kernel's fused check (forced: the router sends GF(16) / GF(256)
+    to the product-row kernels and most GF(2) / GF(4) shapes to the TMEM
+    engine), 32 and 64 coded packets per CTA, with and without an injected
+    fault."""
     gfm.set_encode_path("lanek")
     try:
         for N, K, M, batch in ((20, 30, 1540, 3), (20, 40, 1540, 3)):
