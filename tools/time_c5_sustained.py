@@ -1,4 +1,4 @@
-"""GF(2) C5 split engine: per-launch time of 256-generation launches over a
+"""GF(2) C5 encode (default kernel: the TMEM engine since 0.2.01): per-launch time of 256-generation launches over a
 long back-to-back run (does the board's 1 kW power cap slow it down?), with
 nvidia-smi clocks / power sampled alongside."""
 import os
