@@ -560,9 +560,9 @@ static int launch_tmem(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, in
     return GF_EARG;
 }
 
-// the TMEM engine with the check fused (GF(2) / GF(4), K <= 64): 12 warps per
-// CTA for GF(4) (the check's registers), 8 for GF(2); 8 / 4 when the per-warp
-// shared memory does not fit
+// the TMEM engine with the check fused (GF(2) / GF(4) / GF(16), K <= 64): 12
+// warps per CTA for GF(4), 8 otherwise; 8 / 4 when the per-warp shared memory
+// does not fit
 template <int LOGW, int T>
 static int launch_tmem_check(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M, size_t batch,
                              cudaStream_t st, const TmParams *vp)
@@ -844,7 +844,7 @@ static int configure_field(int optin, uint32_t smem_base)
     }
     if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<log2_field(F), tm_wpc<log2_field(F)>()>, optin);
     if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<log2_field(F), tm_wpc2<log2_field(F)>()>, optin);
-    if constexpr (F <= 4) {
+    if constexpr (F <= 16) {
         constexpr int L = log2_field(F), W0 = L == 1 ? 12 : 8, W1 = L == 1 ? 8 : 4;
         if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<L, W0, 1>, optin);
         if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<L, W0, 2>, optin);
@@ -1208,12 +1208,15 @@ int gf_encode_verify_batch(int field, const uint8_t *A, const uint8_t *C, uint8_
                                                                       field - 1);
     if ((rc = launch_status()) != GF_OK) return rc;
     const int path = encode_path(field, N, K, M, A, B);
-    if (path == 14 && field <= 4 && K <= 64) {                 // fused: the TMEM engine
+    if (path == 14 && field <= 16 && K <= 64) {                // fused: the TMEM engine
         TmParams vp{};
         vp.U = U; vp.RB = RB; vp.kw = kw; vp.mismatch = mismatch; vp.fault = tls_fault;
         if (field == 2)
             return t == 1 ? launch_tmem_check<0, 1>(A, C, B, N, K, M, batch, st, &vp)
                           : launch_tmem_check<0, 2>(A, C, B, N, K, M, batch, st, &vp);
+        if (field == 16)
+            return t == 1 ? launch_tmem_check<2, 1>(A, C, B, N, K, M, batch, st, &vp)
+                          : launch_tmem_check<2, 2>(A, C, B, N, K, M, batch, st, &vp);
         return t == 1 ? launch_tmem_check<1, 1>(A, C, B, N, K, M, batch, st, &vp)
                       : launch_tmem_check<1, 2>(A, C, B, N, K, M, batch, st, &vp);
     }

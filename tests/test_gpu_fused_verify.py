@@ -60,7 +60,8 @@ CASES = [  # (q, N, K, M, batch, expected kernel)
     # a partial last group (N = 33), a ragged last span, several generations
     # per warp; K > 64 runs the streaming check after it
     (4, 33, 64, 4112, 3, "tmem"), (2, 64, 64, 8192, 2, "tmem"), (4, 32, 40, 20480, 2, "tmem"),
-    (2, 7, 24, 4096, 40, "tmem"), (4, 32, 70, 4096, 2, "tmem")]
+    (2, 7, 24, 4096, 40, "tmem"), (4, 32, 70, 4096, 2, "tmem"), (16, 32, 32, 4096, 3, "tmem"),
+    (16, 20, 60, 2048, 2, "tmem")]
 
 
 @pytest.mark.parametrize("q,N,K,M,batch,kern", CASES)
@@ -91,7 +92,7 @@ def test_fused_verify_matches_oracle(gfm, q, N, K, M, batch, kern, t):
     assert got.sum() == got[batch // 2]
 
 
-@pytest.mark.parametrize("q", (2, 4))
+@pytest.mark.parametrize("q", (2, 4, 16))
 def test_fused_verify_forced_tmem(gfm, q):
     """The TMEM engine's fused check on short packets (forced: the router sends
     packets below 4 KiB elsewhere), one and two projections, with and without
