@@ -27,7 +27,9 @@
  *           no lock and no kernel-attribute call inside gf_maddrc / gf_mulrc /
  *           gf_encode_batch (and gf_invert_batch / gf_decode_batch /
  *           gf_verify_batch): gf_init prepares everything once per (device,
- *           field), so these calls may be captured into a CUDA graph.
+ *           field), so these calls may be captured into a CUDA graph.  (The
+ *           TMEM engine encodes a TMA tensor map of A on the host per launch:
+ *           host-only work, no driver round trip.)
  */
 #ifndef GFRLNC_H
 #define GFRLNC_H
@@ -53,7 +55,8 @@ enum {
  * and upload them to the CURRENT device (Alg. 1 tables tl/th,
  * re-cut for the GPU into three byte-permute tables), and
  * prepare the field's kernels on that device (dynamic shared-memory opt-ins,
- * the product-row kernel's shared-window probe).  Allocates and synchronises
+ * the product-row kernel's shared-window probe, the TMEM engine's tensor-map
+ * encoder from the driver).  Allocates and synchronises
  * (not a hot-path call).  Idempotent and thread-safe; call once per (device,
  * field) before any other call for that field.  Returns GF_OK, GF_EFIELD or
  * GF_ECUDA. */

@@ -958,6 +958,7 @@ int gf_init(int field)
             g_sm_count[dev] = sms;
         }
         if (configure_kernels(field, dev) != GF_OK) return GF_ECUDA;
+        if (!tm_resolve_encoder()) return GF_ECUDA;   // the TMEM engine's tensor-map encoder
         void *sym;                               // cache the table addresses (no symbol lookups at launch)
         if (symbol_address(0, &sym) != GF_OK || symbol_address(1, &sym) != GF_OK ||
             symbol_address(2, &sym) != GF_OK)
