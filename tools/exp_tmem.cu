@@ -75,7 +75,7 @@ static void run(int N, int K, size_t M, size_t G, int reps)
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int blocks = (int)((p.units + (uint64_t)WPC * p.upw - 1) / ((uint64_t)WPC * p.upw));
     CUtensorMap map;
-    if (!tm_make_map(&map, A, (uint64_t)G * N, M, LOGW)) { printf("tensor map failed\n"); exit(1); }
+    if (!tm_resolve_encoder() || !tm_make_map(&map, A, (uint64_t)G * N, M, LOGW)) { printf("tensor map failed\n"); exit(1); }
     kern<<<blocks, WPC * 32, smem>>>(p, map);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("GF(%d) launch error %s (smem %zu)\n", q, cudaGetErrorString(e), smem); exit(1); }
