@@ -23,15 +23,18 @@
 // memory datapath beside the shared-memory pipe (~200-270 B/clk
 // per SM from ordinary warps, tools/ubench_tmem.cu).
 //
-// Layout: warp wid owns TMEM lanes 32 (wid % 4) .. +31 and 64 columns
-// (2 groups x 16 combos x 2 words).  Lane l holds words 2l, 2l+1 of a 64-word
-// (256-byte) span of every packet; a work unit is (generation, span), and
-// each warp walks a contiguous range of units.  A unit is processed in passes
-// of 32 coded packets (accumulators acc[32][2] in registers) and steps of 2
-// groups: per step the lane builds the 2 x 16 combos of its two words
-// (11 XORs per group and word, plus the field's x-multiples), stores them with
-// one tcgen05.st.32x32b.x32 per group, and each coded packet XORs two
-// tcgen05.ld.32x32b.x2 results into its accumulator (one LOP3 per word).
+// Layout (W = 2 words per lane, the instantiated width): warp wid owns TMEM
+// lanes 32 (wid % 4) .. +31 and 128 columns (4 groups x 16 combos x 2 words).
+// Lane l holds words 2l, 2l+1 of a 64-word (256-byte) span of every packet; a
+// work unit is (generation, span), and each warp walks a contiguous range of
+// units.  A unit is processed in passes of 32 coded packets (accumulators
+// acc[32][2] in registers) and steps of 4 groups: per step the lane builds
+// the 4 x 16 combos of its two words (11 XORs per group and word, plus the
+// field's x-multiples), stores them with one tcgen05.st.32x32b.x32 per group,
+// and each coded packet XORs four tcgen05.ld.32x32b.x2 results into its
+// accumulator (two LOP3 per word).  (W = 4, .x4 loads and 16-byte stores,
+// compiles and is bit-exact but measured slower: 128 accumulator registers
+// spill at 8 warps.)
 // The TMEM column addresses of every (pass, group, k) are precomputed per
 // warp and generation in shared memory and read with broadcast LDS.128.
 // Source words stream through a per-warp ring of kTmRing steps: one lane
@@ -54,12 +57,13 @@
 
 namespace gfr {
 
-constexpr int kTmW = 2;                         // words per lane per span
-constexpr int kTmSpanWords = 32 * kTmW;         // 64 words = 256 bytes per warp and packet
+// W (template parameter, 2 or 4): 32-bit words per lane per span; a span is
+// 32 W words of every packet, a lookup one tcgen05.ld.32x32b.xW
 constexpr int kTmKB = 32;                       // coded packets per pass
 constexpr int kTmGPB = 4;                       // groups per step
 constexpr int kTmRing = 4;                      // steps of source words in flight per warp
-constexpr int kTmColsPerWarp = kTmGPB * 16 * kTmW;   // 128
+__host__ __device__ constexpr int tm_span_words(int W) { return 32 * W; }
+__host__ __device__ constexpr int tm_cols_per_warp(int W) { return kTmGPB * 16 * W; }   // 128 / 256
 
 struct TmParams {
     const uint8_t *A;      // [batch][N][M]
@@ -88,10 +92,10 @@ __host__ __device__ constexpr int tm_sps(int logw) { return (4 * kTmGPB) >> logw
 // then the source ring, then one mbarrier per ring stage
 __host__ __device__ constexpr size_t tm_tab_bytes(int NG, int passes) { return (size_t)passes * NG * kTmKB * 4; }
 __host__ __device__ constexpr size_t tm_tabu_bytes(int NG, int T) { return ((size_t)NG * T * 4 + 127) / 128 * 128; }
-__host__ __device__ constexpr size_t tm_warp_bytes(int logw, int NG, int passes, int T = 0)
+__host__ __device__ constexpr size_t tm_warp_bytes(int logw, int NG, int passes, int T = 0, int W = 2)
 {
     // (a multiple of 128 bytes: TMA destinations are 128-byte aligned)
-    return (tm_tab_bytes(NG, passes) + tm_tabu_bytes(NG, T) + (size_t)kTmRing * tm_sps(logw) * kTmSpanWords * 4 + kTmRing * 8 + 127) / 128 * 128;
+    return (tm_tab_bytes(NG, passes) + tm_tabu_bytes(NG, T) + (size_t)kTmRing * tm_sps(logw) * tm_span_words(W) * 4 + kTmRing * 8 + 127) / 128 * 128;
 }
 
 // x * a on packed w-bit elements (bit j of an element = coefficient of x^j)
@@ -126,6 +130,18 @@ __device__ __forceinline__ void tm_ld2(uint32_t taddr, uint32_t &x, uint32_t &y)
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(x), "=r"(y) : "r"(taddr));
 }
 
+__device__ __forceinline__ void tm_ld4(uint32_t taddr, uint32_t *x)
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]) : "r"(taddr));
+}
+template <int W>
+__device__ __forceinline__ void tm_ldw(uint32_t taddr, uint32_t *x)
+{
+    if constexpr (W == 2) tm_ld2(taddr, x[0], x[1]);
+    else tm_ld4(taddr, x);
+}
+
 // wait for this thread's outstanding tcgen05.ld; the loaded registers pass
 // through the asm so that no use of them is scheduled above the wait
 #define TM_P8(v, o) "+r"(v[o]), "+r"(v[o + 1]), "+r"(v[o + 2]), "+r"(v[o + 3]), "+r"(v[o + 4]), "+r"(v[o + 5]), "+r"(v[o + 6]), "+r"(v[o + 7])
@@ -157,7 +173,7 @@ __device__ __forceinline__ void tm_unroll_i(F &&f)
 template <int NI, class F>
 __device__ __forceinline__ void tm_unroll(F &&f) { tm_unroll_i<0, NI>(f); }
 
-// one TMA tile load (box SPS rows x 256 bytes at byte x, row y of A) into
+// one TMA tile load (box SPS rows x 32 W words at word x, row y of A) into
 // shared memory, completing its bytes on an mbarrier
 __device__ __forceinline__ void tm_tma_load(uint32_t sdst, const CUtensorMap *map, uint32_t x, uint32_t y, uint32_t bar)
 {
@@ -184,19 +200,19 @@ static inline bool tm_resolve_encoder()
     return true;
 }
 
-// Host: the tensor map of A for the kernel's source ring (2-D: M bytes per
-// row, rows of stride M; box 256 bytes x SPS rows).  M % 16 == 0 and 16-byte
-// aligned A (TMA's stride / address rules).  Returns false when the encoder
-// was not resolved (tm_resolve_encoder) or the encode fails.
-static inline bool tm_make_map(CUtensorMap *map, const void *A, uint64_t rows, uint64_t M, int logw)
+// Host: the tensor map of A for the kernel's source ring (2-D: M / 4 words
+// per row, rows of stride M bytes; box 32 W words x SPS rows).  M % 16 == 0
+// and 16-byte aligned A (TMA's stride / address rules).  Returns false when
+// the encoder was not resolved (tm_resolve_encoder) or the encode fails.
+static inline bool tm_make_map(CUtensorMap *map, const void *A, uint64_t rows, uint64_t M, int logw, int W = 2)
 {
     const PFN_cuTensorMapEncodeTiled_v12000 fn = __atomic_load_n(&tm_encode_fn(), __ATOMIC_ACQUIRE);
     if (!fn) return false;
-    const cuuint64_t dims[2] = {M, rows};
+    const cuuint64_t dims[2] = {M / 4, rows};
     const cuuint64_t strides[1] = {M};
-    const cuuint32_t box[2] = {(cuuint32_t)(kTmSpanWords * 4), (cuuint32_t)tm_sps(logw)};
+    const cuuint32_t box[2] = {(cuuint32_t)tm_span_words(W), (cuuint32_t)tm_sps(logw)};
     const cuuint32_t estr[2] = {1, 1};
-    return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(A), dims, strides, box, estr,
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void *>(A), dims, strides, box, estr,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -206,7 +222,7 @@ __device__ __forceinline__ void tm_expect_tx(uint32_t bar, uint32_t bytes)
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
 }
 
-// Grid: 1-D, WPC warps per block, one block per SM (TMEM: WPC / 4 x 128 columns).
+// Grid: 1-D, WPC warps per block, one block per SM (TMEM: WPC / 4 x 64 W columns).
 //
 // T > 0: the fused Freivalds check of gf_encode_verify_batch (SURVEY 8(c) step
 // 7, 8(f) NEXT-4) with T binary projections r_j (K <= 64): B == A C iff
@@ -217,14 +233,16 @@ __device__ __forceinline__ void tm_expect_tx(uint32_t bar, uint32_t bytes)
 // end of a unit the differing bytes of y1_j and y2_j are counted into
 // mismatch[g].  FT: the harness fault injection (gf_set_verify_fault), a
 // separate instantiation.
-template <int LOGW, int WPC, int T = 0, bool FT = false>
+template <int LOGW, int WPC, int T = 0, bool FT = false, int W = 2>
 __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, const __grid_constant__ CUtensorMap tmA)
 {
     constexpr int w = 1 << LOGW;
     constexpr int SPS = tm_sps(LOGW);
     constexpr int SPG = SPS / kTmGPB > 0 ? SPS / kTmGPB : 1;      // sources per group (GF(256): 2 groups per source)
-    static_assert((WPC / 4) * kTmColsPerWarp <= 512, "TMEM columns");
-    constexpr uint32_t kCols = (WPC / 4) * kTmColsPerWarp <= 128 ? 128 : (WPC / 4) * kTmColsPerWarp <= 256 ? 256 : 512;
+    constexpr int SW = tm_span_words(W), CPW = tm_cols_per_warp(W);
+    static_assert(W == 2 || W == 4, "2 or 4 words per lane");
+    static_assert((WPC / 4) * CPW <= 512, "TMEM columns");
+    constexpr uint32_t kCols = (WPC / 4) * CPW <= 128 ? 128 : (WPC / 4) * CPW <= 256 ? 256 : 512;
     extern __shared__ __align__(1024) uint8_t smem8[];
     __shared__ uint32_t s_tbase;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -236,18 +254,18 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, co
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    // this warp's TMEM: lanes 32 (wid % 4) .., columns (wid / 4) * 128 ..
-    const uint32_t tb = s_tbase + ((uint32_t)(32 * (wid & 3)) << 16) + (uint32_t)(wid >> 2) * kTmColsPerWarp;
+    // this warp's TMEM: lanes 32 (wid % 4) .., columns (wid / 4) * CPW ..
+    const uint32_t tb = s_tbase + ((uint32_t)(32 * (wid & 3)) << 16) + (uint32_t)(wid >> 2) * CPW;
 
     const int N = p.N, K = p.K, NG = p.NG, passes = p.passes, steps = NG / kTmGPB;
     const uint32_t Mw = p.Mw, spans = p.spans;
     const size_t tabb = tm_tab_bytes(NG, passes);
-    uint8_t *wbase = smem8 + (size_t)wid * tm_warp_bytes(LOGW, NG, passes, T);
+    uint8_t *wbase = smem8 + (size_t)wid * tm_warp_bytes(LOGW, NG, passes, T, W);
     uint32_t *tab = reinterpret_cast<uint32_t *>(wbase);
     uint32_t *tabu = reinterpret_cast<uint32_t *>(wbase + tabb);               // [NG][T]
     const uint32_t *ring = reinterpret_cast<const uint32_t *>(wbase + tabb + tm_tabu_bytes(NG, T));
     const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
-    const uint32_t bar_s = ring_s + kTmRing * SPS * kTmSpanWords * 4;
+    const uint32_t bar_s = ring_s + kTmRing * SPS * SW * 4;
     if (lane < kTmRing) mbar_init(bar_s + 8 * lane, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncwarp();
@@ -275,15 +293,15 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, co
     Cur pc{u0 / spans, (uint32_t)(u0 % spans), 0, 0, 0};
     Cur cc = pc;
     // producer: one TMA tile load per step, rows g N + gs SPS .. + SPS - 1,
-    // bytes sp * 256 .. + 255 (rows past the generation's N belong to the next
+    // words sp SW .. + SW - 1 (rows past the generation's N belong to the next
     // one or lie past the end of A, and only meet zero coefficients; bytes past
     // the packet end belong to lanes that never store)
     auto issue = [&]() {
         if (pc.t < nsteps) {
             if (lane == 0) {
                 const uint32_t st = (uint32_t)(pc.t % kTmRing);
-                tm_expect_tx(bar_s + 8 * st, SPS * kTmSpanWords * 4u);
-                tm_tma_load(ring_s + st * (SPS * kTmSpanWords * 4u), &tmA, pc.sp * (kTmSpanWords * 4u),
+                tm_expect_tx(bar_s + 8 * st, SPS * SW * 4u);
+                tm_tma_load(ring_s + st * (SPS * SW * 4u), &tmA, pc.sp * (uint32_t)SW,
                             (uint32_t)(pc.g * N) + (uint32_t)(pc.gs * SPS), bar_s + 8 * st);
             }
             advance(pc);
@@ -296,13 +314,19 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, co
     uint64_t cur_g = ~0ull;
     uint32_t bad = 0;                                // check: differing bytes of this warp's current generation
     int fk = -1;                                     // FT: coded packet to corrupt in this generation
-    uint32_t y1[T > 0 ? T : 1][2], y2[T > 0 ? T : 1][2], rw[T > 0 ? T : 1];
+    uint32_t y1[T > 0 ? T : 1][W], y2[T > 0 ? T : 1][W], rw[T > 0 ? T : 1];
 #pragma unroll
-    for (int j = 0; j < (T > 0 ? T : 1); j++) y1[j][0] = y1[j][1] = y2[j][0] = y2[j][1] = rw[j] = 0u;
+    for (int j = 0; j < (T > 0 ? T : 1); j++) {
+        rw[j] = 0u;
+#pragma unroll
+        for (int wd = 0; wd < W; wd++) y1[j][wd] = y2[j][wd] = 0u;
+    }
     (void)fk; (void)y1; (void)y2; (void)rw;
-    uint32_t acc[kTmKB][2];
+    uint32_t acc[kTmKB][W];
 #pragma unroll
-    for (int k = 0; k < kTmKB; k++) acc[k][0] = acc[k][1] = 0u;
+    for (int k = 0; k < kTmKB; k++)
+#pragma unroll
+        for (int wd = 0; wd < W; wd++) acc[k][wd] = 0u;
 
 #pragma unroll 1
     for (int64_t t = 0; t < nsteps; t++) {
@@ -334,7 +358,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, co
                         if (i < N) idx |= ((__ldg(Cg + (size_t)i * K + k) >> j) & 1u) << b;
                     }
                 }
-                tab[e] = tb + (uint32_t)sl * (16 * kTmW) + idx * kTmW;
+                tab[e] = tb + (uint32_t)sl * (16 * W) + idx * W;
             }
             if constexpr (T > 0) {
                 const uint8_t *Ug = p.U + g * 2 * (size_t)N;
@@ -346,78 +370,89 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, co
                         const int tt = 4 * grp + b, i = tt >> LOGW, jj = tt & (w - 1);
                         if (i < N) idx |= ((__ldg(Ug + (size_t)j * N + i) >> jj) & 1u) << b;
                     }
-                    tabu[e] = tb + (uint32_t)(grp % kTmGPB) * (16 * kTmW) + idx * kTmW;
+                    tabu[e] = tb + (uint32_t)(grp % kTmGPB) * (16 * W) + idx * W;
                 }
             }
             __syncwarp();
         }
         mbar_wait(bar_s + 8 * (uint32_t)(t % kTmRing), (uint32_t)(t / kTmRing) & 1u);   // stage t has landed
-        const uint32_t *rs = ring + (size_t)(t % kTmRing) * SPS * kTmSpanWords + 2 * lane;
-        uint32_t hi4[SPG][2];                        // GF(256): x^4 a of the step's sources
+        const uint32_t *rs = ring + (size_t)(t % kTmRing) * SPS * SW + W * lane;
+        uint32_t hi4[SPG][W];                        // GF(256): x^3 a of the step's source
         (void)hi4;
 #pragma unroll
         for (int sl = 0; sl < kTmGPB; sl++) {
-            uint32_t e[4][2];
+            uint32_t e[4][W];
 #pragma unroll
-            for (int wd = 0; wd < 2; wd++) {
+            for (int wd = 0; wd < W; wd++) {
                 if constexpr (LOGW == 0) {
 #pragma unroll
-                    for (int b = 0; b < 4; b++) e[b][wd] = rs[(sl * 4 + b) * kTmSpanWords + wd];
+                    for (int b = 0; b < 4; b++) e[b][wd] = rs[(sl * 4 + b) * SW + wd];
                 } else if constexpr (LOGW == 1) {
-                    const uint32_t a = rs[(sl * 2) * kTmSpanWords + wd], c = rs[(sl * 2 + 1) * kTmSpanWords + wd];
+                    const uint32_t a = rs[(sl * 2) * SW + wd], c = rs[(sl * 2 + 1) * SW + wd];
                     e[0][wd] = a; e[1][wd] = tm_xtime<1>(a); e[2][wd] = c; e[3][wd] = tm_xtime<1>(c);
                 } else if constexpr (LOGW == 2) {
-                    const uint32_t a = rs[sl * kTmSpanWords + wd];
+                    const uint32_t a = rs[sl * SW + wd];
                     e[0][wd] = a; e[1][wd] = tm_xtime<2>(a); e[2][wd] = tm_xtime<2>(e[1][wd]);
                     e[3][wd] = tm_xtime<2>(e[2][wd]);
                 } else {
-                    const uint32_t a = (sl & 1) ? tm_xtime<3>(hi4[0][wd]) : rs[(sl >> 1) * kTmSpanWords + wd];
+                    const uint32_t a = (sl & 1) ? tm_xtime<3>(hi4[0][wd]) : rs[(sl >> 1) * SW + wd];
                     e[0][wd] = a; e[1][wd] = tm_xtime<3>(a); e[2][wd] = tm_xtime<3>(e[1][wd]);
                     e[3][wd] = tm_xtime<3>(e[2][wd]);
                     if (!(sl & 1)) hi4[0][wd] = e[3][wd];     // x^3 a; x^4 a = x * that
                 }
             }
+            // combos c = 0 .. 15 at columns c W + wd, stored 32 registers at a time
+            // (W = 2: all 16 combos; W = 4: combos 0-7, then 8-15 = e3 ^ those)
             uint32_t v[32];
 #pragma unroll
-            for (int wd = 0; wd < 2; wd++) {
-                v[0 + wd] = 0u;
-                v[2 + wd] = e[0][wd];
-                v[4 + wd] = e[1][wd];
-                v[6 + wd] = e[0][wd] ^ e[1][wd];
+            for (int wd = 0; wd < W; wd++) {
+                v[0 * W + wd] = 0u;
+                v[1 * W + wd] = e[0][wd];
+                v[2 * W + wd] = e[1][wd];
+                v[3 * W + wd] = e[0][wd] ^ e[1][wd];
 #pragma unroll
-                for (int c = 4; c < 8; c++) v[2 * c + wd] = e[2][wd] ^ v[2 * (c - 4) + wd];
+                for (int c = 4; c < 8; c++) v[c * W + wd] = e[2][wd] ^ v[(c - 4) * W + wd];
+                if constexpr (W == 2) {
 #pragma unroll
-                for (int c = 8; c < 16; c++) v[2 * c + wd] = e[3][wd] ^ v[2 * (c - 8) + wd];
+                    for (int c = 8; c < 16; c++) v[c * W + wd] = e[3][wd] ^ v[(c - 8) * W + wd];
+                }
             }
-            tm_st32(tb + (uint32_t)sl * (16 * kTmW), v);
+            tm_st32(tb + (uint32_t)sl * (16 * W), v);
+            if constexpr (W == 4) {
+#pragma unroll
+                for (int c = 0; c < 8; c++)
+#pragma unroll
+                    for (int wd = 0; wd < W; wd++) v[c * W + wd] ^= e[3][wd];
+                tm_st32(tb + (uint32_t)sl * (16 * W) + 32, v);
+            }
         }
         tm_wait_st();
         const uint4 *ta = reinterpret_cast<const uint4 *>(tab + ((size_t)pass * steps + gs) * (kTmKB * kTmGPB));
         const int kpass = K - pass * kTmKB;          // coded packets of this pass (warp-uniform)
-        // one kq step: lookups of coded packets 4 kq .. 4 kq + 3
+        // one kq step: lookups of coded packets 4 kq .. 4 kq + 3, in two
+        // half-batches of 2 coded packets x 4 groups (8 loads in flight per wait)
         auto kstep = [&](auto kqc) {
             constexpr int kq = decltype(kqc)::value;
             uint4 a4[kTmGPB];                       // addresses of k = 4 kq .. 4 kq + 3, per group
 #pragma unroll
             for (int sl = 0; sl < kTmGPB; sl++) a4[sl] = ta[kq * kTmGPB + sl];
-            // two half-batches of 2 coded packets x 4 groups (8 loads in flight
-            // per wait: fewer live registers than 16)
 #pragma unroll
             for (int h = 0; h < 2; h++) {
-                uint32_t r[16];
+                uint32_t r[8 * W];                  // [kk][sl][wd]
 #pragma unroll
                 for (int sl = 0; sl < kTmGPB; sl++) {
-                    tm_ld2(h ? a4[sl].z : a4[sl].x, r[sl * 2], r[sl * 2 + 1]);
-                    tm_ld2(h ? a4[sl].w : a4[sl].y, r[8 + sl * 2], r[8 + sl * 2 + 1]);
+                    tm_ldw<W>(h ? a4[sl].z : a4[sl].x, r + (0 * kTmGPB + sl) * W);
+                    tm_ldw<W>(h ? a4[sl].w : a4[sl].y, r + (1 * kTmGPB + sl) * W);
                 }
-                tm_wait_ld16(r);
+                if constexpr (W == 2) tm_wait_ld16(*reinterpret_cast<uint32_t(*)[16]>(r));
+                else tm_wait_ld32(*reinterpret_cast<uint32_t(*)[32]>(r));
 #pragma unroll
                 for (int kk = 0; kk < 2; kk++)
 #pragma unroll
-                    for (int wd = 0; wd < 2; wd++) {
+                    for (int wd = 0; wd < W; wd++) {
                         uint32_t &y = acc[kq * 4 + 2 * h + kk][wd];
-                        const uint32_t x = y ^ r[kk * 8 + wd] ^ r[kk * 8 + 2 + wd];
-                        y = x ^ r[kk * 8 + 4 + wd] ^ r[kk * 8 + 6 + wd];
+                        const uint32_t x = y ^ r[(kk * kTmGPB + 0) * W + wd] ^ r[(kk * kTmGPB + 1) * W + wd];
+                        y = x ^ r[(kk * kTmGPB + 2) * W + wd] ^ r[(kk * kTmGPB + 3) * W + wd];
                     }
             }
         };
@@ -431,55 +466,68 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, co
 #pragma unroll
                 for (int j = 0; j < T; j++) rw[j] = __ldg(p.RB + (g * 2 + j) * (size_t)p.kw + pass);
             if (pass == 0) {                         // A side: u_j's 4-bit index per group, same tables
-                uint32_t r[32];
+                uint32_t r[32];                      // kTmGPB T W <= 32
 #pragma unroll
                 for (int e = 0; e < 32; e++) r[e] = 0u;
                 const uint32_t *tu = tabu + (size_t)gs * kTmGPB * T;
 #pragma unroll
-                for (int e = 0; e < kTmGPB * T; e++) tm_ld2(tu[e], r[2 * e], r[2 * e + 1]);
+                for (int e = 0; e < kTmGPB * T; e++) tm_ldw<W>(tu[e], r + W * e);
                 tm_wait_ld32(r);
 #pragma unroll
-                for (int e = 0; e < kTmGPB * T; e++) {
-                    y1[e % T][0] ^= r[2 * e];
-                    y1[e % T][1] ^= r[2 * e + 1];
-                }
+                for (int e = 0; e < kTmGPB * T; e++)
+#pragma unroll
+                    for (int wd = 0; wd < W; wd++) y1[e % T][wd] ^= r[W * e + wd];
             }
         }
         if (gs == steps - 1) {                       // the pass is complete: store and reset
-            const uint32_t wi = cc.sp * kTmSpanWords + 2 * lane;
+            const uint32_t wi = cc.sp * SW + W * lane;
             uint32_t *Bg = reinterpret_cast<uint32_t *>(p.B) + (g * K + (size_t)pass * kTmKB) * Mw + wi;
             const int kn = K - pass * kTmKB;
             if constexpr (T > 0) {
 #pragma unroll
                 for (int k = 0; k < kTmKB; k++) {
                     if constexpr (FT)
-                        if (pass * kTmKB + k == fk && wi == ((uint32_t)p.fault & 0xFFFFEu)) {
-                            if (p.fault & 1u) acc[k][1] ^= 0x5Au;      // harness: one wrong byte
-                            else acc[k][0] ^= 0x5Au;
+                        if (pass * kTmKB + k == fk && wi == ((uint32_t)p.fault & 0xFFFFFu & ~(uint32_t)(W - 1))) {
+#pragma unroll
+                            for (int wd = 0; wd < W; wd++)          // harness: one wrong byte
+                                if ((p.fault & (W - 1)) == (uint64_t)wd) acc[k][wd] ^= 0x5Au;
                         }
 #pragma unroll
                     for (int j = 0; j < T; j++)
-                        if ((rw[j] >> k) & 1u) { y2[j][0] ^= acc[k][0]; y2[j][1] ^= acc[k][1]; }
+                        if ((rw[j] >> k) & 1u) {
+#pragma unroll
+                            for (int wd = 0; wd < W; wd++) y2[j][wd] ^= acc[k][wd];
+                        }
                 }
             }
             if (wi < Mw) {                           // row k of the pass: one pointer step of Mw words
                 uint32_t *q = Bg;
 #pragma unroll
                 for (int k = 0; k < kTmKB; k++) {
-                    if (k < kn)
-                        asm volatile("st.global.v2.u32 [%0], {%1,%2};" :: "l"(q), "r"(acc[k][0]), "r"(acc[k][1])
-                                     : "memory");
+                    if (k < kn) {
+                        if constexpr (W == 2)
+                            asm volatile("st.global.v2.u32 [%0], {%1,%2};" :: "l"(q), "r"(acc[k][0]), "r"(acc[k][1])
+                                         : "memory");
+                        else
+                            asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" :: "l"(q), "r"(acc[k][0]),
+                                         "r"(acc[k][1]), "r"(acc[k][2]), "r"(acc[k][3]) : "memory");
+                    }
                     q += Mw;
                 }
             }
 #pragma unroll
-            for (int k = 0; k < kTmKB; k++) acc[k][0] = acc[k][1] = 0u;
+            for (int k = 0; k < kTmKB; k++)
+#pragma unroll
+                for (int wd = 0; wd < W; wd++) acc[k][wd] = 0u;
             if constexpr (T > 0) {
                 if (pass == passes - 1) {            // the unit is complete: compare the projections
 #pragma unroll
                     for (int j = 0; j < T; j++) {
-                        if (wi < Mw) bad += nz_bytes(y1[j][0] ^ y2[j][0]) + nz_bytes(y1[j][1] ^ y2[j][1]);
-                        y1[j][0] = y1[j][1] = y2[j][0] = y2[j][1] = 0u;
+#pragma unroll
+                        for (int wd = 0; wd < W; wd++) {
+                            if (wi < Mw) bad += nz_bytes(y1[j][wd] ^ y2[j][wd]);
+                            y1[j][wd] = y2[j][wd] = 0u;
+                        }
                     }
                 }
             }

@@ -532,7 +532,7 @@ static int launch_tmem_w(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, 
         }
         p.A = A + g0 * N * M; p.C = C + g0 * N * K; p.B = B + g0 * K * M; p.N = N; p.K = K;
         p.Mw = (uint32_t)(M / 4);
-        p.spans = (p.Mw + kTmSpanWords - 1) / kTmSpanWords;
+        p.spans = (p.Mw + tm_span_words(2) - 1) / tm_span_words(2);
         p.NG = tm_groups(LOGW, N);
         p.passes = (K + kTmKB - 1) / kTmKB;
         p.units = (uint64_t)nb * p.spans;

@@ -45,7 +45,7 @@ static uint8_t hmul_packed(int q, uint8_t c, uint8_t a)
     return r;
 }
 
-template <int LOGW, int WPC>
+template <int LOGW, int WPC, int W = 2>
 static void run(int N, int K, size_t M, size_t G, int reps)
 {
     const int q = 1 << (1 << LOGW);
@@ -60,7 +60,7 @@ static void run(int N, int K, size_t M, size_t G, int reps)
     TmParams p{};
     p.A = A; p.C = C; p.B = B;
     p.Mw = (uint32_t)(M / 4);
-    p.spans = (p.Mw + kTmSpanWords - 1) / kTmSpanWords;
+    p.spans = (p.Mw + tm_span_words(W) - 1) / tm_span_words(W);
     p.N = N; p.K = K;
     const int w = 1 << LOGW;
     int NG = (N * w + 3) / 4;
@@ -70,12 +70,12 @@ static void run(int N, int K, size_t M, size_t G, int reps)
     p.units = (uint64_t)G * p.spans;
     const uint64_t warps = (uint64_t)sms * WPC;
     p.upw = (p.units + warps - 1) / warps;
-    const size_t smem = (size_t)WPC * tm_warp_bytes(LOGW, NG, p.passes, 0);
-    auto kern = encode_tmem_kernel<LOGW, WPC>;
+    const size_t smem = (size_t)WPC * tm_warp_bytes(LOGW, NG, p.passes, 0, W);
+    auto kern = encode_tmem_kernel<LOGW, WPC, 0, false, W>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int blocks = (int)((p.units + (uint64_t)WPC * p.upw - 1) / ((uint64_t)WPC * p.upw));
     CUtensorMap map;
-    if (!tm_resolve_encoder() || !tm_make_map(&map, A, (uint64_t)G * N, M, LOGW)) { printf("tensor map failed\n"); exit(1); }
+    if (!tm_resolve_encoder() || !tm_make_map(&map, A, (uint64_t)G * N, M, LOGW, W)) { printf("tensor map failed\n"); exit(1); }
     kern<<<blocks, WPC * 32, smem>>>(p, map);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("GF(%d) launch error %s (smem %zu)\n", q, cudaGetErrorString(e), smem); exit(1); }
@@ -109,8 +109,8 @@ static void run(int N, int K, size_t M, size_t G, int reps)
     cudaEventElapsedTime(&ms, e0, e1);
     ms /= reps;
     const double src = (double)G * N * M;
-    printf("GF(%3d) N=%d K=%d M=%zu G=%zu WPC=%d blocks=%d smem=%zu: %.3f ms  %.1f GB/s source  (%.1f%% of 3273)  "
-           "check %zu/%zu bad\n", q, N, K, M, G, WPC, blocks, smem, ms, src / ms / 1e6, src / ms / 1e6 / 3273 * 100,
+    printf("GF(%3d) W=%d N=%d K=%d M=%zu G=%zu WPC=%d blocks=%d smem=%zu: %.3f ms  %.1f GB/s source  (%.1f%% of 3273)  "
+           "check %zu/%zu bad\n", q, W, N, K, M, G, WPC, blocks, smem, ms, src / ms / 1e6, src / ms / 1e6 / 3273 * 100,
            bad, checked);
     cudaFree(A); cudaFree(B); cudaFree(C);
 }
@@ -127,6 +127,13 @@ int main(int argc, char **argv)
         if (sel & 8) run<2, W>(32, 32, 1 << 20, 64, 5);                              \
         if (sel & 16) run<3, W>(64, 64, 1504, 16384, 5);                             \
         if (sel & 32) run<3, W>(32, 32, 1 << 20, 64, 5);                             \
+    }
+    if (wpc == 4) {                                  // W = 4 (4 words per lane), 8 warps
+        if (sel & 1) run<1, 8, 4>(32, 32, 1 << 20, 256, 5);
+        if (sel & 2) run<0, 8, 4>(32, 32, 1 << 20, 256, 5);
+        if (sel & 8) run<2, 8, 4>(32, 32, 1 << 20, 64, 5);
+        if (sel & 32) run<3, 8, 4>(32, 32, 1 << 20, 64, 5);
+        if (sel & 64) run<1, 4, 4>(32, 32, 1 << 20, 256, 5);
     }
     RUNS(8)
     RUNS(12)
