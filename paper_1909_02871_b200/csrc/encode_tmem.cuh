@@ -89,13 +89,24 @@ __host__ __device__ constexpr int tm_sps(int logw) { return (4 * kTmGPB) >> logw
 
 // per-warp shared memory: TMEM addresses [passes][steps][kTmKB / 4][kTmGPB][4]
 // (one word per (pass, group, k)), the check's addresses [NG][T] (T > 0),
-// then the source ring, then one mbarrier per ring stage
+// the store staging tile [kTmKB][32 W] words, the source ring, then one
+// mbarrier per ring stage
 __host__ __device__ constexpr size_t tm_tab_bytes(int NG, int passes) { return (size_t)passes * NG * kTmKB * 4; }
+// B leaves through TMA stores from a staging tile for GF(4) / GF(16) / GF(256)
+// (C5 GF(4): 1.81 -> 2.06 TB/s: the per-row store addresses and their memory
+// descriptors had cost ~45 ALU instructions per step), through 8-byte STG
+// for GF(2), whose HBM-bound loop lost 7% with the TMA stores
+// (profiles/r02_exp_tmem_v9.txt)
+__host__ __device__ constexpr bool tm_tma_store_on(int logw) { return logw != 0; }
+__host__ __device__ constexpr size_t tm_stage_bytes(int logw, int W)
+{
+    return tm_tma_store_on(logw) ? (size_t)kTmKB * tm_span_words(W) * 4 : 0;
+}
 __host__ __device__ constexpr size_t tm_tabu_bytes(int NG, int T) { return ((size_t)NG * T * 4 + 127) / 128 * 128; }
 __host__ __device__ constexpr size_t tm_warp_bytes(int logw, int NG, int passes, int T = 0, int W = 2)
 {
     // (a multiple of 128 bytes: TMA destinations are 128-byte aligned)
-    return (tm_tab_bytes(NG, passes) + tm_tabu_bytes(NG, T) + (size_t)kTmRing * tm_sps(logw) * tm_span_words(W) * 4 + kTmRing * 8 + 127) / 128 * 128;
+    return (tm_tab_bytes(NG, passes) + tm_tabu_bytes(NG, T) + tm_stage_bytes(logw, W) + (size_t)kTmRing * tm_sps(logw) * tm_span_words(W) * 4 + kTmRing * 8 + 127) / 128 * 128;
 }
 
 // x * a on packed w-bit elements (bit j of an element = coefficient of x^j)
@@ -161,6 +172,15 @@ __device__ __forceinline__ void tm_wait_ld16(uint32_t (&v)[16])
 
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// one TMA tile store: box of 32 W words x kTmKB rows x 1 generation from
+// shared memory to B (3-D tensor map [batch][K][M / 4]: rows past K and words
+// past M are clipped by the hardware)
+__device__ __forceinline__ void tm_tma_store(const CUtensorMap *map, uint32_t x, uint32_t y, uint32_t z, uint32_t ssrc)
+{
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];"
+                 :: "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(ssrc) : "memory");
+}
+
 // f(integral_constant<int, i>) for i = 0 .. NI-1, unrolled at compile time
 template <int I, int NI, class F>
 __device__ __forceinline__ void tm_unroll_i(F &&f)
@@ -180,6 +200,10 @@ __device__ __forceinline__ void tm_tma_load(uint32_t sdst, const CUtensorMap *ma
     asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
                  :: "r"(sdst), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar) : "memory");
 }
+
+// Host: the tensor map of B for the TMA stores (3-D: M / 4 words, K rows,
+// batch generations; box 32 W words x kTmKB rows x 1).
+static inline bool tm_make_map_b(CUtensorMap *map, void *B, uint64_t batch, uint64_t K, uint64_t M, int W = 2);
 
 // Host: the driver's tensor-map encoder, resolved once by gf_init (no driver
 // call on the launch path but the encode itself, which is host-only work).
@@ -217,6 +241,19 @@ static inline bool tm_make_map(CUtensorMap *map, const void *A, uint64_t rows, u
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+static inline bool tm_make_map_b(CUtensorMap *map, void *B, uint64_t batch, uint64_t K, uint64_t M, int W)
+{
+    const PFN_cuTensorMapEncodeTiled_v12000 fn = __atomic_load_n(&tm_encode_fn(), __ATOMIC_ACQUIRE);
+    if (!fn) return false;
+    const cuuint64_t dims[3] = {M / 4, K, batch};
+    const cuuint64_t strides[2] = {M, K * M};
+    const cuuint32_t box[3] = {(cuuint32_t)tm_span_words(W), (cuuint32_t)kTmKB, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, B, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+           CUDA_SUCCESS;
+}
+
 __device__ __forceinline__ void tm_expect_tx(uint32_t bar, uint32_t bytes)
 {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
@@ -234,7 +271,8 @@ __device__ __forceinline__ void tm_expect_tx(uint32_t bar, uint32_t bytes)
 // mismatch[g].  FT: the harness fault injection (gf_set_verify_fault), a
 // separate instantiation.
 template <int LOGW, int WPC, int T = 0, bool FT = false, int W = 2>
-__global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, const __grid_constant__ CUtensorMap tmA)
+__global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, const __grid_constant__ CUtensorMap tmA,
+                                                                  const __grid_constant__ CUtensorMap tmB)
 {
     constexpr int w = 1 << LOGW;
     constexpr int SPS = tm_sps(LOGW);
@@ -263,7 +301,8 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, co
     uint8_t *wbase = smem8 + (size_t)wid * tm_warp_bytes(LOGW, NG, passes, T, W);
     uint32_t *tab = reinterpret_cast<uint32_t *>(wbase);
     uint32_t *tabu = reinterpret_cast<uint32_t *>(wbase + tabb);               // [NG][T]
-    const uint32_t *ring = reinterpret_cast<const uint32_t *>(wbase + tabb + tm_tabu_bytes(NG, T));
+    const uint32_t stg_s = (uint32_t)__cvta_generic_to_shared(wbase + tabb + tm_tabu_bytes(NG, T));   // [kTmKB][SW]
+    const uint32_t *ring = reinterpret_cast<const uint32_t *>(wbase + tabb + tm_tabu_bytes(NG, T) + tm_stage_bytes(LOGW, W));
     const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
     const uint32_t bar_s = ring_s + kTmRing * SPS * SW * 4;
     if (lane < kTmRing) mbar_init(bar_s + 8 * lane, 1);
@@ -500,7 +539,30 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, co
                         }
                 }
             }
-            if (wi < Mw) {                           // row k of the pass: one pointer step of Mw words
+            if constexpr (tm_tma_store_on(LOGW)) {
+                // the pass's 32 coded rows of the span leave through one TMA store:
+                // stage them (lane l: words W l ..), make the writes visible to the
+                // async proxy, lane 0 issues the store (rows past K and words past
+                // M are clipped).  The staging tile is rewritten only after the
+                // previous store has read it.
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                __syncwarp();
+#pragma unroll
+                for (int k = 0; k < kTmKB; k++) {
+                    const uint32_t a = stg_s + (uint32_t)(k * SW + W * lane) * 4u;
+                    if constexpr (W == 2)
+                        asm volatile("st.shared.v2.u32 [%0], {%1,%2};" :: "r"(a), "r"(acc[k][0]), "r"(acc[k][1]) : "memory");
+                    else
+                        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" :: "r"(a), "r"(acc[k][0]), "r"(acc[k][1]),
+                                     "r"(acc[k][2]), "r"(acc[k][3]) : "memory");
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                    tm_tma_store(&tmB, cc.sp * (uint32_t)SW, (uint32_t)(pass * kTmKB), (uint32_t)g, stg_s);
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+            } else if (wi < Mw) {                    // row k of the pass: one pointer step of Mw words
                 uint32_t *q = Bg;
 #pragma unroll
                 for (int k = 0; k < kTmKB; k++) {
@@ -538,6 +600,8 @@ __global__ void __launch_bounds__(WPC * 32, 1) encode_tmem_kernel(TmParams p, co
         bad = __reduce_add_sync(0xffffffffu, bad);
         if (lane == 0 && bad && cur_g != ~0ull) atomicAdd(p.mismatch + cur_g, (unsigned long long)bad);
     }
+    if constexpr (tm_tma_store_on(LOGW))
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // the last TMA stores
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");

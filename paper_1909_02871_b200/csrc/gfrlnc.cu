@@ -541,8 +541,10 @@ static int launch_tmem_w(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, 
         const uint64_t blocks = (p.units + WPC * p.upw - 1) / (WPC * p.upw);
         const size_t smem = tm_smem_w(LOGW, N, K, WPC, T);
         CUtensorMap map;
-        if (!tm_make_map(&map, p.A, (uint64_t)nb * N, M, LOGW)) return GF_ECUDA;
-        encode_tmem_kernel<LOGW, WPC, T, FT><<<(unsigned)blocks, WPC * 32, smem, st>>>(p, map);
+        CUtensorMap mapb;
+        if (!tm_make_map(&map, p.A, (uint64_t)nb * N, M, LOGW) || !tm_make_map_b(&mapb, p.B, nb, K, M))
+            return GF_ECUDA;
+        encode_tmem_kernel<LOGW, WPC, T, FT><<<(unsigned)blocks, WPC * 32, smem, st>>>(p, map, mapb);
         const int rc = launch_status();
         if (rc != GF_OK) return rc;
     }

@@ -75,8 +75,10 @@ static void run(int N, int K, size_t M, size_t G, int reps)
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int blocks = (int)((p.units + (uint64_t)WPC * p.upw - 1) / ((uint64_t)WPC * p.upw));
     CUtensorMap map;
-    if (!tm_resolve_encoder() || !tm_make_map(&map, A, (uint64_t)G * N, M, LOGW, W)) { printf("tensor map failed\n"); exit(1); }
-    kern<<<blocks, WPC * 32, smem>>>(p, map);
+    CUtensorMap mapb;
+    if (!tm_resolve_encoder() || !tm_make_map(&map, A, (uint64_t)G * N, M, LOGW, W) ||
+        !tm_make_map_b(&mapb, B, G, K, M, W)) { printf("tensor map failed\n"); exit(1); }
+    kern<<<blocks, WPC * 32, smem>>>(p, map, mapb);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("GF(%d) launch error %s (smem %zu)\n", q, cudaGetErrorString(e), smem); exit(1); }
     // spot check: sampled (g, k, m)
@@ -102,7 +104,7 @@ static void run(int N, int K, size_t M, size_t G, int reps)
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    for (int r = 0; r < reps; r++) kern<<<blocks, WPC * 32, smem>>>(p, map);
+    for (int r = 0; r < reps; r++) kern<<<blocks, WPC * 32, smem>>>(p, map, mapb);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms = 0;
