@@ -20,8 +20,8 @@
 //   GF(256): 2 groups per source (x^0..3 a, x^4..7 a), idx = low / high nibble
 // A warp-uniform index is what TMEM serves: tcgen05.ld reads one column (a
 // uniform address) for all 32 lanes of the warp's lane quarter, on the tensor
-// memory datapath beside the shared-memory pipe (~200-270 B/clk
-// per SM from ordinary warps, tools/ubench_tmem.cu).
+// memory datapath beside the shared-memory pipe (.x2 loads
+// ~130 B/clk per SM from ordinary warps, tools/ubench_tmem2.cu).
 //
 // Layout (W = 2 words per lane, the instantiated width): warp wid owns TMEM
 // lanes 32 (wid % 4) .. +31 and 128 columns (4 groups x 16 combos x 2 words).
@@ -39,8 +39,10 @@
 // warp and generation in shared memory and read with broadcast LDS.128.
 // Source words stream through a per-warp ring of kTmRing steps: one lane
 // issues one TMA tile load per step (2-D tensor map over A viewed as
-// [batch N rows][M bytes], box SPS rows x 256 bytes), completing on the
-// stage's mbarrier; rows and bytes past the end of A are zero-filled.
+// [batch N rows][M / 4 words], box SPS rows x 32 W words), completing on the
+// stage's mbarrier; rows and words past the end of A are zero-filled.  B
+// leaves per (unit, pass) through a staging tile and one 3-D TMA tile store
+// (GF(4) / GF(16) / GF(256)) or 8-byte stores (GF(2)); see tm_tma_store_on.
 // HBM traffic is the algorithmic N*M + K*M (+ N*K) per generation (each
 // pass > 0 re-reads the span's sources, from L2).
 //
