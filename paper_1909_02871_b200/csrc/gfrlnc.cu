@@ -505,7 +505,7 @@ static int tm_pick_wpc(int logw, int N, int K)
 
 static bool tmem_ok(int field, int N, int K, size_t M, const void *A, const void *B)
 {
-    return M % 16 == 0 && M / 4 < 0xFFFFFFFFull && N * K > 0 &&
+    return M % 16 == 0 && M / 4 < 0xFFFFFFFFull && N > 0 && K > 0 &&
            ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15u) == 0 &&
            tm_pick_wpc(log2_field(field), N, K) > 0;
 }
