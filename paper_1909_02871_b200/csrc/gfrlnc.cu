@@ -475,15 +475,16 @@ static int launch_gf2(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int
 
 // TMEM lookup-table engine (encode_tmem.cuh): 4-bit groups of the basis words
 // x^j a_i, their 16 XOR-subsets in tensor memory, one lookup per (group, k).
-// Warps per CTA: 12 for GF(4) (C5: 1.85 TB/s against 1.46 at 16 -- register
-// spills at 128 per thread -- and 1.66 at 8), 8 otherwise (GF(2) C5: 2.81
-// TB/s against 2.69 at 12; tools/exp_tmem.cu, profiles/r02_exp_tmem_v7.txt);
-// tm_wpc2 when the per-warp shared memory (coefficient-address table +
-// source ring) does not fit.
+// Warps per CTA: 8 for GF(2) (C5: 2.81 TB/s against 2.69 at 12), 12 for the
+// other fields (GF(4) C5: 1.85 TB/s against 1.46 at 16 -- register spills at
+// 128 per thread -- and 1.66 at 8; GF(16), N = K = 32: 1.03 against 0.90 at
+// 8; tools/exp_tmem.cu, profiles/r02_exp_tmem_v7.txt, r02_exp_tmem_v13.txt);
+// tm_wpc2 when the per-warp shared memory (coefficient-address table,
+// staging tile, source ring) does not fit.
 template <int LOGW>
-constexpr int tm_wpc() { return LOGW == 1 ? 12 : 8; }
+constexpr int tm_wpc() { return LOGW == 0 ? 8 : 12; }
 template <int LOGW>
-constexpr int tm_wpc2() { return LOGW == 1 ? 8 : 4; }
+constexpr int tm_wpc2() { return LOGW == 0 ? 4 : 8; }
 
 static int tm_groups(int logw, int N) { return ((((N << logw) + 3) / 4) + kTmGPB - 1) / kTmGPB * kTmGPB; }
 
@@ -497,7 +498,7 @@ static constexpr int log2_field(int field) { return field == 2 ? 0 : field == 4 
 // warps per CTA for this shape: the preferred count or half of it, 0 if neither fits
 static int tm_pick_wpc(int logw, int N, int K)
 {
-    const int w0 = logw == 1 ? tm_wpc<1>() : tm_wpc<0>(), w1 = logw == 1 ? tm_wpc2<1>() : tm_wpc2<0>();
+    const int w0 = logw == 0 ? tm_wpc<0>() : tm_wpc<1>(), w1 = logw == 0 ? tm_wpc2<0>() : tm_wpc2<1>();
     if (tm_smem_w(logw, N, K, w0) <= 226 * 1024) return w0;
     if (tm_smem_w(logw, N, K, w1) <= 226 * 1024) return w1;
     return 0;
@@ -562,14 +563,13 @@ static int launch_tmem(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, in
     return GF_EARG;
 }
 
-// the TMEM engine with the check fused (GF(2) / GF(4) / GF(16), K <= 64): 12
-// warps per CTA for GF(4), 8 otherwise; 8 / 4 when the per-warp shared memory
-// does not fit
+// the TMEM engine with the check fused (GF(2) / GF(4) / GF(16), K <= 64): the
+// encode's warps per CTA (tm_wpc, tm_wpc2 when the shared memory does not fit)
 template <int LOGW, int T>
 static int launch_tmem_check(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, int K, size_t M, size_t batch,
                              cudaStream_t st, const TmParams *vp)
 {
-    constexpr int W0 = LOGW == 1 ? 12 : 8, W1 = LOGW == 1 ? 8 : 4;
+    constexpr int W0 = tm_wpc<LOGW>(), W1 = tm_wpc2<LOGW>();
     const bool ft = (vp->fault >> 63) != 0;
     if (tm_smem_w(LOGW, N, K, W0, T) <= 226 * 1024)
         return ft ? launch_tmem_w<LOGW, W0, T, true>(A, C, B, N, K, M, batch, st, vp)
@@ -847,7 +847,7 @@ static int configure_field(int optin, uint32_t smem_base)
     if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<log2_field(F), tm_wpc<log2_field(F)>()>, optin);
     if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<log2_field(F), tm_wpc2<log2_field(F)>()>, optin);
     if constexpr (F <= 16) {
-        constexpr int L = log2_field(F), W0 = L == 1 ? 12 : 8, W1 = L == 1 ? 8 : 4;
+        constexpr int L = log2_field(F), W0 = tm_wpc<L>(), W1 = tm_wpc2<L>();
         if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<L, W0, 1>, optin);
         if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<L, W0, 2>, optin);
         if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<L, W0, 1, true>, optin);
