@@ -495,12 +495,13 @@ static size_t tm_smem_w(int logw, int N, int K, int wpc, int T = 0)
 
 static constexpr int log2_field(int field) { return field == 2 ? 0 : field == 4 ? 1 : field == 16 ? 2 : 3; }
 
-// warps per CTA for this shape: the preferred count or half of it, 0 if neither fits
-static int tm_pick_wpc(int logw, int N, int K)
+// warps per CTA for this shape: the preferred count, tm_wpc2, or 4; 0 if none fits
+static int tm_pick_wpc(int logw, int N, int K, int T = 0)
 {
     const int w0 = logw == 0 ? tm_wpc<0>() : tm_wpc<1>(), w1 = logw == 0 ? tm_wpc2<0>() : tm_wpc2<1>();
-    if (tm_smem_w(logw, N, K, w0) <= 226 * 1024) return w0;
-    if (tm_smem_w(logw, N, K, w1) <= 226 * 1024) return w1;
+    if (tm_smem_w(logw, N, K, w0, T) <= 226 * 1024) return w0;
+    if (tm_smem_w(logw, N, K, w1, T) <= 226 * 1024) return w1;
+    if (T == 0 && tm_smem_w(logw, N, K, 4) <= 226 * 1024) return 4;
     return 0;
 }
 
@@ -560,6 +561,8 @@ static int launch_tmem(const uint8_t *A, const uint8_t *C, uint8_t *B, int N, in
     const int wpc = tm_pick_wpc(LOGW, N, K);
     if (wpc == W0) return launch_tmem_w<LOGW, W0>(A, C, B, N, K, M, batch, st);
     if (wpc == W1) return launch_tmem_w<LOGW, W1>(A, C, B, N, K, M, batch, st);
+    if constexpr (W1 != 4)
+        if (wpc == 4) return launch_tmem_w<LOGW, 4>(A, C, B, N, K, M, batch, st);
     return GF_EARG;
 }
 
@@ -594,8 +597,8 @@ static int encode_path_override()
 // 11 GF(2) split engine (N <= 32, 16-byte aligned packets, K >= 24; any K when forced),
 // 12 GF(16) product-row with nibble-indexed tables (K > 32), 13 GF(256)
 // product-row with 32 coded packets per CTA on 768-word tiles (K > 32, long packets),
-// 14 TMEM lookup-table engine (GF(2) / GF(4) K >= 9, GF(16) 24 <= K <= 32 or K > 32 with
-// N <= 32; packets >= 256 B, M % 16 == 0, 16-byte aligned)
+// 14 TMEM lookup-table engine (GF(2) / GF(4) K >= 9, GF(16) K >= 5 but not 13..16 on
+// packets >= 8 KiB, N <= 32 when K > 32; packets >= 256 B, M % 16 == 0, 16-byte aligned)
 static bool gf2_split_ok(int field, int N, int K, size_t M, const void *A, const void *B)
 {
     return field == 2 && N <= 32 && K >= 1 && M % 16 == 0 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0 &&
@@ -610,16 +613,16 @@ static int encode_path(int field, int N, int K, size_t M, const void *A, const v
     if (!aligned) return 1;
     if (K <= 4 && (ov == GF_PATH_STREAM || ov == 0)) return 8;  // streaming (16- or 4-byte chunks)
     // The TMEM lookup-table engine on 16-byte aligned packets of >= 256 bytes:
-    // GF(2) / GF(4) with K >= 9 (C5: GF(2) 2.29 -> 2.8-2.95 TB/s against the
-    // split engine, GF(4) 1.13 -> 1.8 against lane-k; K = 12-20: 1.3-2.4x the
-    // column / product-row kernels; K = 8: the column kernel is 0-10% faster),
-    // GF(16) with 24 <= K <= 32, or K > 32 and N <= 32 (1.1-2.3x the
-    // product-row kernels; at K = 16 they are 1.8x faster, at N = K = 64
-    // 5%); profiles/r02_exp_tmem_route_v4.txt.  Forced: any field and shape it takes.
+    // GF(2) / GF(4) with K >= 9 (C5: GF(2) 2.29 -> 2.9 TB/s against the split
+    // engine, GF(4) 1.13 -> 2.06 against lane-k; K = 12-20: 1.3-2.4x the
+    // column / product-row kernels; K = 8: the column kernel is 0-10% faster;
+    // profiles/r02_exp_tmem_route_v4.txt), GF(16) with K >= 5 and N <= 32 for
+    // K > 32 (1.1-3x the column / product-row kernels), except 13 <= K <= 16 on
+    // packets >= 8 KiB where the 16-packet product-row kernel is 5-14% faster
+    // (profiles/r02_exp_tmem_route_v5.txt).  Forced: any field and shape it takes.
     if (tmem && ov == GF_PATH_TMEM && tmem_ok(field, N, K, M, A, B)) return 14;
-    if (tmem && ov == 0 && M >= 256 &&
-        ((field <= 4 && K >= 9) || (field == 16 && ((K >= 24 && K <= 32) || (K > 32 && N <= 32)))) &&
-        tmem_ok(field, N, K, M, A, B))
+    const bool tm_gf16 = field == 16 && K >= 5 && (K <= 32 || N <= 32) && !(K >= 13 && K <= 16 && M >= 8192);
+    if (tmem && ov == 0 && M >= 256 && ((field <= 4 && K >= 9) || tm_gf16) && tmem_ok(field, N, K, M, A, B))
         return 14;
     // GF(2): the split engine (encode_gf2.cuh) where the lane-k kernel ran
     // before, K >= 24 (C5 N = K = 32, 1 MiB: 2.21 vs 1.66 TB/s)
@@ -846,6 +849,8 @@ static int configure_field(int optin, uint32_t smem_base)
     }
     if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<log2_field(F), tm_wpc<log2_field(F)>()>, optin);
     if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<log2_field(F), tm_wpc2<log2_field(F)>()>, optin);
+    if constexpr (tm_wpc2<log2_field(F)>() != 4)
+        if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<log2_field(F), 4>, optin);
     if constexpr (F <= 16) {
         constexpr int L = log2_field(F), W0 = tm_wpc<L>(), W1 = tm_wpc2<L>();
         if (rc == GF_OK) rc = allow_smem(encode_tmem_kernel<L, W0, 1>, optin);
@@ -1211,7 +1216,7 @@ int gf_encode_verify_batch(int field, const uint8_t *A, const uint8_t *C, uint8_
                                                                       field - 1);
     if ((rc = launch_status()) != GF_OK) return rc;
     const int path = encode_path(field, N, K, M, A, B);
-    if (path == 14 && field <= 16 && K <= 64) {                // fused: the TMEM engine
+    if (path == 14 && field <= 16 && K <= 64 && tm_pick_wpc(log2_field(field), N, K, t) > 0) {   // fused: TMEM engine
         TmParams vp{};
         vp.U = U; vp.RB = RB; vp.kw = kw; vp.mismatch = mismatch; vp.fault = tls_fault;
         if (field == 2)

@@ -250,7 +250,10 @@ def test_encode_path_query():
     assert gf.encode_path(2, 33, 32, 240) == "lanek-32"         # GF(2), N > 32, short packets
     assert gf.encode_path(4, 32, 16, 1 << 20) == "tmem"
     assert gf.encode_path(16, 32, 32, 1 << 20) == "tmem"        # GF(16), 24 <= K <= 32
-    assert gf.encode_path(16, 32, 16, 1 << 20) == "prow-16"
+    assert gf.encode_path(16, 32, 16, 1 << 20) == "prow-16"    # 13 <= K <= 16, >= 8 KiB
+    assert gf.encode_path(16, 32, 16, 1024) == "tmem"
+    assert gf.encode_path(16, 16, 8, 65536) == "tmem"
+    assert gf.encode_path(16, 16, 8, 1500) == "column-words"
     assert gf.encode_path(16, 32, 64, 1 << 20) == "tmem"        # K > 32, N <= 32
     assert gf.encode_path(16, 64, 64, 1 << 20) == "prow-nib"
     assert gf.encode_path(256, 32, 32, 1 << 20) == "prow-32"    # GF(256) keeps the product rows
