@@ -206,7 +206,7 @@ int gf_host_tables(int field, uint32_t *out, size_t cap_words);
  * 12 = GF(16) product-row kernel with nibble-indexed tables (K > 32: C3 GF(16)),
  * 13 = GF(256) product-row kernel with 32 coded packets per CTA on 768-word
  * tiles (K > 32, packets of >= 6144 words tiled >= 90%: C4)
- * 14 = TMEM lookup-table engine (GF(2) / GF(4) with K >= 9, GF(16) with
+ * 14 = TMEM lookup-table engine (GF(2) with K >= 9, GF(4) with K >= 5, GF(16) with
  * K >= 5 -- N <= 32 when K > 32, not 13 <= K <= 16 on packets >= 8 KiB;
  * M >= 256, M % 16 == 0, 16-byte aligned A and B: C5)
  * (DESIGN.md section 6), or GF_EFIELD / GF_EARG. */

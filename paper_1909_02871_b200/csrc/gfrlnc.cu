@@ -597,7 +597,7 @@ static int encode_path_override()
 // 11 GF(2) split engine (N <= 32, 16-byte aligned packets, K >= 24; any K when forced),
 // 12 GF(16) product-row with nibble-indexed tables (K > 32), 13 GF(256)
 // product-row with 32 coded packets per CTA on 768-word tiles (K > 32, long packets),
-// 14 TMEM lookup-table engine (GF(2) / GF(4) K >= 9, GF(16) K >= 5 but not 13..16 on
+// 14 TMEM lookup-table engine (GF(2) K >= 9, GF(4) K >= 5, GF(16) K >= 5 but not 13..16 on
 // packets >= 8 KiB, N <= 32 when K > 32; packets >= 256 B, M % 16 == 0, 16-byte aligned)
 static bool gf2_split_ok(int field, int N, int K, size_t M, const void *A, const void *B)
 {
@@ -613,16 +613,17 @@ static int encode_path(int field, int N, int K, size_t M, const void *A, const v
     if (!aligned) return 1;
     if (K <= 4 && (ov == GF_PATH_STREAM || ov == 0)) return 8;  // streaming (16- or 4-byte chunks)
     // The TMEM lookup-table engine on 16-byte aligned packets of >= 256 bytes:
-    // GF(2) / GF(4) with K >= 9 (C5: GF(2) 2.29 -> 2.9 TB/s against the split
-    // engine, GF(4) 1.13 -> 2.06 against lane-k; K = 12-20: 1.3-2.4x the
-    // column / product-row kernels; K = 8: the column kernel is 0-10% faster;
-    // profiles/r02_exp_tmem_route_v4.txt), GF(16) with K >= 5 and N <= 32 for
+    // GF(2) with K >= 9 and GF(4) with K >= 5 (C5: GF(2) 2.29 -> 2.9 TB/s
+    // against the split engine, GF(4) 1.13 -> 2.06 against lane-k; K = 5-20:
+    // 1.3-2.4x the column / product-row kernels; GF(2) K <= 8: the column
+    // kernel is 0-10% faster; profiles/r02_exp_tmem_route_v6.txt), GF(16) with K >= 5 and N <= 32 for
     // K > 32 (1.1-3x the column / product-row kernels), except 13 <= K <= 16 on
     // packets >= 8 KiB where the 16-packet product-row kernel is 5-14% faster
     // (profiles/r02_exp_tmem_route_v5.txt).  Forced: any field and shape it takes.
     if (tmem && ov == GF_PATH_TMEM && tmem_ok(field, N, K, M, A, B)) return 14;
     const bool tm_gf16 = field == 16 && K >= 5 && (K <= 32 || N <= 32) && !(K >= 13 && K <= 16 && M >= 8192);
-    if (tmem && ov == 0 && M >= 256 && ((field <= 4 && K >= 9) || tm_gf16) && tmem_ok(field, N, K, M, A, B))
+    if (tmem && ov == 0 && M >= 256 && ((field == 2 && K >= 9) || (field == 4 && K >= 5) || tm_gf16) &&
+        tmem_ok(field, N, K, M, A, B))
         return 14;
     // GF(2): the split engine (encode_gf2.cuh) where the lane-k kernel ran
     // before, K >= 24 (C5 N = K = 32, 1 MiB: 2.21 vs 1.66 TB/s)
