@@ -37,6 +37,20 @@ def test_roofline_gf2_split_is_hbm_with_issue_beside():
     assert 0 < r["issue_frac"] < 1
 
 
+def test_roofline_tmem_is_hbm_with_tmem_reads_beside():
+    """TMEM engine (C5): HBM-bound view, TMEM bytes = one 8-byte .x2 load per
+    lane per (4-bit group, coded packet of the 32-packet passes, 64-word span)."""
+    r, h = bench.dominant_roofline(4, 32, 32, 1 << 20, 256, "tmem", 0.0042, PEAKS)
+    assert r["bound"] == "hbm" and r["frac"] == h["frac"]
+    spans = (1 << 18) // 64
+    assert r["tmem_read_bytes_per_launch"] == 256 * spans * 32 * 16 * 32 * 8    # 16 groups of {a, xa, b, xb}
+    r2, _ = bench.dominant_roofline(2, 32, 32, 1 << 20, 256, "tmem", 0.003, PEAKS)
+    assert r2["tmem_read_bytes_per_launch"] == 256 * spans * 32 * 8 * 32 * 8     # 8 groups of 4 sources
+    r3, _ = bench.dominant_roofline(16, 17, 40, 4096, 3, "tmem", 1e-4, PEAKS)
+    assert r3["tmem_read_bytes_per_launch"] == 3 * 16 * 32 * 20 * 64 * 8         # 17 groups -> 20, K -> 64
+    assert 0 < r["tmem_read_frac"] < 1.5
+
+
 def test_rank_shard_splits_the_baseline_job():
     for ws in (1, 2, 4, 8):
         parts = [bench.rank_shard(shard, si.C3, ws, r)[0] for r in range(ws)]
