@@ -97,3 +97,34 @@ def test_inversion_deterministic_under_perturbation(gfm, q, N):
         assert torch.equal(r, r0) and torch.equal(D[r0 == N], D0[r0 == N])
     Ch = si.uniform_coeffs(q, 51 + N, si.STREAM_C, 0, 16 * N * N).reshape(16, N, N)
     assert all(oracle.rank(q, Ch[g]) == int(r0[g]) for g in range(16))
+
+
+@pytest.mark.timeout(300)
+def test_tmem_engine_concurrent_streams(gfm):
+    """Two TMEM-engine encodes (GF(2) and GF(4), different warps per CTA and
+    TMEM allocations) issued back to back on two streams, several times: the
+    CTAs may share SMs and must each obtain their tensor-memory columns; every
+    output equals the oracle on sampled generations."""
+    shapes = [(2, 16, 24, 8192, 64), (4, 8, 12, 4096, 128)]
+    jobs = []
+    for i, (q, N, K, M, G) in enumerate(shapes):
+        assert gfm.encode_path(q, N, K, M) == "tmem"
+        A = torch.empty((G, N, M), dtype=torch.uint8, device="cuda")
+        C = torch.empty((G, N, K), dtype=torch.uint8, device="cuda")
+        gfm.fill_random(A, 70 + i, si.STREAM_A, 0)
+        gfm.fill_random(C, 70 + i, si.STREAM_C, 0, mask=q - 1)
+        jobs.append((q, N, K, M, G, A, C, torch.cuda.Stream()))
+    torch.cuda.synchronize()
+    outs = [[] for _ in jobs]
+    for _ in range(6):
+        for j, (q, N, K, M, G, A, C, s) in enumerate(jobs):
+            with torch.cuda.stream(s):
+                outs[j].append(gfm.encode_batch(q, A, C))
+    torch.cuda.synchronize()
+    for j, (q, N, K, M, G, A, C, s) in enumerate(jobs):
+        for o in outs[j][1:]:
+            assert torch.equal(o, outs[j][0])
+        for g in (0, G // 2, G - 1):
+            Ah = si.random_bytes(70 + j, si.STREAM_A, g * N * M, N * M).reshape(1, N, M)
+            Ch = si.uniform_coeffs(q, 70 + j, si.STREAM_C, g * N * K, N * K).reshape(1, N, K)
+            assert np.array_equal(outs[j][0][g].cpu().numpy(), oracle.encode_batch(q, Ah, Ch)[0]), (q, g)
