@@ -37,15 +37,18 @@ def test_roofline_gf2_split_is_hbm_with_issue_beside():
     assert 0 < r["issue_frac"] < 1
 
 
-def test_roofline_tmem_is_hbm_with_tmem_reads_beside():
-    """TMEM engine (C5): HBM-bound view, TMEM bytes = one 8-byte .x2 load per
-    lane per (4-bit group, coded packet of the 32-packet passes, 64-word span)."""
+def test_roofline_tmem_reports_the_larger_of_tmem_reads_and_hbm():
+    """TMEM engine (C5): TMEM bytes = one 8-byte .x2 load per lane per (4-bit
+    group, coded packet of the 32-packet passes, 64-word span) against the
+    measured .x2 rate; the bound is the larger fraction (GF(4): TMEM reads,
+    GF(2): HBM), both stay on the line."""
     r, h = bench.dominant_roofline(4, 32, 32, 1 << 20, 256, "tmem", 0.0042, PEAKS)
-    assert r["bound"] == "hbm" and r["frac"] == h["frac"]
+    assert r["bound"] == "tmem" and r["frac"] > h["frac"] and r["tmem_read_frac"] == r["frac"]
     spans = (1 << 18) // 64
     assert r["tmem_read_bytes_per_launch"] == 256 * spans * 32 * 16 * 32 * 8    # 16 groups of {a, xa, b, xb}
-    r2, _ = bench.dominant_roofline(2, 32, 32, 1 << 20, 256, "tmem", 0.003, PEAKS)
+    r2, h2 = bench.dominant_roofline(2, 32, 32, 1 << 20, 256, "tmem", 0.003, PEAKS)
     assert r2["tmem_read_bytes_per_launch"] == 256 * spans * 32 * 8 * 32 * 8     # 8 groups of 4 sources
+    assert r2["bound"] == "hbm" and r2["frac"] == h2["frac"] and r2["tmem_read_frac"] < r2["frac"]
     r3, _ = bench.dominant_roofline(16, 17, 40, 4096, 3, "tmem", 1e-4, PEAKS)
     assert r3["tmem_read_bytes_per_launch"] == 3 * 16 * 32 * 20 * 64 * 8         # 17 groups -> 20, K -> 64
     assert 0 < r["tmem_read_frac"] < 1.5
